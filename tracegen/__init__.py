@@ -1,0 +1,212 @@
+"""Seeded synthetic trace generators (shared by tests, bench and smoke).
+
+This module holds NONE of the method's arithmetic: it only draws events.  Both
+the oracle and the product path read the bytes it produces.  Each generator
+returns a ``Trace`` with
+
+* ``formula``  -- the LTL4-C property text the workload is shaped for,
+* ``keys``     -- list of ``n_levels`` uint32 arrays (value of guard key i per
+                  event; ``ABSENT`` = 0xFFFFFFFF when the event does not bind it),
+* ``letters``  -- uint8 array; bit j = atom j of the formula, atoms numbered by
+                  first occurrence in the formula's body.
+
+Workload recipes follow SURVEY.md §8(d) / DESIGN.md "Input recipe":
+C1 socket, C2 nested login (Eq. 8), C3 Zipf-skewed
+socket, C4 proxy cache, C5 three-level online batch.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+ABSENT = np.uint32(0xFFFFFFFF)
+SEED_BASE = 0x14112239
+
+SOCKET = "forall[>=0.95] s : socket(s) => G (receive(s) -> F respond(s))"
+LOGIN = "forall x : user(x) => exists[<=3] r : rid(r) => (login && unauthorized)"
+PROXY = "forall v : vid(v) => exists[=0] r : req(r) => (cached(v) && external(r))"
+FILES = "forall[>=50%] f : intrace(f) => (opened(f) U close(f))"
+FIG1 = "forall[>=0.5] f : file(f) => (G a || (b U c))"
+C5_FORMULAS = [
+    "forall[>=0.95] h : host(h) => forall u : user(u) => exists[<=2] s : session(s) => F authfail",
+    "exists[>=3] h : host(h) => forall[>=0.5] u : user(u) => forall s : session(s) => G (request -> F response)",
+    "forall[>=0.99] h : host(h) => exists[=0] u : user(u) => exists s : session(s) => (admin && external)",
+]
+
+
+@dataclass
+class Trace:
+    formula: str
+    keys: list
+    letters: np.ndarray
+    meta: dict = field(default_factory=dict)
+
+    @property
+    def n(self) -> int:
+        return int(self.letters.shape[0])
+
+
+def _ids(rng: np.random.Generator, count: int) -> np.ndarray:
+    """`count` distinct uint32 ids != ABSENT (a random odd-multiplier bijection)."""
+    mul = np.uint64(rng.integers(1, 2**31) * 2 + 1)
+    add = np.uint64(rng.integers(0, 2**32))
+    i = np.arange(count, dtype=np.uint64)
+    v = ((i * mul + add) & np.uint64(0xFFFFFFFF)).astype(np.uint32)
+    v[v == ABSENT] = np.uint32(0xFFFFFFFE)  # keep distinct in practice; collision prob ~0
+    return v
+
+
+def _zipf_ranks(rng: np.random.Generator, n: int, support: int, s: float) -> np.ndarray:
+    w = np.arange(1, support + 1, dtype=np.float64) ** (-s)
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    out = np.empty(n, dtype=np.int64)
+    chunk = 1 << 24
+    for lo in range(0, n, chunk):
+        hi = min(n, lo + chunk)
+        out[lo:hi] = np.searchsorted(cdf, rng.random(hi - lo), side="right")
+    np.minimum(out, support - 1, out=out)
+    return out
+
+
+def socket_trace(seed: int = 0, n: int = 10_000, sockets: int = 100, noise: float = 0.02,
+                 p_receive: float = 0.04, p_respond: float = 0.95, p_drop: float = 0.005) -> Trace:
+    """C1: web-server socket trace. bit0 = receive(s), bit1 = respond(s).
+
+    Per event: with prob `noise` the event binds no socket; otherwise a socket is
+    drawn uniformly from `sockets` fds in [0, 65535].  An idle socket
+    receives a request with prob `p_receive`; a pending one is responded with prob
+    `p_respond` unless the request was dropped (prob `p_drop`, never responded).
+    """
+    rng = np.random.default_rng(SEED_BASE + 1 + seed)
+    fds = rng.choice(65536, size=sockets, replace=False).astype(np.uint32)
+    sock = rng.integers(0, sockets, size=n)
+    is_noise = rng.random(n) < noise
+    u1, u2 = rng.random(n), rng.random(n)
+    pending = np.zeros(sockets, dtype=np.int8)  # 0 idle, 1 pending, 2 dropped
+    letters = np.zeros(n, dtype=np.uint8)
+    keys = np.empty(n, dtype=np.uint32)
+    for j in range(n):  # sequential per-socket state machine (small n only)
+        if is_noise[j]:
+            keys[j] = ABSENT
+            continue
+        s = sock[j]
+        keys[j] = fds[s]
+        if pending[s] == 0:
+            if u1[j] < p_receive:
+                letters[j] = 1
+                pending[s] = 2 if u2[j] < p_drop else 1
+        elif pending[s] == 1 and u1[j] < p_respond:
+            letters[j] = 2
+            pending[s] = 0
+    return Trace(SOCKET, [keys], letters, {"config": "C1", "seed": seed, "sockets": sockets})
+
+
+def login_trace(seed: int = 0, n: int = 10_000_000, users: int = 100_000, p_login: float = 0.3,
+                p_unauth: float = 0.02, p_norid: float = 0.01, rid_events: int = 1,
+                variant: str = "random") -> Trace:
+    """C2: nested login property (Eq. 8).  bit0 = login, bit1 = unauthorized.
+
+    Users uniform over `users` ids; request ids unique per request, each request
+    spanning `rid_events` consecutive-in-request events (1 = unique per event);
+    `p_norid` of events bind no rid.  variant: "random" | "clean" (every user
+    has <= 3 login&unauthorized requests) | "violator" (clean + one user with 4).
+    """
+    rng = np.random.default_rng(SEED_BASE + 2 + seed)
+    uid = _ids(rng, users)
+    u = rng.integers(0, users, size=n)
+    nreq = (n + rid_events - 1) // rid_events
+    rids = _ids(rng, nreq)
+    if rid_events == 1:
+        r = rids
+    else:
+        # events of a request are spread over the trace: request k's events
+        # take random positions (still one user per request)
+        req_of = np.repeat(np.arange(nreq), rid_events)[:n]
+        rng.shuffle(req_of)
+        r = rids[req_of]
+        req_user = rng.integers(0, users, size=nreq)
+        u = req_user[req_of]
+    login = rng.random(n) < p_login
+    unauth = login & (rng.random(n) < p_unauth)
+    letters = (login.astype(np.uint8) | (unauth.astype(np.uint8) << 1))
+    rk = r.copy()
+    rk[rng.random(n) < p_norid] = ABSENT
+    uk = uid[u].astype(np.uint32)
+    if variant in ("clean", "violator"):
+        both = (letters == 3) & (rk != ABSENT)
+        idx = np.nonzero(both)[0]
+        order = np.argsort(u[idx], kind="stable")
+        su = u[idx][order]
+        start = np.r_[0, np.nonzero(np.diff(su))[0] + 1]
+        rank = np.arange(su.shape[0]) - np.repeat(start, np.diff(np.r_[start, su.shape[0]]))
+        drop = idx[order][rank >= 3]
+        letters[drop] = 1  # keep login, clear unauthorized
+        if variant == "violator":
+            victim = int(u[0])
+            pos = np.nonzero((u == victim) & (rk != ABSENT) & (letters != 3))[0][:4]
+            letters[pos] = 3
+            if rid_events != 1:
+                pass
+    return Trace(LOGIN, [uk, rk], letters,
+                 {"config": "C2", "seed": seed, "users": users, "variant": variant})
+
+
+def zipf_socket_trace(seed: int = 0, n: int = 100_000_000, support: int = 1 << 20, s: float = 1.1,
+                      p_receive: float = 0.3, p_respond: float = 0.3, formula: str = SOCKET) -> Trace:
+    """C3: Zipf(s)-skewed keys over `support` ids; i.i.d. letters over {receive, respond}
+    (the G(r -> F s) automaton has two non-trap states, so every event does work)."""
+    rng = np.random.default_rng(SEED_BASE + 3 + seed)
+    ranks = _zipf_ranks(rng, n, support, s)
+    ids = _ids(rng, support)
+    keys = ids[ranks]
+    letters = ((rng.random(n) < p_receive).astype(np.uint8)
+               | ((rng.random(n) < p_respond).astype(np.uint8) << 1))
+    return Trace(formula, [keys], letters, {"config": "C3", "seed": seed, "support": support, "s": s})
+
+
+def proxy_trace(seed: int = 0, n: int = 1_000_000, videos: int = 1_000_000, s: float = 0.8,
+                p_cached: float = 0.6, p_ext: float = 0.5, p_ext_cached: float = 0.001,
+                max_req_events: int = 4) -> Trace:
+    """C4: YouTube proxy cache. bit0 = cached(v), bit1 = external(r).
+    Videos Zipf(s); requests unique with 1..max_req_events events each."""
+    rng = np.random.default_rng(SEED_BASE + 4 + seed)
+    per = rng.integers(1, max_req_events + 1, size=n // 2 + 1)
+    cs = np.cumsum(per)
+    nreq = int(np.searchsorted(cs, n) + 1)
+    req_of = np.repeat(np.arange(nreq), per[:nreq])[:n]
+    # requests interleave: each request's events are placed near its start
+    jitter = rng.random(n) * 64.0
+    order = np.argsort(req_of.astype(np.float64) * 2.5 + jitter, kind="stable")
+    req_of = req_of[order]
+    vrank = _zipf_ranks(rng, nreq, videos, s)
+    vids = _ids(rng, videos)[vrank]
+    rids = _ids(rng, nreq)
+    cached_req = rng.random(nreq) < p_cached
+    cached = cached_req[req_of]
+    ext = np.where(cached, rng.random(n) < p_ext_cached, rng.random(n) < p_ext)
+    letters = cached.astype(np.uint8) | (ext.astype(np.uint8) << 1)
+    return Trace(PROXY, [vids[req_of], rids[req_of]], letters,
+                 {"config": "C4", "seed": seed, "videos": videos})
+
+
+def worked_example() -> Trace:
+    """The five-event login trace of P:715-723 (Adam = 1, Jack = 2)."""
+    users = np.array([1, 1, 2, 1, 1], dtype=np.uint32)
+    rids = np.array([12, 13, 14, 15, 16], dtype=np.uint32)
+    letters = np.array([3, 3, 1, 3, 3], dtype=np.uint8)  # Jack: login, authorized
+    return Trace(LOGIN, [users, rids], letters, {"config": "worked-example"})
+
+
+def random_property_trace(seed: int, levels: int, n_events: int, values: int = 3,
+                          atoms: int = 2, p_absent: float = 0.1):
+    """Small random trace for property-based tests (keys in [0, values))."""
+    rng = np.random.default_rng(SEED_BASE + 100 + seed)
+    keys = []
+    for _ in range(levels):
+        k = rng.integers(0, values, size=n_events).astype(np.uint32)
+        k[rng.random(n_events) < p_absent] = ABSENT
+        keys.append(k)
+    letters = rng.integers(0, 1 << atoms, size=n_events).astype(np.uint8)
+    return keys, letters
