@@ -1,0 +1,195 @@
+/*
+ * ltl4c.h -- C ABI of the B200-native LTL4-C verifier (libltl4c.so).
+ *
+ * Method: Medhat, Joshi, Bonakdarpour, Fischmeister, "Accelerated Runtime
+ * Verification of LTL Specifications with Counting Semantics", arXiv:1411.2239.
+ * `P:n` = line n of the paper text.  Readings of ambiguous passages (A1..A20)
+ * are listed in DESIGN.md.
+ *
+ * Conventions for every entry point:
+ *   - all calls return ltl4c_status; nothing throws across the ABI;
+ *   - on a non-OK status, ltl4c_last_error() returns a thread-local message;
+ *   - "device pointer" = CUDA global memory on the state's device, owned by the
+ *     caller, read-only to the library, not retained after the call returns;
+ *   - programs are immutable and may be shared between threads; a state has a
+ *     single writer (calls on one state must not overlap).
+ */
+#ifndef LTL4C_H
+#define LTL4C_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTL4C_MAX_LEVELS 3      /* quantifier string length n (Eq. 5)        */
+#define LTL4C_MAX_ATOMS 8       /* atoms of psi; a letter is a u8 bitmask           */
+#define LTL4C_MAX_STATES 16     /* LTL4 monitor states (after minimisation/product) */
+#define LTL4C_MAX_FORMULAS 4    /* formulas verified together (ltl4c_compile_batch) */
+#define LTL4C_ABSENT 0xFFFFFFFFu /* key value meaning "the event does not bind it"  */
+
+typedef enum {
+  LTL4C_OK = 0,
+  LTL4C_E_SYNTAX = 1,        /* bad token or grammar violation (Def. 3)      */
+  LTL4C_E_NONCANONICAL = 2,  /* quantifier below a temporal/boolean operator    */
+  LTL4C_E_UNBOUND = 3,       /* predicate argument not bound by the quantifier prefix   */
+  LTL4C_E_RANGE = 4,         /* A constant outside [0,1] / >6 decimals, E constant < 0  */
+  LTL4C_E_BUDGET = 5,        /* > 3 levels, > 8 atoms, > 16 monitor states, n = 0       */
+  LTL4C_E_INVALID = 6,       /* null pointer, bad argument, non-contiguous online batch */
+  LTL4C_E_CUDA = 7,          /* CUDA runtime error (message in ltl4c_last_error)        */
+  LTL4C_E_NCCL = 8,          /* NCCL error                                              */
+  LTL4C_E_OOM = 9,           /* device allocation failed                                */
+  LTL4C_E_POISONED = 10      /* a previous verify failed mid-way; call ltl4c_state_reset */
+} ltl4c_status;
+
+/* six verdicts B6 in lattice order bottom < ... < top */
+typedef enum {
+  LTL4C_FALSE = 0,
+  LTL4C_CURRENTLY_FALSE = 1,
+  LTL4C_PRESUMABLY_FALSE = 2,
+  LTL4C_PRESUMABLY_TRUE = 3,
+  LTL4C_CURRENTLY_TRUE = 4,
+  LTL4C_TRUE = 5
+} ltl4c_verdict;
+
+typedef enum { LTL4C_QUANT_A = 0, LTL4C_QUANT_E = 1 } ltl4c_quant_kind; /* A: percentage, E: instance */
+typedef enum { LTL4C_LT = 0, LTL4C_LE = 1, LTL4C_GT = 2, LTL4C_GE = 3, LTL4C_EQ = 4 } ltl4c_cmp;
+
+typedef struct ltl4c_program ltl4c_program;
+typedef struct ltl4c_state ltl4c_state;
+
+/* One counting quantifier Q_i = <Q_i, ~_i, c_i, x_i, p_i> (Eq. 5).
+ * A: c = num/den, a reduced fraction in [0,1] (reading A5);  E: c = num, den = 1. */
+typedef struct {
+  int32_t kind; /* ltl4c_quant_kind */
+  int32_t cmp;  /* ltl4c_cmp        */
+  uint64_t num, den;
+  char key[64]; /* guard predicate p_i = the event key holding x_i's value */
+} ltl4c_quantifier;
+
+/* Read-only view of a compiled program (host memory owned by the program).
+ * delta[q * (1 << n_atoms) + a] is the LTL4 monitor transition (Def. 5)
+ * of the (product) automaton; label[f * n_states + q] is lambda_f(q) in B6 codes
+ * {0,2,3,5}; states with label 0/5 are traps. */
+typedef struct {
+  uint32_t n_formulas, n_levels, n_atoms, n_states, initial;
+  const uint8_t *delta;
+  const uint8_t *label;
+  const ltl4c_quantifier *quant; /* [n_formulas][n_levels] */
+  const char *const *atom_names; /* [n_atoms], bit j of a letter = atom j             */
+} ltl4c_tables;
+
+/* A trace batch u (Def. 2) in encoded form, n_events events.
+ * keys[i][j]  : value of guard key i (quantifier level i) in event j, or LTL4C_ABSENT;
+ *               an event binding every key has value vector D = (keys[0][j] ...
+ *               keys[n-1][j]) (epsilon; Eq. D); others bind no vector.
+ * letters[j]  : bit k set iff atom k of the program holds in event j.
+ * first_index : global index of event 0; for an online state it must equal the
+ *               previous batch's first_index + n_events (else LTL4C_E_INVALID).
+ * Pointers are device pointers for ltl4c_verify and host pointers for
+ * ltl4c_verify_host.  n_events may be 0 (pointers may then be NULL). */
+typedef struct {
+  uint64_t n_events;
+  uint64_t first_index;
+  const uint32_t *keys[LTL4C_MAX_LEVELS];
+  const uint8_t *letters;
+} ltl4c_batch;
+
+/* Result of Algorithm 1 after the batch, per formula.
+ * hist[l][v] = number of depth-l nodes of the submonitor tree (Fig. 2) with
+ * verdict v: l = 0 is the root (one-hot of `verdict`), l = n_levels the leaves
+ * (LTL4 submonitors, verdicts in {0,2,3,5}).  For an online state these are the
+ * values for the concatenation of all batches since create/reset. */
+typedef struct {
+  int32_t verdict; /* ltl4c_verdict of the root */
+  uint32_t n_levels;
+  uint64_t hist[LTL4C_MAX_LEVELS + 1][6];
+  uint64_t events_seen;  /* events consumed so far            */
+  uint64_t events_bound; /* of those, events binding every key */
+} ltl4c_result;
+
+/* Per-state counters for benchmarking (kernel launches and CUDA-event times of
+ * the library's kernels, accumulated while profiling is enabled). */
+#define LTL4C_MAX_KERNELS 16
+typedef struct {
+  uint64_t verifies;
+  uint64_t launches;                 /* kernels launched by the library */
+  uint32_t n_kernels;
+  char kernel_name[LTL4C_MAX_KERNELS][32];
+  uint64_t kernel_launches[LTL4C_MAX_KERNELS];
+  double kernel_ms[LTL4C_MAX_KERNELS]; /* sum of CUDA-event durations          */
+} ltl4c_stats;
+
+/* --- programs (host only) -------------------------------------------------- */
+
+/* Parse an LTL4-C property (Def. 3; grammar in DESIGN.md "Surface syntax") and
+ * synthesise its LTL4 monitor (Def. 5; construction in DESIGN.md "Compiler").
+ * Errors: E_SYNTAX, E_NONCANONICAL, E_UNBOUND, E_RANGE, E_BUDGET, E_INVALID. */
+ltl4c_status ltl4c_compile(const char *formula_utf8, ltl4c_program **out);
+
+/* F <= LTL4C_MAX_FORMULAS formulas with the same guard-key string, verified in
+ * one pass (reading A20).  Atoms are the union in order of first occurrence
+ * (formula 0's atoms first); the monitor is the minimised product automaton. */
+ltl4c_status ltl4c_compile_batch(const char *const *formulas_utf8, int n_formulas,
+                                 ltl4c_program **out);
+
+/* Fill *view with pointers into the program (valid until ltl4c_program_free). */
+ltl4c_status ltl4c_program_tables(const ltl4c_program *prog, ltl4c_tables *view);
+
+void ltl4c_program_free(ltl4c_program *prog);
+
+/* --- states (device) ------------------------------------------------------- */
+
+#define LTL4C_STATE_ONLINE 1u /* carry the submonitor tree across verify calls */
+
+/* Create a verification state on CUDA device `device`.  capacity_hint: expected
+ * events per batch (buffers grow on demand).  flags: 0 = offline (every verify
+ * evaluates its batch alone), LTL4C_STATE_ONLINE = online. */
+ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t capacity_hint,
+                                uint32_t flags, ltl4c_state **out);
+
+/* Multi-GPU: join a communicator of n_ranks processes (one per GPU).  nccl_id is
+ * the 128-byte ncclUniqueId, created by rank 0 and broadcast by the caller.
+ * Afterwards ltl4c_verify shards events by hash(k0) across ranks (all-to-all)
+ * and sums the per-level counts (all-reduce); every rank returns the global
+ * result.  Not yet implemented in this build: returns LTL4C_E_INVALID. */
+ltl4c_status ltl4c_state_comm(ltl4c_state *st, const void *nccl_id, int n_ranks, int rank);
+
+/* Run Algorithm 1 on one batch of device-resident events.  Work is enqueued on
+ * `cuda_stream` (a cudaStream_t; NULL = legacy default stream); the call returns
+ * after the <= 200-byte result has been copied to *out (one per formula: out
+ * must hold n_formulas results).  On error the state is poisoned (online) or
+ * unchanged (offline). */
+ltl4c_status ltl4c_verify(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream,
+                          ltl4c_result *out);
+
+/* As ltl4c_verify, but batch pointers are HOST pointers: the library copies the
+ * events to device buffers it owns (cudaMemcpyAsync on `cuda_stream`; pinned
+ * host memory gives asynchronous copies), then verifies. */
+ltl4c_status ltl4c_verify_host(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream,
+                               ltl4c_result *out);
+
+/* Forget all carried state (online) and clear the poisoned flag. */
+ltl4c_status ltl4c_state_reset(ltl4c_state *st);
+
+void ltl4c_state_free(ltl4c_state *st);
+
+/* Kernel-level profiling: when enabled, every library kernel launch is bracketed
+ * by CUDA events on the stream it runs on; ltl4c_state_stats sums them (this
+ * synchronises the stream).  ltl4c_state_stats_reset zeroes the counters. */
+ltl4c_status ltl4c_state_profile(ltl4c_state *st, int enable);
+ltl4c_status ltl4c_state_stats(ltl4c_state *st, ltl4c_stats *out);
+ltl4c_status ltl4c_state_stats_reset(ltl4c_state *st);
+
+/* Thread-local message of the last non-OK status ("" if none). */
+const char *ltl4c_last_error(void);
+
+/* Library version string, e.g. "ltl4c 0.1 sm_100a". */
+const char *ltl4c_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LTL4C_H */

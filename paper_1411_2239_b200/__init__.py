@@ -1,0 +1,276 @@
+"""paper_1411_2239_b200 -- B200-native LTL4-C runtime verification (arXiv:1411.2239).
+
+Thin ctypes binding of ``libltl4c.so`` (C ABI in ``include/ltl4c.h``).  This
+module only marshals arguments: compilation runs in the library's C++ compiler
+and every step of the verification path runs in the library's sm_100a kernels.
+There is no CPU fallback: if the library is missing this import fails, and a
+state cannot be created without a B200.
+
+    import paper_1411_2239_b200 as ltl4c
+    prog = ltl4c.compile("forall x : user(x) => exists[<=3] r : rid(r) => (login && unauthorized)")
+    st = prog.state(device=0)                 # offline; prog.state(online=True) for online mode
+    res = st.verify([users, rids], letters)   # torch CUDA tensors (uint32 / int32 keys, uint8 letters)
+    res[0].verdict, res[0].hist
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libltl4c.so")
+HEADER = os.path.join(os.path.dirname(_HERE), "include", "ltl4c.h")
+
+MAX_LEVELS = 3
+MAX_FORMULAS = 4
+MAX_KERNELS = 16
+ABSENT = 0xFFFFFFFF
+ONLINE = 1
+VERDICTS = ["FALSE", "CURRENTLY_FALSE", "PRESUMABLY_FALSE", "PRESUMABLY_TRUE",
+            "CURRENTLY_TRUE", "TRUE"]
+STATUS = {0: "OK", 1: "E_SYNTAX", 2: "E_NONCANONICAL", 3: "E_UNBOUND", 4: "E_RANGE",
+          5: "E_BUDGET", 6: "E_INVALID", 7: "E_CUDA", 8: "E_NCCL", 9: "E_OOM", 10: "E_POISONED"}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                      "(this package has no CPU fallback)")
+
+
+class Ltl4cError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+        self.name = STATUS.get(status, str(status))
+
+
+class _Quant(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("cmp", ctypes.c_int32), ("num", ctypes.c_uint64),
+                ("den", ctypes.c_uint64), ("key", ctypes.c_char * 64)]
+
+
+class _Tables(ctypes.Structure):
+    _fields_ = [("n_formulas", ctypes.c_uint32), ("n_levels", ctypes.c_uint32),
+                ("n_atoms", ctypes.c_uint32), ("n_states", ctypes.c_uint32),
+                ("initial", ctypes.c_uint32), ("delta", ctypes.POINTER(ctypes.c_uint8)),
+                ("label", ctypes.POINTER(ctypes.c_uint8)), ("quant", ctypes.POINTER(_Quant)),
+                ("atom_names", ctypes.POINTER(ctypes.c_char_p))]
+
+
+class _Batch(ctypes.Structure):
+    _fields_ = [("n_events", ctypes.c_uint64), ("first_index", ctypes.c_uint64),
+                ("keys", ctypes.c_void_p * MAX_LEVELS), ("letters", ctypes.c_void_p)]
+
+
+class _Result(ctypes.Structure):
+    _fields_ = [("verdict", ctypes.c_int32), ("n_levels", ctypes.c_uint32),
+                ("hist", (ctypes.c_uint64 * 6) * (MAX_LEVELS + 1)),
+                ("events_seen", ctypes.c_uint64), ("events_bound", ctypes.c_uint64)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("verifies", ctypes.c_uint64), ("launches", ctypes.c_uint64),
+                ("n_kernels", ctypes.c_uint32), ("kernel_name", (ctypes.c_char * 32) * MAX_KERNELS),
+                ("kernel_launches", ctypes.c_uint64 * MAX_KERNELS),
+                ("kernel_ms", ctypes.c_double * MAX_KERNELS)]
+
+
+_lib = ctypes.CDLL(LIB_PATH)
+_P = ctypes.c_void_p
+_lib.ltl4c_compile.argtypes = [ctypes.c_char_p, ctypes.POINTER(_P)]
+_lib.ltl4c_compile_batch.argtypes = [ctypes.POINTER(ctypes.c_char_p), ctypes.c_int, ctypes.POINTER(_P)]
+_lib.ltl4c_program_tables.argtypes = [_P, ctypes.POINTER(_Tables)]
+_lib.ltl4c_program_free.argtypes = [_P]
+_lib.ltl4c_program_free.restype = None
+_lib.ltl4c_state_create.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_P)]
+_lib.ltl4c_state_comm.argtypes = [_P, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+_lib.ltl4c_verify.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
+_lib.ltl4c_verify_host.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
+_lib.ltl4c_state_reset.argtypes = [_P]
+_lib.ltl4c_state_free.argtypes = [_P]
+_lib.ltl4c_state_free.restype = None
+_lib.ltl4c_state_profile.argtypes = [_P, ctypes.c_int]
+_lib.ltl4c_state_stats.argtypes = [_P, ctypes.POINTER(_Stats)]
+_lib.ltl4c_state_stats_reset.argtypes = [_P]
+_lib.ltl4c_last_error.restype = ctypes.c_char_p
+_lib.ltl4c_version.restype = ctypes.c_char_p
+for _fn in ("ltl4c_compile", "ltl4c_compile_batch", "ltl4c_program_tables", "ltl4c_state_create",
+            "ltl4c_state_comm", "ltl4c_verify", "ltl4c_verify_host", "ltl4c_state_reset",
+            "ltl4c_state_profile", "ltl4c_state_stats", "ltl4c_state_stats_reset"):
+    getattr(_lib, _fn).restype = ctypes.c_int
+
+
+def _check(st: int):
+    if st != 0:
+        raise Ltl4cError(st, _lib.ltl4c_last_error().decode(errors="replace"))
+
+
+def version() -> str:
+    return _lib.ltl4c_version().decode()
+
+
+@dataclass
+class Result:
+    verdict: int
+    hist: np.ndarray          # [n_levels + 1, 6]: depth 0 (root) .. n (leaves)
+    events_seen: int
+    events_bound: int
+
+    @property
+    def verdict_name(self) -> str:
+        return VERDICTS[self.verdict]
+
+
+class Program:
+    """A compiled LTL4-C program: LTL4 monitor + quantifier string (immutable)."""
+
+    def __init__(self, handle: ctypes.c_void_p, texts):
+        self._h = handle
+        self.texts = list(texts)
+        t = _Tables()
+        _check(_lib.ltl4c_program_tables(self._h, ctypes.byref(t)))
+        self.n_formulas = t.n_formulas
+        self.n_levels = t.n_levels
+        self.n_atoms = t.n_atoms
+        self.n_states = t.n_states
+        self.initial = t.initial
+        A = 1 << t.n_atoms
+        self.delta = np.ctypeslib.as_array(t.delta, shape=(t.n_states * A,)).reshape(t.n_states, A).copy()
+        self.label = np.ctypeslib.as_array(t.label, shape=(t.n_formulas * t.n_states,)).reshape(
+            t.n_formulas, t.n_states).copy()
+        self.atoms = [t.atom_names[j].decode() for j in range(t.n_atoms)]
+        self.quantifiers = []
+        for f in range(t.n_formulas):
+            row = []
+            for l in range(t.n_levels):
+                q = t.quant[f * t.n_levels + l]
+                row.append({"kind": "AE"[q.kind], "cmp": ["<", "<=", ">", ">=", "="][q.cmp],
+                            "num": q.num, "den": q.den, "key": q.key.decode()})
+            self.quantifiers.append(row)
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ltl4c_program_free(self._h)
+            self._h = None
+
+    def state(self, device: int = 0, online: bool = False, capacity: int = 0) -> "State":
+        return State(self, device, online, capacity)
+
+    def run_word(self, word) -> list[int]:
+        """Host-side replay of the monitor tables on one word (for table checks;
+        the verification path itself runs on the GPU)."""
+        q = self.initial
+        for a in word:
+            q = int(self.delta[q, a])
+        return [int(self.label[f, q]) for f in range(self.n_formulas)]
+
+
+def compile(text: str) -> Program:  # noqa: A001 (mirrors ltl4c_compile)
+    h = ctypes.c_void_p()
+    _check(_lib.ltl4c_compile(text.encode(), ctypes.byref(h)))
+    return Program(h, [text])
+
+
+def compile_batch(texts) -> Program:
+    arr = (ctypes.c_char_p * len(texts))(*[t.encode() for t in texts])
+    h = ctypes.c_void_p()
+    _check(_lib.ltl4c_compile_batch(arr, len(texts), ctypes.byref(h)))
+    return Program(h, texts)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(int(stream))
+
+
+class State:
+    """Verification state on one B200 (carried submonitor tree when online)."""
+
+    def __init__(self, prog: Program, device: int, online: bool, capacity: int):
+        self.prog = prog
+        self.device = device
+        self.online = online
+        self._h = ctypes.c_void_p()
+        _check(_lib.ltl4c_state_create(prog._h, device, capacity, ONLINE if online else 0,
+                                       ctypes.byref(self._h)))
+        self.next_index = 0
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _lib.ltl4c_state_free(self._h)
+            self._h = None
+
+    def _results(self, res) -> list[Result]:
+        n = self.prog.n_levels
+        out = []
+        for f in range(self.prog.n_formulas):
+            r = res[f]
+            h = np.array([[r.hist[l][v] for v in range(6)] for l in range(n + 1)], dtype=np.uint64)
+            out.append(Result(int(r.verdict), h, int(r.events_seen), int(r.events_bound)))
+        return out
+
+    def _batch(self, keys, letters, n, first_index, ptr):
+        b = _Batch()
+        b.n_events = n
+        b.first_index = self.next_index if first_index is None else first_index
+        for i in range(self.prog.n_levels):
+            b.keys[i] = ptr(keys[i])
+        b.letters = ptr(letters)
+        return b
+
+    def verify(self, keys, letters, first_index=None, stream=None) -> list[Result]:
+        """keys: n_levels CUDA tensors (uint32 or int32 bit patterns), letters: uint8 CUDA tensor."""
+        import torch
+        n = int(letters.numel())
+        for k in list(keys)[: self.prog.n_levels]:
+            if not (k.is_cuda and k.is_contiguous() and k.element_size() == 4 and k.numel() == n):
+                raise ValueError("keys must be contiguous 4-byte CUDA tensors of the same length as letters")
+        if not (letters.is_cuda and letters.is_contiguous() and letters.dtype == torch.uint8):
+            raise ValueError("letters must be a contiguous uint8 CUDA tensor")
+        b = self._batch(keys, letters, n, first_index, lambda t: t.data_ptr() if n else None)
+        res = (_Result * self.prog.n_formulas)()
+        _check(_lib.ltl4c_verify(self._h, ctypes.byref(b), _stream_handle(stream), res))
+        self.next_index = b.first_index + n
+        return self._results(res)
+
+    def verify_host(self, keys, letters, first_index=None, stream=None) -> list[Result]:
+        """As verify(), with host arrays (numpy or pinned torch CPU tensors); the
+        host->device copies run inside the library call."""
+        def ptr(a):
+            if hasattr(a, "data_ptr"):
+                return a.data_ptr()
+            return a.ctypes.data
+        n = int(letters.shape[0])
+        keep = [np.ascontiguousarray(k, dtype=np.uint32) if isinstance(k, np.ndarray) else k
+                for k in list(keys)[: self.prog.n_levels]]
+        let = np.ascontiguousarray(letters, dtype=np.uint8) if isinstance(letters, np.ndarray) else letters
+        b = self._batch(keep, let, n, first_index, lambda a: ptr(a) if n else None)
+        res = (_Result * self.prog.n_formulas)()
+        _check(_lib.ltl4c_verify_host(self._h, ctypes.byref(b), _stream_handle(stream), res))
+        self.next_index = b.first_index + n
+        return self._results(res)
+
+    def reset(self):
+        _check(_lib.ltl4c_state_reset(self._h))
+        self.next_index = 0
+
+    def profile(self, enable: bool = True):
+        _check(_lib.ltl4c_state_profile(self._h, 1 if enable else 0))
+
+    def stats(self) -> dict:
+        s = _Stats()
+        _check(_lib.ltl4c_state_stats(self._h, ctypes.byref(s)))
+        kernels = {}
+        for k in range(s.n_kernels):
+            kernels[s.kernel_name[k].value.decode()] = {"launches": int(s.kernel_launches[k]),
+                                                        "ms": float(s.kernel_ms[k])}
+        return {"verifies": int(s.verifies), "launches": int(s.launches), "kernels": kernels}
+
+    def stats_reset(self):
+        _check(_lib.ltl4c_state_stats_reset(self._h))

@@ -1,0 +1,866 @@
+// kernels.cu -- sm_100a kernels of the LTL4-C verification hot path.
+//
+// arXiv:1411.2239, Algorithm 1, re-designed for B200:
+//
+//  part_count / part_scan / part_scatter
+//      a1 epsilon (Eq. D) fused with a2 SortTrace:
+//      a STABLE LSD partition of the bound events by bucket = top bits of
+//      hash(k0).  Every node of the submonitor tree below the root is keyed by a
+//      vector that starts with k0, so a bucket holds whole level-0 subtrees, and
+//      stability keeps every slice u^D in trace order (reading A15).
+//  bucket_scan
+//      exclusive scan of the bucket histogram -> bucket offsets (mu).
+//  bucket_fast
+//      one CTA per bucket, everything in shared memory:
+//        a3 SpawnMonitors: dedup of value vectors (smem hash) = leaves
+//        a4 Distribute / UpdateMonitor: each leaf steps the LTL4 monitor delta
+//           over its slice in order (Def. 5); lane per short slice,
+//           warp per long slice (ordered composition of transition maps)
+//        a5 ApplyQuantifiers: level by level, group children by parent prefix
+//           (P), histogram B, rule Def. 6
+//  bucket_global
+//      same steps in chunks of kCap events with carried leaf / node tables in
+//      global memory and delta propagation (online mode P:943, and buckets
+//      larger than one chunk).
+//  finalize
+//      root verdict from the depth-1 histogram, result record.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+
+namespace ltl4c {
+
+const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter",
+                                                "bucket_scan", "bucket_fast", "bucket_global",
+                                                "finalize", "rehash"};
+
+namespace {
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// ------------------------------------------------------------------ scans
+// Exclusive scan of n (<= blockDim * per) values held in smem `a` (u32), in place.
+// Returns the total.  All threads of the block must call it.
+__device__ uint32_t block_exclusive_scan(uint32_t *a, int n, uint32_t *warp_tot) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int lo = min(n, tid * per), hi = min(n, lo + per);
+  uint32_t s = 0;
+  for (int i = lo; i < hi; ++i) s += a[i];
+  uint32_t x = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) warp_tot[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = nt >> 5;
+    uint32_t w = lane < nw ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    if (lane < nw) warp_tot[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  uint32_t base = (x - s) + (wid ? warp_tot[wid - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    uint32_t v = a[i];
+    a[i] = base;
+    base += v;
+  }
+  uint32_t total = warp_tot[(nt >> 5) - 1];
+  __syncthreads();
+  return total;
+}
+
+// ------------------------------------------------------------------ partition
+__global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartParams p) {
+  extern __shared__ uint32_t bhist[];  // 1 << bits bins when small (pass 0)
+  __shared__ uint32_t dcnt[1 << kMaxDigitBits];
+  __shared__ uint32_t nvalid;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t ndig = 1u << p.width, dmask = ndig - 1u;
+  const bool small_hist = p.first && p.bits <= 13;
+  const uint32_t nb = 1u << p.bits;
+  for (uint32_t d = tid; d < ndig; d += blockDim.x) dcnt[d] = 0;
+  if (small_hist)
+    for (uint32_t b = tid; b < nb; b += blockDim.x) bhist[b] = 0;
+  if (tid == 0) nvalid = 0;
+  __syncthreads();
+  unsigned long long n = p.n;
+  if (p.n_dev) n = min(n, *p.n_dev);
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv + (unsigned long long)wid * 512;
+  uint32_t myvalid = 0;
+  for (int r = 0; r < 16; ++r) {
+    const unsigned long long j = base + r * 32 + lane;
+    bool valid = j < n;
+    uint32_t k0 = 0;
+    if (valid) {
+      k0 = p.in_key[0][j];
+      if (p.first)
+        for (int i = 0; i < p.K; ++i) valid &= p.in_key[i][j] != kAbsent;
+    }
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t b = bucket_of(k0, p.bits);
+      const uint32_t d = (b >> p.lo) & dmask;
+      const uint32_t peers = __match_any_sync(vm, d);
+      if ((peers & lanemask_lt()) == 0) atomicAdd(&dcnt[d], __popc(peers));
+      if (p.first) {
+        const uint32_t bp = __match_any_sync(vm, b);
+        if ((bp & lanemask_lt()) == 0) {
+          if (small_hist) atomicAdd(&bhist[b], __popc(bp));
+          else atomicAdd(&p.bucket_count[b], __popc(bp));
+        }
+      }
+    }
+    myvalid += valid;
+  }
+  if (p.first) {
+    for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
+    if (lane == 0) atomicAdd(&nvalid, myvalid);
+  }
+  __syncthreads();
+  for (uint32_t d = tid; d < ndig; d += blockDim.x)
+    p.counts[(size_t)d * p.n_tiles + blockIdx.x] = dcnt[d];
+  if (p.first) {
+    if (tid == 0 && nvalid) {
+      atomicAdd(&p.acc->events_bound, (unsigned long long)nvalid);
+      atomicAdd(p.nvalid, (unsigned long long)nvalid);
+    }
+    if (small_hist)
+      for (uint32_t b = tid; b < nb; b += blockDim.x)
+        if (bhist[b]) atomicAdd(&p.bucket_count[b], bhist[b]);
+  }
+}
+
+// exclusive scan of counts[d][0..n_tiles) (one CTA per digit), totals[d]
+__global__ void __launch_bounds__(1024) part_scan_kernel(PartParams p) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  uint32_t *row = p.counts + (size_t)blockIdx.x * p.n_tiles;
+  uint32_t carry = 0;
+  for (uint32_t off = 0; off < p.n_tiles; off += 1024) {
+    const uint32_t i = off + threadIdx.x;
+    buf[threadIdx.x] = i < p.n_tiles ? row[i] : 0;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < p.n_tiles) row[i] = buf[threadIdx.x] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) p.totals[blockIdx.x] = carry;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartParams p) {
+  __shared__ uint32_t dbase[1 << kMaxDigitBits];
+  __shared__ uint16_t wcnt[kPartThreads / 32][1 << kMaxDigitBits];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t ndig = 1u << p.width, dmask = ndig - 1u;
+  // digit bases: exclusive scan of the digit totals + this tile's prefix
+  if (tid == 0) {
+    uint32_t run = 0;
+    for (uint32_t d = 0; d < ndig; ++d) {
+      dbase[d] = run;
+      run += p.totals[d];
+    }
+  }
+  for (uint32_t d = tid; d < ndig * (kPartThreads / 32); d += blockDim.x)
+    wcnt[d / ndig][d % ndig] = 0;
+  __syncthreads();
+  for (uint32_t d = tid; d < ndig; d += blockDim.x)
+    dbase[d] += p.counts[(size_t)d * p.n_tiles + blockIdx.x];
+  unsigned long long n = p.n;
+  if (p.n_dev) n = min(n, *p.n_dev);
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv + (unsigned long long)wid * 512;
+  uint32_t kv[16][K];
+  uint8_t lv[16];
+  uint16_t dig[16], rank[16];
+  uint32_t validmask = 0;
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const unsigned long long j = base + r * 32 + lane;
+    bool valid = j < n;
+    if (valid) {
+#pragma unroll
+      for (int i = 0; i < K; ++i) kv[r][i] = p.in_key[i][j];
+      lv[r] = p.in_let[j];
+      if (p.first) {
+#pragma unroll
+        for (int i = 0; i < K; ++i) valid &= kv[r][i] != kAbsent;
+      }
+    }
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t d = (bucket_of(kv[r][0], p.bits) >> p.lo) & dmask;
+      const uint32_t peers = __match_any_sync(vm, d);
+      const uint32_t old = wcnt[wid][d];
+      rank[r] = (uint16_t)(old + __popc(peers & lanemask_lt()));
+      dig[r] = (uint16_t)d;
+      __syncwarp(vm);
+      if ((peers & lanemask_lt()) == 0) wcnt[wid][d] = (uint16_t)(old + __popc(peers));
+      __syncwarp(vm);
+      validmask |= 1u << r;
+    }
+  }
+  __syncthreads();
+  // exclusive prefix over warps, per digit (in place)
+  for (uint32_t d = tid; d < ndig; d += blockDim.x) {
+    uint32_t run = 0;
+    for (int w = 0; w < kPartThreads / 32; ++w) {
+      const uint32_t c = wcnt[w][d];
+      wcnt[w][d] = (uint16_t)run;
+      run += c;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    if (!((validmask >> r) & 1)) continue;
+    const uint32_t d = dig[r];
+    const size_t pos = (size_t)dbase[d] + wcnt[wid][d] + rank[r];
+#pragma unroll
+    for (int i = 0; i < K; ++i) p.out_key[i][pos] = kv[r][i];
+    p.out_let[pos] = lv[r];
+  }
+}
+
+// exclusive scan of n bucket counts -> off[0..n] (single CTA)
+__global__ void __launch_bounds__(1024) bucket_scan_kernel(const uint32_t *count, uint32_t *off, uint32_t n) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  uint32_t carry = 0;
+  for (uint32_t o = 0; o < n; o += 1024) {
+    const uint32_t i = o + threadIdx.x;
+    buf[threadIdx.x] = i < n ? count[i] : 0;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < n) off[i] = buf[threadIdx.x] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) off[n] = carry;
+}
+
+// ------------------------------------------------------------------ buckets
+struct Smem {
+  uint32_t *key[kMaxLevels];  // [kCap] each
+  uint8_t *let;               // [kCap]
+  uint16_t *cls;              // class of each item
+  uint16_t *rep;              // rep event of each class
+  uint16_t *item_rep;         // rep event of each item
+  uint16_t *htab;             // [2 * kCap]
+  uint16_t *owner;            // [kCap]
+  uint32_t *scan;             // [kCap + 1]
+  uint32_t *cur;              // [kCap + 1]
+  uint16_t *perm;             // [kCap]
+  uint8_t *state;             // [kCap]
+  uint8_t *iv;                // [kMaxFormulas][kCap] item verdicts (new)
+  uint8_t *ov;                // [kMaxFormulas][kCap] item verdicts (old, global path)
+  uint8_t *nv;                // [kMaxFormulas][kCap] node verdicts
+  uint8_t *nov;               // [kMaxFormulas][kCap] node old verdicts (global path)
+  uint32_t *sortbuf;          // [kCap]
+  uint8_t *delta;             // [kMaxStates * 256]
+  unsigned long long *map;    // [256]
+  uint8_t *lab;               // [kMaxFormulas * kMaxStates]
+  int *acc;                   // [kMaxFormulas][kMaxLevels + 1][6] signed
+  uint32_t *misc;             // [64]
+};
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+
+// Shared-memory plan of a bucket CTA: K key words and nf formulas; the global
+// path additionally keeps the old verdicts (ov, nov).
+__host__ __device__ inline size_t smem_bytes(int K, int nf, bool global) {
+  const size_t fv = align16((size_t)nf * kCap);
+  return align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
+         align16(2 * 2 * kCap) + align16(2 * kCap) + 2 * align16(4 * (kCap + 1)) + align16(2 * kCap) +
+         align16(kCap) + (global ? 4 : 2) * fv + align16(4 * kCap) + align16(kMaxStates * 256) +
+         align16(8 * 256) + align16(kMaxFormulas * kMaxStates) +
+         align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6) + align16(4 * 64);
+}
+
+__device__ Smem carve(uint8_t *base, int K, int nf, bool global) {
+  Smem s;
+  uint8_t *p = base;
+  auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
+  for (int i = 0; i < kMaxLevels; ++i) s.key[i] = i < K ? (uint32_t *)take(sizeof(uint32_t) * kCap) : nullptr;
+  s.let = take(kCap);
+  s.cls = (uint16_t *)take(2 * kCap);
+  s.rep = (uint16_t *)take(2 * kCap);
+  s.item_rep = (uint16_t *)take(2 * kCap);
+  s.htab = (uint16_t *)take(2 * 2 * kCap);
+  s.owner = (uint16_t *)take(2 * kCap);
+  s.scan = (uint32_t *)take(4 * (kCap + 1));
+  s.cur = (uint32_t *)take(4 * (kCap + 1));
+  s.perm = (uint16_t *)take(2 * kCap);
+  s.state = take(kCap);
+  s.iv = take((size_t)nf * kCap);
+  s.nv = take((size_t)nf * kCap);
+  s.ov = global ? take((size_t)nf * kCap) : nullptr;
+  s.nov = global ? take((size_t)nf * kCap) : nullptr;
+  s.sortbuf = (uint32_t *)take(4 * kCap);
+  s.delta = take(kMaxStates * 256);
+  s.map = (unsigned long long *)take(8 * 256);
+  s.lab = take(kMaxFormulas * kMaxStates);
+  s.acc = (int *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
+  s.misc = (uint32_t *)take(4 * 64);
+  return s;
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t hash_prefix(const Smem &s, int e, int m) {
+  uint32_t h = 0x2545F491u;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (i < m) h = fmix32(h ^ s.key[i][e]) + 0x9e3779b9u * (i + 1);
+  return h;
+}
+
+template <int K>
+__device__ __forceinline__ bool same_prefix(const Smem &s, int a, int b, int m) {
+  bool eq = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (i < m) eq &= s.key[i][a] == s.key[i][b];
+  return eq;
+}
+
+// Group n items (rep event item_rep[i]) by the first m keys of their rep.
+// Out: s.cls[i] = dense class id, s.rep[c] = rep event of class c. Returns #classes.
+template <int K>
+__device__ int dedup(const Smem &s, int n, int m) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  constexpr int TS = 2 * kCap;
+  for (int i = tid; i < TS; i += nt) s.htab[i] = 0xFFFF;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) {
+    const int r = s.item_rep[i];
+    uint32_t slot = hash_prefix<K>(s, r, m) & (TS - 1);
+    while (true) {
+      const unsigned short old = atomicCAS(&s.htab[slot], (unsigned short)0xFFFF, (unsigned short)i);
+      if (old == 0xFFFF) { s.owner[i] = (uint16_t)i; break; }
+      if (same_prefix<K>(s, s.item_rep[old], r, m)) { s.owner[i] = old; break; }
+      slot = (slot + 1) & (TS - 1);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) s.scan[i] = s.owner[i] == i;
+  __syncthreads();
+  const int C = (int)block_exclusive_scan(s.scan, n, s.misc);
+  for (int i = tid; i < n; i += nt)
+    if (s.owner[i] == i) s.rep[s.scan[i]] = s.item_rep[i];
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) s.cls[i] = (uint16_t)s.scan[s.owner[i]];
+  __syncthreads();
+  return C;
+}
+
+// Counting sort of n items by class (C classes): s.perm = items grouped by
+// class, s.scan[c] .. s.scan[c+1] = segment of class c.  Unstable.
+__device__ void group_by_class(const Smem &s, int n, int C) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int c = tid; c <= C; c += nt) s.scan[c] = 0;
+  __syncthreads();
+  for (int i = tid; i < n; i += nt) s.owner[i] = (uint16_t)atomicAdd(&s.scan[s.cls[i]], 1u);
+  __syncthreads();
+  block_exclusive_scan(s.scan, C + 1, s.misc);  // scan[C] = n
+  for (int i = tid; i < n; i += nt) s.perm[s.scan[s.cls[i]] + s.owner[i]] = (uint16_t)i;
+  __syncthreads();
+}
+
+// Make every class segment of s.perm ascending (trace order, reading A15).
+__device__ void order_segments(const Smem &s, int n, int C) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (tid == 0) s.misc[40] = 0;
+  __syncthreads();
+  for (int c = tid; c < C; c += nt) {
+    const int a = s.scan[c], b = s.scan[c + 1];
+    if (b - a > 32) { s.misc[40] = 1; continue; }
+    for (int i = a + 1; i < b; ++i) {  // insertion sort
+      const uint16_t x = s.perm[i];
+      int j = i - 1;
+      while (j >= a && s.perm[j] > x) { s.perm[j + 1] = s.perm[j]; --j; }
+      s.perm[j + 1] = x;
+    }
+  }
+  __syncthreads();
+  if (!s.misc[40]) return;
+  // long segments present: bitonic sort of (class << 16 | item) over the chunk
+  int P = 1;
+  while (P < n) P <<= 1;
+  for (int i = tid; i < P; i += nt) s.sortbuf[i] = i < n ? ((uint32_t)s.cls[i] << 16) | (uint32_t)i : 0xFFFFFFFFu;
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < P; i += nt) {
+        const int ix = i ^ j;
+        if (ix > i) {
+          const uint32_t x = s.sortbuf[i], y = s.sortbuf[ix];
+          const bool up = (i & k) == 0;
+          if ((x > y) == up) { s.sortbuf[i] = y; s.sortbuf[ix] = x; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = tid; i < n; i += nt) s.perm[i] = (uint16_t)(s.sortbuf[i] & 0xFFFF);
+  __syncthreads();
+}
+
+__device__ __forceinline__ unsigned long long map_apply(unsigned long long g, unsigned long long f, int nq) {
+  // (g o f)[q] = g[f[q]]
+  unsigned long long r = 0;
+  for (int q = 0; q < nq; ++q) {
+    const int fq = (int)((f >> (4 * q)) & 15ull);
+    r |= ((g >> (4 * fq)) & 15ull) << (4 * q);
+  }
+  return r;
+}
+
+// Step every leaf class over its (ordered) segment from start state st0[c]
+// (kept in s.state on entry, replaced by the final state).
+__device__ void step_leaves(const Smem &s, int C, int nq, int na_letters) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  // short slices: one lane per leaf, delta in shared memory (Def. 5)
+  for (int c = tid; c < C; c += nt) {
+    const int a = s.scan[c], b = s.scan[c + 1];
+    if (b - a > 32) continue;
+    int q = s.state[c];
+    for (int i = a; i < b; ++i) q = s.delta[q * na_letters + s.let[s.perm[i]]];
+    s.state[c] = (uint8_t)q;
+  }
+  // long slices: one warp per leaf, each lane composes the transition maps of a
+  // contiguous piece, then the 32 maps are composed in order (associativity).
+  unsigned long long ident = 0;
+  for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
+  for (int c = wid; c < C; c += nw) {
+    const int a = s.scan[c], b = s.scan[c + 1];
+    const int len = b - a;
+    if (len <= 32) continue;
+    const int per = (len + 31) / 32;
+    const int lo = a + min(len, lane * per), hi = a + min(len, (lane + 1) * per);
+    unsigned long long m = ident;
+    for (int i = lo; i < hi; ++i) m = map_apply(s.map[s.let[s.perm[i]]], m, nq);
+    unsigned long long total = ident;
+    for (int l = 0; l < 32; ++l) {
+      const unsigned long long ml = __shfl_sync(0xffffffffu, m, l);
+      total = map_apply(ml, total, nq);
+    }
+    if (lane == 0) s.state[c] = (uint8_t)((total >> (4 * s.state[c])) & 15ull);
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+__device__ void load_prog(const Smem &s, const DevProg *prog) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int A = 1 << prog->na;
+  for (int i = tid; i < (int)prog->nq * A; i += nt) s.delta[i] = prog->delta[i / A][i % A];
+  for (int i = tid; i < A; i += nt) s.map[i] = prog->map[i];
+  for (int i = tid; i < kMaxFormulas * kMaxStates; i += nt) s.lab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
+  for (int i = tid; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += nt) s.acc[i] = 0;
+}
+
+__device__ __forceinline__ int acc_idx(int f, int l, int v) { return (f * (kMaxLevels + 1) + l) * 6 + v; }
+
+__device__ void flush_acc(const Smem &s, DevAcc *acc, int nf, int nl) {
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const int v = s.acc[i];
+    const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), b = i % 6;
+    if (v != 0 && f < nf && l >= 1 && l <= nl)
+      atomicAdd(&acc->hist[f][l][b], (unsigned long long)(long long)v);
+  }
+}
+
+template <int K>
+__device__ int load_chunk(const Smem &s, const BucketParams &p, uint32_t start, int cnt) {
+  for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) s.key[i][e] = p.key[i][start + e];
+    s.let[e] = p.let[start + e];
+    s.item_rep[e] = (uint16_t)e;
+  }
+  __syncthreads();
+  return cnt;
+}
+
+// ----------------------------------------------- fast path (offline, fits)
+template <int K>
+__global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t b = blockIdx.x;
+  const uint32_t start = p.bucket_off[b], cnt = p.bucket_off[b + 1] - start;
+  if (cnt == 0) return;
+  if (cnt > (uint32_t)kCap) {
+    if (threadIdx.x == 0) {
+      const unsigned long long i = atomicAdd(&p.acc->oversize_buckets, 1ull);
+      p.oversize_list[i] = b;
+      atomicAdd(&p.acc->oversize_events, (unsigned long long)cnt);
+    }
+    return;
+  }
+  const DevProg *prog = p.prog;
+  const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
+  const Smem s = carve(smem_raw, K, nf, false);
+  load_prog(s, prog);
+  const int n = load_chunk<K>(s, p, start, (int)cnt);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  // a3: leaves = distinct value vectors D of the bucket (Eq. D)
+  const int L = dedup<K>(s, n, K);
+  group_by_class(s, n, L);
+  order_segments(s, n, L);
+  // a4: every leaf starts at q0 (offline) and steps over u^D
+  for (int c = tid; c < L; c += nt) s.state[c] = (uint8_t)prog->q0;
+  __syncthreads();
+  step_leaves(s, L, nq, A);
+  // leaf verdicts lambda_f (Def. 5) and the depth-n histogram
+  for (int c = tid; c < L; c += nt) {
+    s.item_rep[c] = s.rep[c];
+    for (int f = 0; f < nf; ++f) {
+      const uint8_t v = s.lab[f * kMaxStates + s.state[c]];
+      s.iv[f * kCap + c] = v;
+      atomicAdd(&s.acc[acc_idx(f, nl, v)], 1);
+    }
+  }
+  __syncthreads();
+  // a5: ApplyQuantifiers for depth nl-1 .. 1 (depth 0, the root, in finalize)
+  int items = L;
+  for (int l = nl - 1; l >= 1; --l) {
+    const int C = dedup<K>(s, items, l);
+    group_by_class(s, items, C);
+    for (int x = tid; x < C; x += nt) {
+      const int a = s.scan[x], e = s.scan[x + 1];
+      for (int f = 0; f < nf; ++f) {
+        uint32_t h[6] = {0, 0, 0, 0, 0, 0};
+        for (int i = a; i < e; ++i) h[s.iv[f * kCap + s.perm[i]]]++;
+        const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l],
+                                   prog->qden[f][l], h);
+        s.nv[f * kCap + x] = (uint8_t)v;
+        atomicAdd(&s.acc[acc_idx(f, l, v)], 1);
+      }
+    }
+    __syncthreads();
+    for (int x = tid; x < C; x += nt) {
+      s.item_rep[x] = s.rep[x];
+      for (int f = 0; f < nf; ++f) s.iv[f * kCap + x] = s.nv[f * kCap + x];
+    }
+    __syncthreads();
+    items = C;
+  }
+  flush_acc(s, p.acc, nf, nl);
+}
+
+// ----------------------------------------------- global tables
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// find-or-insert of an m-key vector in an epoch-tagged open-addressing table.
+// Returns the slot; *inserted = 1 if the vector was not present.
+__device__ unsigned long long table_find_insert(uint4 *slots, unsigned long long cap, uint32_t epoch,
+                                                const uint32_t *k, int m, int *inserted,
+                                                unsigned long long *overflow) {
+  const uint32_t ready = (epoch << 1) | 1u, busy = epoch << 1;
+  uint32_t h = 0x7F4A7C15u;
+  for (int i = 0; i < m; ++i) h = fmix32(h ^ k[i]) + 0x632BE5ABu * (i + 1);
+  unsigned long long slot = h & (cap - 1);
+  for (unsigned long long probes = 0; probes < cap; ++probes) {
+    uint32_t *tag = &slots[slot].x;
+    uint32_t t = ld_acquire(tag);
+    while (t == busy) t = ld_acquire(tag);
+    if (t == ready) {
+      const uint4 s = slots[slot];
+      const bool eq = s.y == k[0] && (m < 2 || s.z == k[1]) && (m < 3 || s.w == k[2]);
+      if (eq) { *inserted = 0; return slot; }
+      slot = (slot + 1) & (cap - 1);
+      continue;
+    }
+    // empty or stale (older epoch): claim it
+    if (atomicCAS(tag, t, busy) == t) {
+      slots[slot].y = k[0];
+      slots[slot].z = m > 1 ? k[1] : 0u;
+      slots[slot].w = m > 2 ? k[2] : 0u;
+      *inserted = 1;
+      return slot;  // caller initialises payload then publishes with table_publish
+    }
+    // lost the race: re-examine the same slot
+  }
+  atomicAdd(overflow, 1ull);
+  *inserted = -1;
+  return 0;
+}
+
+__device__ __forceinline__ void table_publish(uint4 *slots, unsigned long long slot, uint32_t epoch) {
+  __threadfence();
+  st_release(&slots[slot].x, (epoch << 1) | 1u);
+}
+
+// ----------------------------------------------- global path (online / oversize)
+template <int K>
+__global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  uint32_t b;
+  if (p.list) {
+    if (blockIdx.x >= *p.list_len) return;
+    b = p.list[blockIdx.x];
+  } else {
+    b = blockIdx.x;
+  }
+  const uint32_t start = p.bucket_off[b], total = p.bucket_off[b + 1] - start;
+  if (total == 0) return;
+  const DevProg *prog = p.prog;
+  const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
+  const Smem s = carve(smem_raw, K, nf, true);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const DevTables &T = p.tab;
+  load_prog(s, prog);
+  __syncthreads();
+  for (uint32_t off = 0; off < total; off += kCap) {
+    const int n = load_chunk<K>(s, p, start + off, (int)min((uint32_t)kCap, total - off));
+    const int L = dedup<K>(s, n, K);
+    group_by_class(s, n, L);
+    order_segments(s, n, L);
+    // carried leaf state (merged submonitors)
+    for (int c = tid; c < L; c += nt) {
+      uint32_t k[kMaxLevels] = {0, 0, 0};
+      for (int i = 0; i < K; ++i) k[i] = s.key[i][s.rep[c]];
+      int ins;
+      const unsigned long long slot =
+          table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &p.acc->table_overflow);
+      s.cur[c] = (uint32_t)slot;  // slot index (cap <= 2^32)
+      if (ins == 1) {
+        s.state[c] = (uint8_t)prog->q0;
+        for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = 0xFF;
+        atomicAdd(&p.acc->leaves, 1ull);
+      } else {
+        const uint8_t q = ins == 0 ? T.leaf_state[slot] : (uint8_t)prog->q0;
+        s.state[c] = q;
+        for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = ins == 0 ? s.lab[f * kMaxStates + q] : 0xFF;
+      }
+      s.owner[c] = (uint16_t)(ins == 1);
+    }
+    __syncthreads();
+    step_leaves(s, L, nq, A);
+    for (int c = tid; c < L; c += nt) {
+      const unsigned long long slot = s.cur[c];
+      T.leaf_state[slot] = s.state[c];
+      if (s.owner[c]) table_publish(T.leaf_slot, slot, T.epoch);
+      s.item_rep[c] = s.rep[c];
+      for (int f = 0; f < nf; ++f) {
+        const uint8_t v = s.lab[f * kMaxStates + s.state[c]], o = s.ov[f * kCap + c];
+        s.iv[f * kCap + c] = v;
+        if (o != v) {
+          if (o != 0xFF) atomicAdd(&s.acc[acc_idx(f, nl, o)], -1);
+          atomicAdd(&s.acc[acc_idx(f, nl, v)], 1);
+        }
+      }
+    }
+    __syncthreads();
+    // delta propagation up the tree: depth nl-1 .. 1
+    int items = L;
+    for (int l = nl - 1; l >= 1; --l) {
+      const int C = dedup<K>(s, items, l);
+      group_by_class(s, items, C);
+      for (int x = tid; x < C; x += nt) {
+        uint32_t k[kMaxLevels] = {0, 0, 0};
+        for (int i = 0; i < l; ++i) k[i] = s.key[i][s.rep[x]];
+        int ins;
+        const unsigned long long slot = table_find_insert(T.node_slot[l], T.node_cap[l], T.epoch, k, l,
+                                                          &ins, &p.acc->table_overflow);
+        uint32_t *hist = T.node_hist[l] + slot * (kMaxFormulas * 6);
+        uint32_t packed = 0xFFFFFFFFu;
+        if (ins == 1) {
+          for (int i = 0; i < kMaxFormulas * 6; ++i) hist[i] = 0;
+          atomicAdd(&p.acc->nodes[l], 1ull);
+        } else if (ins == 0) {
+          packed = T.node_verdict[l][slot];
+        }
+        uint32_t newpacked = 0xFFFFFFFFu;
+        const int a = s.scan[x], e = s.scan[x + 1];
+        for (int f = 0; f < nf; ++f) {
+          uint32_t h[6];
+          for (int v = 0; v < 6; ++v) h[v] = ins >= 0 ? hist[f * 6 + v] : 0;
+          for (int i = a; i < e; ++i) {
+            const int it = s.perm[i];
+            const uint8_t o = s.ov[f * kCap + it], v = s.iv[f * kCap + it];
+            if (o != v) {
+              if (o != 0xFF) h[o] -= 1;
+              h[v] += 1;
+            }
+          }
+          if (ins >= 0)
+            for (int v = 0; v < 6; ++v) hist[f * 6 + v] = h[v];
+          const int nvv = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l],
+                                       prog->qden[f][l], h);
+          const uint8_t old = (uint8_t)((packed >> (8 * f)) & 0xFF);
+          s.nov[f * kCap + x] = old;
+          s.nv[f * kCap + x] = (uint8_t)nvv;
+          newpacked = (newpacked & ~(0xFFu << (8 * f))) | ((uint32_t)nvv << (8 * f));
+          if (old != nvv) {
+            if (old != 0xFF) atomicAdd(&s.acc[acc_idx(f, l, old)], -1);
+            atomicAdd(&s.acc[acc_idx(f, l, nvv)], 1);
+          }
+        }
+        if (ins >= 0) {
+          T.node_verdict[l][slot] = newpacked;
+          if (ins == 1) table_publish(T.node_slot[l], slot, T.epoch);
+        }
+      }
+      __syncthreads();
+      for (int x = tid; x < C; x += nt) {
+        s.item_rep[x] = s.rep[x];
+        for (int f = 0; f < nf; ++f) {
+          s.iv[f * kCap + x] = s.nv[f * kCap + x];
+          s.ov[f * kCap + x] = s.nov[f * kCap + x];
+        }
+      }
+      __syncthreads();
+      items = C;
+    }
+  }
+  flush_acc(s, p.acc, nf, nl);
+}
+
+// ----------------------------------------------- rehash (online tables grow)
+__global__ void rehash_kernel(DevTables from, DevTables to, int nl, int nf, unsigned long long *overflow) {
+  const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t ready = (from.epoch << 1) | 1u;
+  // blockIdx.y = 0: leaves (m = nl keys), y = l in [1, nl-1]: nodes of depth l
+  const int l = blockIdx.y;
+  if (l == 0) {
+    if (i >= from.leaf_cap) return;
+    const uint4 s = from.leaf_slot[i];
+    if (s.x != ready) return;
+    const uint32_t k[3] = {s.y, s.z, s.w};
+    int ins;
+    const unsigned long long j = table_find_insert(to.leaf_slot, to.leaf_cap, to.epoch, k, nl, &ins, overflow);
+    if (ins < 0) return;
+    to.leaf_state[j] = from.leaf_state[i];
+    table_publish(to.leaf_slot, j, to.epoch);
+  } else {
+    if (l >= nl || i >= from.node_cap[l]) return;
+    const uint4 s = from.node_slot[l][i];
+    if (s.x != ready) return;
+    const uint32_t k[3] = {s.y, s.z, s.w};
+    int ins;
+    const unsigned long long j = table_find_insert(to.node_slot[l], to.node_cap[l], to.epoch, k, l, &ins, overflow);
+    if (ins < 0) return;
+    to.node_verdict[l][j] = from.node_verdict[l][i];
+    for (int x = 0; x < kMaxFormulas * 6; ++x)
+      to.node_hist[l][j * kMaxFormulas * 6 + x] = from.node_hist[l][i * kMaxFormulas * 6 + x];
+    table_publish(to.node_slot[l], j, to.epoch);
+  }
+}
+
+// ----------------------------------------------- finalize
+__global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *out) {
+  const int f = threadIdx.x;
+  if (f < (int)prog->nf) {
+    const int nl = prog->nl;
+    DevResult &r = out->res[f];
+    unsigned long long h1[6];
+    for (int v = 0; v < 6; ++v) h1[v] = acc->hist[f][1][v];
+    const int root = node_verdict(prog->qkind[f][0], prog->qcmp[f][0], prog->qnum[f][0],
+                                  prog->qden[f][0], h1);
+    r.verdict = root;
+    r.n_levels = nl;
+    for (int l = 0; l <= kMaxLevels; ++l)
+      for (int v = 0; v < 6; ++v)
+        r.hist[l][v] = l == 0 ? (v == root ? 1ull : 0ull) : (l <= nl ? acc->hist[f][l][v] : 0ull);
+    r.events_seen = acc->events_seen;
+    r.events_bound = acc->events_bound;
+  }
+  if (f == 0) {
+    out->oversize_buckets = acc->oversize_buckets;
+    out->oversize_events = acc->oversize_events;
+    out->table_overflow = acc->table_overflow;
+    out->leaves = acc->leaves;
+    for (int l = 0; l <= kMaxLevels; ++l) out->nodes[l] = acc->nodes[l];
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+#define LTL4C_LAUNCH(ID, ...)                         \
+  do {                                                 \
+    if (L.before) L.before(L.ctx, ID);                 \
+    __VA_ARGS__;                                       \
+    cudaError_t e_ = cudaGetLastError();               \
+    if (L.after) L.after(L.ctx, ID);                   \
+    return e_;                                         \
+  } while (0)
+
+cudaError_t launch_part_count(const PartParams &p, const Launcher &L) {
+  const size_t sm = (p.first && p.bits <= 13) ? sizeof(uint32_t) << p.bits : 0;
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<<<p.n_tiles, kPartThreads, sm, L.stream>>>(p));
+}
+cudaError_t launch_part_scan(const PartParams &p, const Launcher &L) {
+  LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width, 1024, 0, L.stream>>>(p));
+}
+cudaError_t launch_part_scatter(const PartParams &p, const Launcher &L) {
+  switch (p.K) {
+    case 1: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<1><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+    case 2: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<2><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+    default: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<3><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+  }
+}
+cudaError_t launch_bucket_scan(const uint32_t *count, uint32_t *off, uint32_t n, const Launcher &L) {
+  LTL4C_LAUNCH(kKBucketScan, bucket_scan_kernel<<<1, 1024, 0, L.stream>>>(count, off, n));
+}
+
+cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, const Launcher &L) {
+  const size_t sm = smem_bytes(K, nf, false);
+  switch (K) {
+    case 1: cudaFuncSetAttribute(bucket_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<1><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+    case 2: cudaFuncSetAttribute(bucket_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<2><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+    default: cudaFuncSetAttribute(bucket_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<3><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+  }
+}
+
+cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
+  const size_t sm = smem_bytes(K, nf, true);
+  switch (K) {
+    case 1: cudaFuncSetAttribute(bucket_global_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
+    case 2: cudaFuncSetAttribute(bucket_global_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<2><<<grid, kBucketThreads, sm, L.stream>>>(p));
+    default: cudaFuncSetAttribute(bucket_global_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
+  }
+}
+
+cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
+                          unsigned long long *overflow, const Launcher &L) {
+  unsigned long long mx = from.leaf_cap;
+  for (int l = 1; l < n_levels; ++l) mx = mx > from.node_cap[l] ? mx : from.node_cap[l];
+  dim3 grid((unsigned)((mx + 255) / 256), (unsigned)n_levels);
+  LTL4C_LAUNCH(kKRehash, rehash_kernel<<<grid, 256, 0, L.stream>>>(from, to, n_levels, nf, overflow));
+}
+
+cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L) {
+  LTL4C_LAUNCH(kKFinalize, finalize_kernel<<<1, 32, 0, L.stream>>>(prog, acc, out));
+}
+
+}  // namespace ltl4c

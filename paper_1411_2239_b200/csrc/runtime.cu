@@ -1,0 +1,574 @@
+// runtime.cu -- C ABI (include/ltl4c.h): states, buffers, launch orchestration.
+//
+// One ltl4c_verify = Algorithm 1 of arXiv:1411.2239 on a batch:
+//   SortTrace       -> P stable LSD passes (part_count, part_scan, part_scatter)
+//                      + bucket_scan                      (a1, a2)
+//   SpawnMonitors,
+//   Distribute,
+//   ApplyQuantifiers -> bucket_fast (offline) / bucket_global (online, or
+//                      buckets larger than one shared-memory chunk)  (a3-a5)
+//   return           -> finalize + one <= 1 KB D2H copy              (a6)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "program.h"
+
+namespace ltl4c {
+
+static thread_local std::string g_err;
+
+ltl4c_status fail(ltl4c_status st, const std::string &msg) {
+  g_err = msg;
+  return st;
+}
+
+#define CU(expr)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? LTL4C_E_OOM : LTL4C_E_CUDA,           \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));                    \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  cudaError_t ensure(size_t want) {
+    if (want <= n && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    size_t cap = std::max<size_t>(want, 1);
+    cudaError_t e = cudaMalloc((void **)&p, cap * sizeof(T));
+    if (e == cudaSuccess) n = cap;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+struct Tables {
+  DevTables d{};
+  DevBuf<uint4> leaf_slot;
+  DevBuf<uint8_t> leaf_state;
+  DevBuf<uint4> node_slot[kMaxLevels];
+  DevBuf<uint32_t> node_verdict[kMaxLevels];
+  DevBuf<uint32_t> node_hist[kMaxLevels];
+  void release() {
+    leaf_slot.release();
+    leaf_state.release();
+    for (int l = 0; l < kMaxLevels; ++l) {
+      node_slot[l].release();
+      node_verdict[l].release();
+      node_hist[l].release();
+    }
+    d = DevTables{};
+  }
+};
+
+struct PendingTiming {
+  int kernel;
+  cudaEvent_t a, b;
+};
+
+}  // namespace ltl4c
+
+using namespace ltl4c;
+
+struct ltl4c_state {
+  const ltl4c_program *prog = nullptr;
+  int device = 0;
+  uint32_t flags = 0;
+  bool poisoned = false;
+  uint64_t next_index = 0;
+  bool have_index = false;
+  uint64_t events_seen = 0;
+  uint32_t epoch = 1;
+  DevProg hprog{};
+  DevBuf<DevProg> d_prog;
+  DevBuf<DevAcc> d_acc;
+  DevBuf<DevOut> d_out;
+  DevOut *h_out = nullptr;  // pinned
+  DevBuf<unsigned long long> d_nvalid;
+  DevBuf<uint32_t> bufkey[2][kMaxLevels];
+  DevBuf<uint8_t> buflet[2];
+  DevBuf<uint32_t> counts, totals, bucket_count, bucket_off, oversize_list;
+  DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
+  DevBuf<uint8_t> hlet;
+  Tables tab;
+  // stats / profiling
+  bool profiling = false;
+  uint64_t verifies = 0, launches = 0;
+  uint64_t k_launches[kKNumKernels] = {};
+  double k_ms[kKNumKernels] = {};
+  std::vector<PendingTiming> pending;
+  std::vector<cudaEvent_t> event_pool;
+  cudaStream_t cur_stream = nullptr;
+};
+
+namespace {
+
+cudaEvent_t take_event(ltl4c_state *st) {
+  if (!st->event_pool.empty()) {
+    cudaEvent_t e = st->event_pool.back();
+    st->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+void before_launch(void *ctx, int k) {
+  auto *st = (ltl4c_state *)ctx;
+  if (!st->profiling) return;
+  PendingTiming t{k, take_event(st), take_event(st)};
+  cudaEventRecord(t.a, st->cur_stream);
+  st->pending.push_back(t);
+}
+
+void after_launch(void *ctx, int k) {
+  auto *st = (ltl4c_state *)ctx;
+  st->launches++;
+  st->k_launches[k]++;
+  if (!st->profiling || st->pending.empty()) return;
+  cudaEventRecord(st->pending.back().b, st->cur_stream);
+}
+
+void drain_timings(ltl4c_state *st) {
+  for (auto &t : st->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(t.b);
+    if (cudaEventElapsedTime(&ms, t.a, t.b) == cudaSuccess) st->k_ms[t.kernel] += ms;
+    st->event_pool.push_back(t.a);
+    st->event_pool.push_back(t.b);
+  }
+  st->pending.clear();
+}
+
+int ceil_log2(uint64_t x) {
+  int b = 0;
+  while ((1ull << b) < x) ++b;
+  return b;
+}
+
+ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_t node_cap, cudaStream_t s) {
+  const int nl = (int)st->prog->n_levels;
+  CU(t.leaf_slot.ensure(leaf_cap));
+  CU(t.leaf_state.ensure(leaf_cap));
+  CU(cudaMemsetAsync(t.leaf_slot.p, 0, sizeof(uint4) * leaf_cap, s));
+  t.d.leaf_cap = leaf_cap;
+  t.d.leaf_slot = t.leaf_slot.p;
+  t.d.leaf_state = t.leaf_state.p;
+  for (int l = 1; l < nl; ++l) {
+    CU(t.node_slot[l].ensure(node_cap));
+    CU(t.node_verdict[l].ensure(node_cap));
+    CU(t.node_hist[l].ensure(node_cap * kMaxFormulas * 6));
+    CU(cudaMemsetAsync(t.node_slot[l].p, 0, sizeof(uint4) * node_cap, s));
+    t.d.node_cap[l] = node_cap;
+    t.d.node_slot[l] = t.node_slot[l].p;
+    t.d.node_verdict[l] = t.node_verdict[l].p;
+    t.d.node_hist[l] = t.node_hist[l].p;
+  }
+  return LTL4C_OK;
+}
+
+// Online: make sure the carried tables can absorb `extra` more leaves/nodes at
+// load <= 1/2, rehashing the carried entries into larger tables if needed.
+ltl4c_status ensure_online_tables(ltl4c_state *st, uint64_t extra, cudaStream_t s, const Launcher &L) {
+  const uint64_t have = st->h_out->leaves;
+  uint64_t need_nodes = 0;
+  for (int l = 1; l < (int)st->prog->n_levels; ++l) need_nodes = std::max<uint64_t>(need_nodes, st->h_out->nodes[l]);
+  const uint64_t want_leaf = 1ull << std::max(16, ceil_log2(2 * (have + extra) + 1));
+  const uint64_t want_node = 1ull << std::max(14, ceil_log2(2 * (need_nodes + extra) + 1));
+  Tables &t = st->tab;
+  bool fresh = t.d.leaf_cap == 0;
+  if (!fresh && t.d.leaf_cap >= want_leaf) {
+    bool ok = true;
+    for (int l = 1; l < (int)st->prog->n_levels; ++l) ok &= t.d.node_cap[l] >= want_node;
+    if (ok) return LTL4C_OK;
+  }
+  if (fresh) {
+    ltl4c_status r = alloc_tables(st, t, want_leaf, want_node, s);
+    if (r) return r;
+    t.d.epoch = st->epoch;
+    return LTL4C_OK;
+  }
+  Tables nt;
+  ltl4c_status r = alloc_tables(st, nt, std::max<uint64_t>(want_leaf, t.d.leaf_cap), std::max<uint64_t>(want_node, t.d.node_cap[1]), s);
+  if (r) return r;
+  nt.d.epoch = st->epoch;
+  CU(launch_rehash(t.d, nt.d, (int)st->prog->n_levels, (int)st->prog->n_formulas,
+                   &st->d_acc.p->table_overflow, L));
+  CU(cudaStreamSynchronize(s));
+  t.release();
+  t = nt;
+  nt = Tables{};  // ownership moved (DevBuf members copied; prevent double free)
+  return LTL4C_OK;
+}
+
+ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, ltl4c_result *out,
+                        const uint32_t *const *keys, const uint8_t *letters) {
+  const ltl4c_program *prog = st->prog;
+  const int K = (int)prog->n_levels;
+  const bool online = st->flags & LTL4C_STATE_ONLINE;
+  const uint64_t N = b->n_events;
+  st->cur_stream = s;
+  Launcher L{s, before_launch, after_launch, st};
+  if (!online) {
+    CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
+    st->events_seen = 0;
+  }
+  st->events_seen += N;
+  CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
+  if (online) {
+    ltl4c_status r = ensure_online_tables(st, N, s, L);
+    if (r) return r;
+  }
+  if (N > 0) {
+    const uint64_t target = std::max<uint64_t>(2, (3 * N + kCap - 1) / kCap);
+    const int B = std::min(24, std::max(1, ceil_log2(target)));
+    const int P = (B + kMaxDigitBits - 1) / kMaxDigitBits;
+    const uint32_t NB = 1u << B;
+    const uint32_t n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
+    for (int i = 0; i < 2; ++i) {
+      for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
+      CU(st->buflet[i].ensure(N));
+    }
+    CU(st->counts.ensure((size_t)(1u << kMaxDigitBits) * n_tiles));
+    CU(st->totals.ensure(1u << kMaxDigitBits));
+    CU(st->bucket_count.ensure(NB));
+    CU(st->bucket_off.ensure((size_t)NB + 1));
+    CU(st->oversize_list.ensure(NB));
+    CU(cudaMemsetAsync(st->bucket_count.p, 0, sizeof(uint32_t) * NB, s));
+    int lo = 0;
+    for (int pass = 0; pass < P; ++pass) {
+      const int width = (B - lo + (P - pass) - 1) / (P - pass);
+      PartParams pp{};
+      for (int l = 0; l < K; ++l) {
+        pp.in_key[l] = pass == 0 ? keys[l] : st->bufkey[(pass - 1) & 1][l].p;
+        pp.out_key[l] = st->bufkey[pass & 1][l].p;
+      }
+      pp.in_let = pass == 0 ? letters : st->buflet[(pass - 1) & 1].p;
+      pp.out_let = st->buflet[pass & 1].p;
+      pp.n = N;
+      pp.n_dev = pass == 0 ? nullptr : st->d_nvalid.p;
+      pp.K = K;
+      pp.bits = B;
+      pp.lo = lo;
+      pp.width = width;
+      pp.first = pass == 0;
+      pp.n_tiles = n_tiles;
+      pp.counts = st->counts.p;
+      pp.totals = st->totals.p;
+      pp.bucket_count = st->bucket_count.p;
+      pp.acc = st->d_acc.p;
+      pp.nvalid = st->d_nvalid.p;
+      CU(launch_part_count(pp, L));
+      CU(launch_part_scan(pp, L));
+      CU(launch_part_scatter(pp, L));
+      lo += width;
+    }
+    CU(launch_bucket_scan(st->bucket_count.p, st->bucket_off.p, NB, L));
+    BucketParams bp{};
+    const int fin = (P - 1) & 1;
+    for (int l = 0; l < K; ++l) bp.key[l] = st->bufkey[fin][l].p;
+    bp.let = st->buflet[fin].p;
+    bp.bucket_off = st->bucket_off.p;
+    bp.n_buckets = NB;
+    bp.oversize_list = st->oversize_list.p;
+    bp.prog = st->d_prog.p;
+    bp.acc = st->d_acc.p;
+    if (!online) {
+      CU(launch_bucket_fast(bp, K, (int)prog->n_formulas, L));
+      CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+      CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      if (st->h_out->oversize_buckets > 0) {
+        // buckets larger than one shared-memory chunk: chunked path with
+        // per-verify tables (fresh epoch, no clearing needed)
+        const uint64_t ev = st->h_out->oversize_events;
+        const uint64_t want = 1ull << std::max(12, ceil_log2(2 * ev + 1));
+        if (st->tab.d.leaf_cap < want || (K > 1 && st->tab.d.node_cap[1] < want)) {
+          st->tab.release();
+          ltl4c_status r = alloc_tables(st, st->tab, want, want, s);
+          if (r) return r;
+        }
+        st->tab.d.epoch = ++st->epoch;
+        bp.tab = st->tab.d;
+        bp.list = st->oversize_list.p;
+        bp.list_len = &st->d_acc.p->oversize_buckets;
+        CU(launch_bucket_global(bp, K, (int)prog->n_formulas, (uint32_t)st->h_out->oversize_buckets, L));
+        CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+        CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+      }
+    } else {
+      bp.tab = st->tab.d;
+      CU(launch_bucket_global(bp, K, (int)prog->n_formulas, NB, L));
+      CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+      CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+    }
+  } else {
+    CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+    CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+  }
+  if (st->h_out->table_overflow)
+    return fail(LTL4C_E_OOM, "carried table overflow");
+  for (uint32_t f = 0; f < prog->n_formulas; ++f) {
+    const DevResult &r = st->h_out->res[f];
+    ltl4c_result &o = out[f];
+    std::memset(&o, 0, sizeof o);
+    o.verdict = r.verdict;
+    o.n_levels = r.n_levels;
+    for (int l = 0; l <= kMaxLevels; ++l)
+      for (int v = 0; v < 6; ++v) o.hist[l][v] = r.hist[l][v];
+    o.events_seen = st->events_seen;
+    o.events_bound = r.events_bound;
+  }
+  st->verifies++;
+  return LTL4C_OK;
+}
+
+ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, ltl4c_result *out,
+                           bool host) {
+  if (!st || !b || !out) return fail(LTL4C_E_INVALID, "null argument");
+  if (st->poisoned) return fail(LTL4C_E_POISONED, "state poisoned by an earlier failure; reset it");
+  const int K = (int)st->prog->n_levels;
+  if (b->n_events > (1ull << 32) - (1ull << 20))
+    return fail(LTL4C_E_INVALID, "batch too large (max ~4.29e9 events)");
+  if (b->n_events > 0) {
+    for (int l = 0; l < K; ++l)
+      if (!b->keys[l]) return fail(LTL4C_E_INVALID, "null key pointer");
+    if (!b->letters) return fail(LTL4C_E_INVALID, "null letters pointer");
+  }
+  const bool online = st->flags & LTL4C_STATE_ONLINE;
+  if (online && st->have_index && b->first_index != st->next_index)
+    return fail(LTL4C_E_INVALID, "online batch is not contiguous with the previous batch");
+  cudaStream_t s = (cudaStream_t)stream;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != st->device) CU(cudaSetDevice(st->device));
+  const uint32_t *keys[kMaxLevels] = {nullptr, nullptr, nullptr};
+  const uint8_t *letters = b->letters;
+  for (int l = 0; l < K; ++l) keys[l] = b->keys[l];
+  ltl4c_status r = LTL4C_OK;
+  if (host && b->n_events > 0) {
+    for (int l = 0; l < K && !r; ++l) {
+      if (st->hkeys[l].ensure(b->n_events) != cudaSuccess) r = fail(LTL4C_E_OOM, "staging alloc");
+      else if (cudaMemcpyAsync(st->hkeys[l].p, b->keys[l], 4 * b->n_events, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        r = fail(LTL4C_E_CUDA, "H2D copy of keys failed");
+      keys[l] = st->hkeys[l].p;
+    }
+    if (!r) {
+      if (st->hlet.ensure(b->n_events) != cudaSuccess) r = fail(LTL4C_E_OOM, "staging alloc");
+      else if (cudaMemcpyAsync(st->hlet.p, b->letters, b->n_events, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        r = fail(LTL4C_E_CUDA, "H2D copy of letters failed");
+      letters = st->hlet.p;
+    }
+  }
+  if (!r) r = run_verify(st, b, s, out, keys, letters);
+  if (prev != st->device) cudaSetDevice(prev);
+  if (r) {
+    if (online) st->poisoned = true;
+    return r;
+  }
+  if (online) {
+    st->next_index = b->first_index + b->n_events;
+    st->have_index = true;
+  }
+  return LTL4C_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ltl4c_last_error(void) { return g_err.c_str(); }
+
+const char *ltl4c_version(void) { return "ltl4c 0.1 sm_100a"; }
+
+ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t capacity_hint,
+                                uint32_t flags, ltl4c_state **out) {
+  if (!prog || !out) return fail(LTL4C_E_INVALID, "null argument");
+  *out = nullptr;
+  if (flags & ~LTL4C_STATE_ONLINE) return fail(LTL4C_E_INVALID, "unknown flags");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return fail(LTL4C_E_CUDA, "no CUDA device visible (this library has no CPU fallback)");
+  if (device < 0 || device >= ndev) return fail(LTL4C_E_INVALID, "bad device ordinal");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(device));
+  cudaDeviceProp dp{};
+  CU(cudaGetDeviceProperties(&dp, device));
+  if (dp.major != 10) {
+    cudaSetDevice(prev);
+    return fail(LTL4C_E_CUDA, "library is built for sm_100a (B200); device is sm_" +
+                                  std::to_string(dp.major) + std::to_string(dp.minor));
+  }
+  auto st = new ltl4c_state();
+  st->prog = prog;
+  st->device = device;
+  st->flags = flags;
+  DevProg &h = st->hprog;
+  h.nf = prog->n_formulas;
+  h.nl = prog->n_levels;
+  h.na = prog->n_atoms;
+  h.nq = prog->n_states;
+  h.q0 = prog->initial;
+  const int A = 1 << prog->n_atoms;
+  for (uint32_t q = 0; q < prog->n_states; ++q)
+    for (int a = 0; a < A; ++a) h.delta[q][a] = prog->delta[q * A + a];
+  for (int a = 0; a < A; ++a) {
+    unsigned long long m = 0;
+    for (uint32_t q = 0; q < prog->n_states; ++q) m |= (unsigned long long)h.delta[q][a] << (4 * q);
+    h.map[a] = m;
+  }
+  for (uint32_t f = 0; f < prog->n_formulas; ++f) {
+    for (uint32_t q = 0; q < prog->n_states; ++q) h.lab[f][q] = prog->label[f * prog->n_states + q];
+    for (uint32_t l = 0; l < prog->n_levels; ++l) {
+      const ltl4c_quantifier &qq = prog->quant[f * prog->n_levels + l];
+      h.qkind[f][l] = qq.kind;
+      h.qcmp[f][l] = qq.cmp;
+      h.qnum[f][l] = qq.num;
+      h.qden[f][l] = qq.den;
+    }
+  }
+  auto cleanup = [&](ltl4c_status r) {
+    ltl4c_state_free(st);
+    cudaSetDevice(prev);
+    return r;
+  };
+  if (st->d_prog.ensure(1) || st->d_acc.ensure(1) || st->d_out.ensure(1) || st->d_nvalid.ensure(1))
+    return cleanup(fail(LTL4C_E_OOM, "device allocation failed"));
+  if (cudaMallocHost((void **)&st->h_out, sizeof(DevOut)) != cudaSuccess)
+    return cleanup(fail(LTL4C_E_OOM, "pinned allocation failed"));
+  std::memset(st->h_out, 0, sizeof(DevOut));
+  if (cudaMemcpy(st->d_prog.p, &h, sizeof(DevProg), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaMemset(st->d_acc.p, 0, sizeof(DevAcc)) != cudaSuccess)
+    return cleanup(fail(LTL4C_E_CUDA, "initialisation copy failed"));
+  if (capacity_hint) {
+    const int K = (int)prog->n_levels;
+    for (int i = 0; i < 2; ++i) {
+      for (int l = 0; l < K; ++l)
+        if (st->bufkey[i][l].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
+      if (st->buflet[i].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
+    }
+  }
+  cudaSetDevice(prev);
+  *out = st;
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_comm(ltl4c_state *st, const void *nccl_id, int n_ranks, int rank) {
+  (void)nccl_id;
+  (void)rank;
+  if (!st) return fail(LTL4C_E_INVALID, "null state");
+  if (n_ranks == 1) return LTL4C_OK;
+  return fail(LTL4C_E_INVALID, "multi-GPU sharding is not implemented in this build");
+}
+
+ltl4c_status ltl4c_verify(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream, ltl4c_result *out) {
+  return verify_common(st, batch, cuda_stream, out, false);
+}
+
+ltl4c_status ltl4c_verify_host(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream,
+                               ltl4c_result *out) {
+  return verify_common(st, batch, cuda_stream, out, true);
+}
+
+ltl4c_status ltl4c_state_reset(ltl4c_state *st) {
+  if (!st) return fail(LTL4C_E_INVALID, "null state");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  CU(cudaMemset(st->d_acc.p, 0, sizeof(DevAcc)));
+  std::memset(st->h_out, 0, sizeof(DevOut));
+  st->epoch++;  // every carried table slot becomes stale
+  st->tab.d.epoch = st->epoch;
+  st->poisoned = false;
+  st->have_index = false;
+  st->next_index = 0;
+  st->events_seen = 0;
+  cudaSetDevice(prev);
+  return LTL4C_OK;
+}
+
+void ltl4c_state_free(ltl4c_state *st) {
+  if (!st) return;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(st->device);
+  st->d_prog.release();
+  st->d_acc.release();
+  st->d_out.release();
+  st->d_nvalid.release();
+  for (int i = 0; i < 2; ++i) {
+    for (int l = 0; l < kMaxLevels; ++l) st->bufkey[i][l].release();
+    st->buflet[i].release();
+  }
+  st->counts.release();
+  st->totals.release();
+  st->bucket_count.release();
+  st->bucket_off.release();
+  st->oversize_list.release();
+  for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
+  st->hlet.release();
+  st->tab.release();
+  for (auto &t : st->pending) {
+    cudaEventDestroy(t.a);
+    cudaEventDestroy(t.b);
+  }
+  for (auto e : st->event_pool) cudaEventDestroy(e);
+  if (st->h_out) cudaFreeHost(st->h_out);
+  cudaSetDevice(prev);
+  delete st;
+}
+
+ltl4c_status ltl4c_state_profile(ltl4c_state *st, int enable) {
+  if (!st) return fail(LTL4C_E_INVALID, "null state");
+  st->profiling = enable != 0;
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_stats(ltl4c_state *st, ltl4c_stats *out) {
+  if (!st || !out) return fail(LTL4C_E_INVALID, "null argument");
+  drain_timings(st);
+  std::memset(out, 0, sizeof *out);
+  out->verifies = st->verifies;
+  out->launches = st->launches;
+  out->n_kernels = kKNumKernels;
+  for (int k = 0; k < kKNumKernels; ++k) {
+    std::snprintf(out->kernel_name[k], sizeof out->kernel_name[k], "%s", kKernelNames[k]);
+    out->kernel_launches[k] = st->k_launches[k];
+    out->kernel_ms[k] = st->k_ms[k];
+  }
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_stats_reset(ltl4c_state *st) {
+  if (!st) return fail(LTL4C_E_INVALID, "null state");
+  drain_timings(st);
+  st->verifies = st->launches = 0;
+  for (int k = 0; k < kKNumKernels; ++k) {
+    st->k_launches[k] = 0;
+    st->k_ms[k] = 0.0;
+  }
+  return LTL4C_OK;
+}
+
+}  // extern "C"

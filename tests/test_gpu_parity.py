@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the oracle, bit-exact
+on verdicts and per-level counts (integer-only path: SURVEY §8(c), BASELINE.json
+"bit-exact verdicts and counts").  Inputs are seeded tracegen workloads."""
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+import tracegen
+from tests import ltl_bruteforce as bf
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env(cuda_ok):
+    import torch
+
+    import paper_1411_2239_b200 as ltl4c
+    return ltl4c, torch, torch.device("cuda:0")
+
+
+def _dev(torch, dev, keys, letters):
+    return ([torch.from_numpy(np.ascontiguousarray(k).view(np.int32)).to(dev) for k in keys],
+            torch.from_numpy(np.ascontiguousarray(letters)).to(dev))
+
+
+def _gpu_offline(env, text, keys, letters):
+    ltl4c, torch, dev = env
+    st = ltl4c.compile(text).state(0)
+    k, l = _dev(torch, dev, keys, letters)
+    return st.verify(k, l)
+
+
+def _assert_same(got, want, ctx=""):
+    assert got.verdict == want["verdict"], (ctx, got.verdict, want["verdict"])
+    assert np.array_equal(got.hist, want["hist"]), (ctx, got.hist, want["hist"])
+    assert got.events_bound == want["events_bound"], ctx
+
+
+def test_worked_example_offline_and_online(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.worked_example()
+    got = _gpu_offline(env, tr.formula, tr.keys, tr.letters)[0]
+    _assert_same(got, oracle.run_offline(tr.formula, tr.keys, tr.letters))
+    assert got.verdict == 0 and list(got.hist[1]) == [1, 0, 0, 0, 1, 0]
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    verdicts = []
+    for j in range(tr.n):
+        k, l = _dev(torch, dev, [x[j:j + 1] for x in tr.keys], tr.letters[j:j + 1])
+        verdicts.append(st.verify(k, l)[0].verdict)
+    assert verdicts == [4, 4, 4, 4, 0]
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_C1_socket(env, seed):
+    tr = tracegen.socket_trace(seed=seed)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), seed)
+
+
+@pytest.mark.parametrize("variant,rid_events", [("random", 1), ("clean", 1), ("violator", 1),
+                                                ("random", 3)])
+def test_C2_login_small(env, variant, rid_events):
+    tr = tracegen.login_trace(seed=7, n=300_000, users=3000, variant=variant, rid_events=rid_events,
+                              p_unauth=0.04)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), variant)
+
+
+def test_C2_login_full_size(env):
+    """BASELINE.json configs[1] at full size (10M events, 100k users), as bench.py runs it."""
+    tr = tracegen.login_trace(seed=0)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), "C2 full")
+
+
+@pytest.mark.parametrize("support,s", [(1 << 12, 1.1), (1 << 16, 1.1)])
+def test_C3_zipf_skew(env, support, s):
+    """Heavy keys exceed one shared-memory chunk: exercises the chunked global path
+    and the warp-level ordered map composition for long slices."""
+    tr = tracegen.zipf_socket_trace(seed=1, n=1_000_000, support=support, s=s)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), support)
+    tr = tracegen.zipf_socket_trace(seed=2, n=400_000, support=4096, formula=tracegen.FIG1)
+    tr.letters = np.random.default_rng(3).choice(np.array([1, 3, 2, 6, 7, 0], np.uint8), size=tr.n,
+                                                 p=[0.6, 0.2, 0.1, 0.05, 0.04, 0.01])
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), "fig1")
+
+
+def test_C4_proxy(env):
+    tr = tracegen.proxy_trace(seed=3, n=1_000_000, videos=20_000, p_ext_cached=0.002)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), "C4")
+
+
+def _project(letters, prog_atoms, prop_atoms):
+    out = np.zeros_like(letters)
+    for j, a in enumerate(prop_atoms):
+        g = prog_atoms.index(a)
+        out |= ((letters >> g) & 1) << j
+    return out
+
+
+def test_C5_formula_batch_online(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.c5_trace(seed=0, n=300_000, users=2000, hosts=64, span_events=60_000)
+    prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+    st = prog.state(0, online=True)
+    props = [oracle.Property(t) for t in tracegen.C5_FORMULAS]
+    mons = [oracle.Monitor(p) for p in props]
+    cuts = [0, 1000, 50_000, 170_000, 300_000]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+        got = st.verify(k, l, first_index=lo)
+        for f, (p, m) in enumerate(zip(props, mons)):
+            m.feed([x[lo:hi] for x in tr.keys], _project(tr.letters[lo:hi], prog.atoms, p.atoms))
+            _assert_same(got[f], m.evaluate(), (f, hi))
+
+
+def test_online_batches_equal_offline_prefix(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.login_trace(seed=9, n=200_000, users=500, rid_events=4, p_unauth=0.05)
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    cuts = [0, 7, 5000, 5001, 120_000, 200_000]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+        got = st.verify(k, l, first_index=lo)[0]
+        want = oracle.run_offline(tr.formula, [x[:hi] for x in tr.keys], tr.letters[:hi])
+        _assert_same(got, want, hi)
+
+
+def test_online_rejects_gap_and_reset(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.worked_example()
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    k, l = _dev(torch, dev, [x[:2] for x in tr.keys], tr.letters[:2])
+    st.verify(k, l, first_index=0)
+    with pytest.raises(ltl4c.Ltl4cError) as e:
+        st.verify(k, l, first_index=5)
+    assert e.value.name == "E_INVALID"
+    st.reset()
+    k, l = _dev(torch, dev, tr.keys, tr.letters)
+    _assert_same(st.verify(k, l, first_index=0)[0], oracle.run_offline(tr.formula, tr.keys, tr.letters))
+
+
+def test_edge_cases(env):
+    ltl4c, torch, dev = env
+    text = tracegen.LOGIN
+    empty = [np.zeros(0, np.uint32)] * 2
+    _assert_same(_gpu_offline(env, text, empty, np.zeros(0, np.uint8))[0],
+                 oracle.run_offline(text, empty, np.zeros(0, np.uint8)), "empty")
+    absent = [np.full(100, 0xFFFFFFFF, np.uint32), np.arange(100, dtype=np.uint32)]
+    lets = np.full(100, 3, np.uint8)
+    _assert_same(_gpu_offline(env, text, absent, lets)[0], oracle.run_offline(text, absent, lets), "absent")
+    one = [np.array([5], np.uint32), np.array([6], np.uint32)]
+    _assert_same(_gpu_offline(env, text, one, np.array([3], np.uint8))[0],
+                 oracle.run_offline(text, one, np.array([3], np.uint8)), "one")
+    # key value 0 and 0xFFFFFFFE are ordinary values
+    k = [np.array([0, 0xFFFFFFFE, 0], np.uint32), np.array([0, 0, 0xFFFFFFFE], np.uint32)]
+    lt = np.array([3, 1, 3], np.uint8)
+    _assert_same(_gpu_offline(env, text, k, lt)[0], oracle.run_offline(text, k, lt), "extreme keys")
+
+
+def test_random_properties_offline_and_online(env):
+    """Random formulas (1-3 levels, <= 3 atoms, depth <= 3) x random traces over tiny
+    domains, offline and online with random batch splits."""
+    ltl4c, torch, dev = env
+    rng = random.Random(411)
+    ops = ["<", "<=", ">", ">=", "="]
+    for case in range(60):
+        levels = rng.randint(1, 3)
+        f = bf.random_formula(rng, ["a", "b", "c"], 3)
+        if not bf.atoms_in_order(f):
+            continue
+        prefix = ""
+        for i in range(levels):
+            if rng.random() < 0.5:
+                c = rng.choice(["0", "0.25", "0.5", "1", "1/3"]) if False else rng.choice(["0", "0.25", "0.5", "1", "0.75"])
+                prefix += f"forall[{rng.choice(ops)}{c}] x{i} : k{i}(x{i}) => "
+            else:
+                prefix += f"exists[{rng.choice(ops)}{rng.randint(0, 3)}] x{i} : k{i}(x{i}) => "
+        text = prefix + bf.to_text(f)
+        na = len(bf.atoms_in_order(f))
+        n = rng.choice([1, 5, 40, 300, 3000])
+        keys, letters = tracegen.random_property_trace(case, levels, n, values=rng.choice([2, 3, 50]),
+                                                       atoms=na)
+        want = oracle.run_offline(text, keys, letters)
+        _assert_same(_gpu_offline(env, text, keys, letters)[0], want, text)
+        st = ltl4c.compile(text).state(0, online=True)
+        cuts = sorted({0, n, *[rng.randint(0, n) for _ in range(3)]})
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            k, l = _dev(torch, dev, [x[lo:hi] for x in keys], letters[lo:hi])
+            got = st.verify(k, l, first_index=lo)[0]
+        _assert_same(got, want, ("online", text))
+
+
+def test_verify_host_equals_device(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.login_trace(seed=4, n=100_000, users=1000, p_unauth=0.05)
+    st = ltl4c.compile(tr.formula).state(0)
+    a = st.verify_host(tr.keys, tr.letters)[0]
+    k, l = _dev(torch, dev, tr.keys, tr.letters)
+    b = st.verify(k, l)[0]
+    assert a.verdict == b.verdict and np.array_equal(a.hist, b.hist)
+
+
+def test_deterministic_reruns(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.zipf_socket_trace(seed=5, n=500_000, support=1 << 14)
+    st = ltl4c.compile(tr.formula).state(0)
+    k, l = _dev(torch, dev, tr.keys, tr.letters)
+    first = st.verify(k, l)[0]
+    for _ in range(3):
+        again = st.verify(k, l)[0]
+        assert again.verdict == first.verdict and np.array_equal(again.hist, first.hist)
+
+
+def test_profiling_counts_launches(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.socket_trace(seed=0)
+    st = ltl4c.compile(tr.formula).state(0)
+    st.profile(True)
+    k, l = _dev(torch, dev, tr.keys, tr.letters)
+    st.verify(k, l)
+    s = st.stats()
+    assert s["launches"] >= 5 and s["kernels"]["bucket_fast"]["launches"] == 1
+    assert s["kernels"]["bucket_fast"]["ms"] > 0

@@ -210,3 +210,33 @@ def random_property_trace(seed: int, levels: int, n_events: int, values: int = 3
         keys.append(k)
     letters = rng.integers(0, 1 << atoms, size=n_events).astype(np.uint8)
     return keys, letters
+
+
+def c5_trace(seed: int = 0, n: int = 2_000_000, hosts: int = 256, users: int = 100_000,
+             mean_len: float = 10.0, span_events: int = 2_000_000,
+             p=(0.01, 0.3, 0.3, 0.01, 0.05)) -> Trace:
+    """C5: three-level keys (host, user, session); sessions are unique with ~mean_len
+    events spread over ~span_events positions (about two 1M-event batches).
+    Letter bits follow the atom union of C5_FORMULAS: authfail, request, response,
+    admin, external."""
+    rng = np.random.default_rng(SEED_BASE + 5 + seed)
+    S = max(1, int(n / mean_len))
+    lens = 1 + rng.poisson(mean_len - 1, size=S)
+    starts = rng.random(S) * n
+    ev_sess = np.repeat(np.arange(S), lens)
+    gaps = rng.exponential(span_events / mean_len, size=ev_sess.shape[0])
+    first = np.r_[0, np.cumsum(lens)[:-1]]
+    cs = np.cumsum(gaps)
+    t = starts[ev_sess] + cs - np.repeat(cs[first], lens)
+    order = np.argsort(t, kind="stable")[:n]
+    ev_sess = ev_sess[order]
+    user_of = rng.integers(0, users, size=S)
+    home = rng.integers(0, hosts, size=users)
+    roam = rng.random(S) < 0.1
+    host_of = np.where(roam, rng.integers(0, hosts, size=S), home[user_of])
+    hid, uid, sid = _ids(rng, hosts), _ids(rng, users), _ids(rng, S)
+    letters = np.zeros(ev_sess.shape[0], dtype=np.uint8)
+    for j, pj in enumerate(p):
+        letters |= (rng.random(ev_sess.shape[0]) < pj).astype(np.uint8) << j
+    keys = [hid[host_of[ev_sess]], uid[user_of[ev_sess]], sid[ev_sess]]
+    return Trace("\n".join(C5_FORMULAS), keys, letters, {"config": "C5", "seed": seed})
