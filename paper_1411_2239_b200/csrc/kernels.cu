@@ -647,6 +647,10 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
           table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &p.acc->table_overflow);
       s.cur[c] = (uint32_t)slot;  // slot index (cap <= 2^32)
       if (ins == 1) {
+        // publish at once (state = q0): a thread of this CTA probing the slot
+        // must never wait across the barriers below
+        T.leaf_state[slot] = (uint8_t)prog->q0;
+        table_publish(T.leaf_slot, slot, T.epoch);
         s.state[c] = (uint8_t)prog->q0;
         for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = 0xFF;
         atomicAdd(&p.acc->leaves, 1ull);
@@ -655,14 +659,13 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
         s.state[c] = q;
         for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = ins == 0 ? s.lab[f * kMaxStates + q] : 0xFF;
       }
-      s.owner[c] = (uint16_t)(ins == 1);
+      s.owner[c] = (uint16_t)(ins < 0 ? 2 : 0);
     }
     __syncthreads();
     step_leaves(s, L, nq, A);
     for (int c = tid; c < L; c += nt) {
       const unsigned long long slot = s.cur[c];
-      T.leaf_state[slot] = s.state[c];
-      if (s.owner[c]) table_publish(T.leaf_slot, slot, T.epoch);
+      if (s.owner[c] != 2) T.leaf_state[slot] = s.state[c];
       s.item_rep[c] = s.rep[c];
       for (int f = 0; f < nf; ++f) {
         const uint8_t v = s.lab[f * kMaxStates + s.state[c]], o = s.ov[f * kCap + c];
@@ -689,6 +692,8 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
         uint32_t packed = 0xFFFFFFFFu;
         if (ins == 1) {
           for (int i = 0; i < kMaxFormulas * 6; ++i) hist[i] = 0;
+          T.node_verdict[l][slot] = 0xFFFFFFFFu;
+          table_publish(T.node_slot[l], slot, T.epoch);
           atomicAdd(&p.acc->nodes[l], 1ull);
         } else if (ins == 0) {
           packed = T.node_verdict[l][slot];
@@ -719,10 +724,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
             atomicAdd(&s.acc[acc_idx(f, l, nvv)], 1);
           }
         }
-        if (ins >= 0) {
-          T.node_verdict[l][slot] = newpacked;
-          if (ins == 1) table_publish(T.node_slot[l], slot, T.epoch);
-        }
+        if (ins >= 0) T.node_verdict[l][slot] = newpacked;
       }
       __syncthreads();
       for (int x = tid; x < C; x += nt) {
