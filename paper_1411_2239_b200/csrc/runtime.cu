@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -142,6 +143,12 @@ void after_launch(void *ctx, int k) {
   auto *st = (ltl4c_state *)ctx;
   st->launches++;
   st->k_launches[k]++;
+  static const bool sync_debug = std::getenv("LTL4C_SYNC_DEBUG") != nullptr;
+  if (sync_debug) {
+    std::fprintf(stderr, "[ltl4c] launched %s ...", kKernelNames[k]);
+    cudaError_t e = cudaStreamSynchronize(st->cur_stream);
+    std::fprintf(stderr, " done (%s)\n", cudaGetErrorString(e));
+  }
   if (!st->profiling || st->pending.empty()) return;
   cudaEventRecord(st->pending.back().b, st->cur_stream);
 }
