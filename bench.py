@@ -1,0 +1,275 @@
+#!/usr/bin/env python
+"""Benchmark of the LTL4-C verification hot path (BASELINE.json metric:
+"trace events verified/sec ...; achieved HBM GB/s vs peak").
+
+Default workload (N=1): BASELINE.json configs[1] = C2, the nested property
+  A x : user(x) => E_{<=3} r : rid(r) => (login && unauthorized)
+over a 10M-event synthetic web-server log with 100k users (tracegen.login_trace).
+A step = one ltl4c_verify of the whole 10M-event batch (all of SURVEY §8(a):
+epsilon + clustering, dedup, stepping, level reduction, root verdict, result
+copy).  Inputs are resident in HBM before the timed region; L2 (126 MB) is
+flushed between steps by writing a 256 MiB buffer (the input is 90 MB).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N>1 runs under torch.distributed.run, one rank per GPU; each rank verifies its
+own independent C2-shaped trace (weak scaling, no data-path collective; the
+hash-sharded single-trace path is not in this build).  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import tracegen  # noqa: E402
+
+METRIC = "trace events verified/sec"
+UNIT = "events/s"
+WORKLOAD = ("C2: A x:user(x) => E_{<=3} r:rid(r) => (login && unauthorized), "
+            "10M-event synthetic web-server log, 100k users (BASELINE.json configs[1])")
+ALG_BYTES_PER_EVENT = 9  # 2 x u32 keys + u8 letter read once
+RESULT_BYTES = 928       # sizeof(DevOut) copied device -> host per verify
+FLUSH_BYTES = 256 << 20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"ltl4c_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines()]
+            rows = [[c.strip() for c in r] for r in rows if len(r) >= 8]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows]
+        mx = max(float(r[1]) for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i].lower().startswith("active")})
+        loaded = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def make_trace(rank: int):
+    return tracegen.login_trace(seed=rank)
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1411_2239_b200 as ltl4c
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    tr = make_trace(rank)
+    n = tr.n
+    keys = [torch.from_numpy(k.view(np.int32)).to(dev) for k in tr.keys]
+    letters = torch.from_numpy(tr.letters).to(dev)
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    prog = ltl4c.compile(tr.formula)
+    st = prog.state(local_rank, capacity=n)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return st.verify(keys, letters, stream=stream)[0]
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        res = step()
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    st.stats_reset()
+    st.profile(True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    with Clocks(local_rank) as clk:
+        for i in range(args.steps):
+            flush.zero_()                 # L2 flush, outside the timed interval
+            ev[i][0].record(stream)
+            res = step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize(dev)
+    st.profile(False)
+    ms = [a.elapsed_time(b) for a, b in ev]
+    total_ms = float(sum(ms))
+    stats = st.stats()
+    if dist is not None:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    # e2e: the same call with HOST (pinned) buffers, H2D copies inside the timed region
+    hkeys = [torch.from_numpy(k.view(np.int32)).pin_memory() for k in tr.keys]
+    hlet = torch.from_numpy(tr.letters).pin_memory()
+    st_h = prog.state(local_rank, capacity=n)
+    for _ in range(max(1, args.warmup)):
+        st_h.verify_host(hkeys, hlet, stream=stream)
+    torch.cuda.synchronize(dev)
+    e2e_ms = []
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        r2 = st_h.verify_host(hkeys, hlet, stream=stream)[0]   # returns after the D2H result copy
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    assert r2.verdict == res.verdict
+    e2e_total = float(sum(e2e_ms))
+    if dist is not None:
+        t = torch.tensor([e2e_total], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_total = float(t.item())
+    return {"n": n, "total_ms": total_ms, "ms": ms, "stats": stats, "clocks": clk.summary(),
+            "verdict": res.verdict, "e2e_total_ms": e2e_total, "tr": tr,
+            "h2d": int(sum(k.numel() * 4 for k in hkeys) + hlet.numel())}
+
+
+def cpu_baseline(tr, max_s=30.0):
+    """The oracle as it stands, single-threaded, on the bench trace (or a prefix)."""
+    import oracle
+    n = tr.n
+    t0 = time.perf_counter()
+    oracle.run_offline(tr.formula, tr.keys, tr.letters)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"whole bench trace ({n} events, seed 0), one pass, {dt:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    r = run_ours(args, rank, world, local_rank)
+    if rank == 0:
+        peak, peak_kind = _peaks()
+        n_total = r["n"] * world
+        value = n_total * args.steps / (r["total_ms"] / 1e3)
+        ks = r["stats"]["kernels"]
+        dom = max(ks, key=lambda k: ks[k]["ms"])
+        per_launch_ms = ks[dom]["ms"] / max(1, ks[dom]["launches"])
+        alg_bytes = ALG_BYTES_PER_EVENT * r["n"]
+        achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+                traffic = json.load(f).get(dom)
+        except Exception:
+            traffic = None
+        shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ks.values())), 4)
+                  for k, v in ks.items() if v["launches"]}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (tracegen, seeded)",
+            "config": {"workload": WORKLOAD, "events_per_gpu": r["n"], "users": 100_000,
+                       "l2": "flushed between steps (256 MiB write, untimed)",
+                       "parallelism": f"{world} independent traces (weak)" if world > 1 else "1 GPU",
+                       "root_verdict": r["verdict"]},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "path_achieved": alg_bytes * args.steps / (r["total_ms"] / 1e3) / 1e9,
+                         "kernel_share": shares},
+            "e2e": {"value": n_total * args.steps / (r["e2e_total_ms"] / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": RESULT_BYTES},
+            "gpu_launches": int(r["stats"]["launches"]),
+            "clocks": r["clocks"],
+        }
+        if world == 1:
+            line["cpu_baseline"] = cpu_baseline(r["tr"])
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, world):
+    """Reference arm: the oracle (oracle/), as it stands, on the host cores; each
+    step verifies a bounded 1M-event sample (prefix) of the same C2 workload."""
+    if rank != 0:
+        return
+    import oracle
+    tr = make_trace(0)
+    m = 1_000_000
+    keys = [k[:m] for k in tr.keys]
+    letters = tr.letters[:m]
+    for _ in range(args.warmup):
+        oracle.run_offline(tr.formula, keys, letters)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.run_offline(tr.formula, keys, letters)
+    dt = time.perf_counter() - t0
+    value = m * args.steps / dt
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (tracegen, seeded)",
+            "config": {"workload": WORKLOAD, "events_per_gpu": tr.n, "users": 100_000},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"first {m} events of the C2 trace per step"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()
