@@ -37,6 +37,7 @@ struct DevAcc {
   unsigned long long hist[kMaxFormulas][kMaxLevels + 1][6];
   unsigned long long events_seen;
   unsigned long long events_bound;
+  unsigned long long medium_buckets;
   unsigned long long oversize_buckets;
   unsigned long long oversize_events;
   unsigned long long table_overflow;

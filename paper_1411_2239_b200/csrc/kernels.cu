@@ -34,7 +34,7 @@ namespace ltl4c {
 
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter",
                                                 "bucket_scan", "bucket_fast", "bucket_global",
-                                                "finalize", "rehash"};
+                                                "finalize", "rehash", "bucket_warp"};
 
 namespace {
 
@@ -501,66 +501,290 @@ __device__ int load_chunk(const Smem &s, const BucketParams &p, uint32_t start, 
 template <int K>
 __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  const uint32_t b = blockIdx.x;
-  const uint32_t start = p.bucket_off[b], cnt = p.bucket_off[b + 1] - start;
-  if (cnt == 0) return;
-  if (cnt > (uint32_t)kCap) {
-    if (threadIdx.x == 0) {
-      const unsigned long long i = atomicAdd(&p.acc->oversize_buckets, 1ull);
-      p.oversize_list[i] = b;
-      atomicAdd(&p.acc->oversize_events, (unsigned long long)cnt);
-    }
-    return;
-  }
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
   const Smem s = carve(smem_raw, K, nf, false);
   load_prog(s, prog);
-  const int n = load_chunk<K>(s, p, start, (int)cnt);
   const int tid = threadIdx.x, nt = blockDim.x;
-  // a3: leaves = distinct value vectors D of the bucket (Eq. D)
-  const int L = dedup<K>(s, n, K);
-  group_by_class(s, n, L);
-  order_segments(s, n, L);
-  // a4: every leaf starts at q0 (offline) and steps over u^D
-  for (int c = tid; c < L; c += nt) s.state[c] = (uint8_t)prog->q0;
-  __syncthreads();
-  step_leaves(s, L, nq, A);
-  // leaf verdicts lambda_f (Def. 5) and the depth-n histogram
-  for (int c = tid; c < L; c += nt) {
-    s.item_rep[c] = s.rep[c];
-    for (int f = 0; f < nf; ++f) {
-      const uint8_t v = s.lab[f * kMaxStates + s.state[c]];
-      s.iv[f * kCap + c] = v;
-      atomicAdd(&s.acc[acc_idx(f, nl, v)], 1);
+  const unsigned long long len = *p.list_len;
+  for (unsigned long long it = blockIdx.x; it < len; it += gridDim.x) {
+    const uint32_t b = p.list[it];
+    const uint32_t start = p.bucket_off[b], cnt = p.bucket_off[b + 1] - start;
+    if (cnt > (uint32_t)kCap) {
+      if (tid == 0) {
+        const unsigned long long i = atomicAdd(&p.acc->oversize_buckets, 1ull);
+        p.oversize_list[i] = b;
+        atomicAdd(&p.acc->oversize_events, (unsigned long long)cnt);
+      }
+      continue;
     }
-  }
-  __syncthreads();
-  // a5: ApplyQuantifiers for depth nl-1 .. 1 (depth 0, the root, in finalize)
-  int items = L;
-  for (int l = nl - 1; l >= 1; --l) {
-    const int C = dedup<K>(s, items, l);
-    group_by_class(s, items, C);
-    for (int x = tid; x < C; x += nt) {
-      const int a = s.scan[x], e = s.scan[x + 1];
+    __syncthreads();
+    const int n = load_chunk<K>(s, p, start, (int)cnt);
+    // a3: leaves = distinct value vectors D of the bucket (Eq. D)
+    const int L = dedup<K>(s, n, K);
+    group_by_class(s, n, L);
+    order_segments(s, n, L);
+    // a4: every leaf starts at q0 (offline) and steps over u^D
+    for (int c = tid; c < L; c += nt) s.state[c] = (uint8_t)prog->q0;
+    __syncthreads();
+    step_leaves(s, L, nq, A);
+    // leaf verdicts lambda_f (Def. 5) and the depth-n histogram
+    for (int c = tid; c < L; c += nt) {
+      s.item_rep[c] = s.rep[c];
       for (int f = 0; f < nf; ++f) {
-        uint32_t h[6] = {0, 0, 0, 0, 0, 0};
-        for (int i = a; i < e; ++i) h[s.iv[f * kCap + s.perm[i]]]++;
-        const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l],
-                                   prog->qden[f][l], h);
-        s.nv[f * kCap + x] = (uint8_t)v;
-        atomicAdd(&s.acc[acc_idx(f, l, v)], 1);
+        const uint8_t v = s.lab[f * kMaxStates + s.state[c]];
+        s.iv[f * kCap + c] = v;
+        atomicAdd(&s.acc[acc_idx(f, nl, v)], 1);
       }
     }
     __syncthreads();
-    for (int x = tid; x < C; x += nt) {
-      s.item_rep[x] = s.rep[x];
-      for (int f = 0; f < nf; ++f) s.iv[f * kCap + x] = s.nv[f * kCap + x];
+    // a5: ApplyQuantifiers for depth nl-1 .. 1 (depth 0, the root, in finalize)
+    int items = L;
+    for (int l = nl - 1; l >= 1; --l) {
+      const int C = dedup<K>(s, items, l);
+      group_by_class(s, items, C);
+      for (int x = tid; x < C; x += nt) {
+        const int a = s.scan[x], e = s.scan[x + 1];
+        for (int f = 0; f < nf; ++f) {
+          uint32_t h[6] = {0, 0, 0, 0, 0, 0};
+          for (int i = a; i < e; ++i) h[s.iv[f * kCap + s.perm[i]]]++;
+          const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l],
+                                     prog->qden[f][l], h);
+          s.nv[f * kCap + x] = (uint8_t)v;
+          atomicAdd(&s.acc[acc_idx(f, l, v)], 1);
+        }
+      }
+      __syncthreads();
+      for (int x = tid; x < C; x += nt) {
+        s.item_rep[x] = s.rep[x];
+        for (int f = 0; f < nf; ++f) s.iv[f * kCap + x] = s.nv[f * kCap + x];
+      }
+      __syncthreads();
+      items = C;
     }
-    __syncthreads();
-    items = C;
   }
   flush_acc(s, p.acc, nf, nl);
+}
+
+// ----------------------------------------------- warp-per-bucket path (offline)
+// One warp owns one bucket of <= kWarpCap events; no block barriers.  Events are
+// consumed in rounds of 32 in trace order; lanes holding the same value vector
+// in a round are grouped with __match_any_sync and their leader applies the
+// letters in lane order (so every slice u^D is stepped in trace order).  Leaves
+// and tree nodes live in warp-private shared-memory hash tables whose slots
+// store the index of a representative event (keys are compared in place).
+struct WarpSmem {
+  uint32_t *key[kMaxLevels];  // [kWarpCap]
+  uint8_t *let;               // [kWarpCap]
+  uint32_t *ltag;             // [kLeafSlots]: 0 empty, else rep event + 1
+  uint8_t *lstate;            // [kLeafSlots]
+  uint16_t *llist;            // [kWarpCap]
+  uint32_t *ntag[kMaxLevels]; // level l in [1, K-1]: [kNodeSlots]
+  uint32_t *nhist[kMaxLevels];// [kNodeSlots][nf][3]: two u16 counters per word
+  uint16_t *nlist[kMaxLevels];// [kNodeSlots]
+  uint32_t *cnt;              // [4]: leaves, nodes per level
+  uint32_t *acc;              // [kMaxFormulas][kMaxLevels + 1][6]
+};
+
+__host__ __device__ inline size_t warp_smem_bytes(int K, int nf) {
+  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) +
+             align16(2 * kWarpCap);
+  b += (size_t)(K - 1) * (align16(4 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) + align16(2 * kNodeSlots));
+  b += align16(16) + align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
+  return b;
+}
+
+__host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf) {
+  return align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) + kWarpsPerCta * warp_smem_bytes(K, nf);
+}
+
+__device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
+  WarpSmem w;
+  auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
+  for (int i = 0; i < kMaxLevels; ++i) w.key[i] = i < K ? (uint32_t *)take(4 * kWarpCap) : nullptr;
+  w.let = take(kWarpCap);
+  w.ltag = (uint32_t *)take(4 * kLeafSlots);
+  w.lstate = take(kLeafSlots);
+  w.llist = (uint16_t *)take(2 * kWarpCap);
+  for (int l = 0; l < kMaxLevels; ++l) { w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; }
+  for (int l = 1; l < K; ++l) {
+    w.ntag[l] = (uint32_t *)take(4 * kNodeSlots);
+    w.nhist[l] = (uint32_t *)take((size_t)4 * kNodeSlots * nf * 3);
+    w.nlist[l] = (uint16_t *)take(2 * kNodeSlots);
+  }
+  w.cnt = (uint32_t *)take(16);
+  w.acc = (uint32_t *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
+  return w;
+}
+
+template <int K>
+__device__ __forceinline__ uint32_t warp_hash(const WarpSmem &w, int e, int m) {
+  uint32_t h = 0x2545F491u;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (i < m) h = fmix32(h ^ w.key[i][e]) + 0x9e3779b9u * (i + 1);
+  return h;
+}
+
+template <int K>
+__device__ __forceinline__ bool warp_same(const WarpSmem &w, int a, int b, int m) {
+  bool eq = true;
+#pragma unroll
+  for (int i = 0; i < K; ++i)
+    if (i < m) eq &= w.key[i][a] == w.key[i][b];
+  return eq;
+}
+
+// find-or-insert of the m-key prefix of event e; slots store rep event + 1.
+// Returns the slot; *isnew when this call created it.  Lock-free: a claimed
+// slot's keys are those of its rep event, already in shared memory.
+template <int K>
+__device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const WarpSmem &w, int e, int m,
+                                          bool *isnew) {
+  uint32_t h = warp_hash<K>(w, e, m) & (uint32_t)(nslots - 1);
+  volatile uint32_t *vt = tag;
+  while (true) {
+    uint32_t t = vt[h];
+    if (t == 0) {
+      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
+      if (t == 0) { *isnew = true; return (int)h; }
+    }
+    if (warp_same<K>(w, (int)t - 1, e, m)) { *isnew = false; return (int)h; }
+    h = (h + 1) & (uint32_t)(nslots - 1);
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(32 * kWarpsPerCta) bucket_warp_kernel(BucketParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const DevProg *prog = p.prog;
+  const int nf = prog->nf, nq = prog->nq, A = 1 << prog->na;
+  uint8_t *sdelta = smem_raw;
+  uint8_t *slab = smem_raw + align16(kMaxStates * 256);
+  for (int i = threadIdx.x; i < nq * A; i += blockDim.x) sdelta[i] = prog->delta[i / A][i % A];
+  for (int i = threadIdx.x; i < kMaxFormulas * kMaxStates; i += blockDim.x)
+    slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const WarpSmem w = carve_warp(smem_raw + align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) +
+                                    (size_t)wid * warp_smem_bytes(K, nf), K, nf);
+  for (int i = lane; i < kLeafSlots; i += 32) w.ltag[i] = 0;
+  for (int l = 1; l < K; ++l) {
+    for (int i = lane; i < kNodeSlots; i += 32) w.ntag[l][i] = 0;
+    for (int i = lane; i < kNodeSlots * nf * 3; i += 32) w.nhist[l][i] = 0;
+  }
+  for (int i = lane; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += 32) w.acc[i] = 0;
+  if (lane < 4) w.cnt[lane] = 0;
+  __syncthreads();
+  const uint32_t q0 = prog->q0;
+  while (true) {
+    uint32_t b = 0;
+    if (lane == 0) b = atomicAdd(p.bucket_counter, 1u);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (b >= p.n_buckets) break;
+    const uint32_t start = p.bucket_off[b], cnt = p.bucket_off[b + 1] - start;
+    if (cnt == 0) continue;
+    if (cnt > (uint32_t)kWarpCap) {
+      if (lane == 0) {
+        const unsigned long long i = atomicAdd(&p.acc->medium_buckets, 1ull);
+        p.medium_list[i] = b;
+      }
+      continue;
+    }
+    for (uint32_t i = lane; i < cnt; i += 32) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) w.key[k][i] = p.key[k][start + i];
+      w.let[i] = p.let[start + i];
+    }
+    __syncwarp();
+    // a3 + a4: rounds of 32 events in trace order
+    for (uint32_t base = 0; base < cnt; base += 32) {
+      const int e = (int)(base + lane);
+      const bool act = e < (int)cnt;
+      const uint32_t am = __ballot_sync(0xffffffffu, act);
+      if (act) {
+        uint32_t peers;
+        if (K == 1) {
+          peers = __match_any_sync(am, w.key[0][e]);
+        } else {
+          const unsigned long long k01 = ((unsigned long long)w.key[1][e] << 32) | w.key[0][e];
+          peers = __match_any_sync(am, k01);
+          if (K == 3) peers &= __match_any_sync(am, w.key[K - 1][e]);
+        }
+        if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
+          bool isnew;
+          const int slot = warp_probe<K>(w.ltag, kLeafSlots, w, e, K, &isnew);
+          uint32_t q = isnew ? q0 : w.lstate[slot];
+          uint32_t m = peers;
+          while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            q = sdelta[q * A + w.let[base + i]];
+          }
+          w.lstate[slot] = (uint8_t)q;
+          if (isnew) w.llist[atomicAdd(&w.cnt[0], 1u)] = (uint16_t)slot;
+        }
+      }
+      __syncwarp();
+    }
+    // a5: leaf verdicts, depth K-1 grouping
+    const uint32_t nleaf = w.cnt[0];
+    for (uint32_t i = lane; i < nleaf; i += 32) {
+      const int slot = w.llist[i];
+      const int q = w.lstate[slot];
+      int nslot = -1;
+      if (K > 1) {
+        bool isnew;
+        nslot = warp_probe<K>(w.ntag[K - 1], kNodeSlots, w, (int)w.ltag[slot] - 1, K - 1, &isnew);
+        if (isnew) w.nlist[K - 1][atomicAdd(&w.cnt[K - 1], 1u)] = (uint16_t)nslot;
+      }
+      for (int f = 0; f < nf; ++f) {
+        const int v = slab[f * kMaxStates + q];
+        atomicAdd(&w.acc[(f * (kMaxLevels + 1) + K) * 6 + v], 1u);
+        if (K > 1) atomicAdd(&w.nhist[K - 1][(nslot * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+      }
+    }
+    __syncwarp();
+    for (int l = K - 1; l >= 1; --l) {
+      const uint32_t nn = w.cnt[l];
+      for (uint32_t i = lane; i < nn; i += 32) {
+        const int slot = w.nlist[l][i];
+        int pslot = -1;
+        if (l > 1) {
+          bool isnew;
+          pslot = warp_probe<K>(w.ntag[l - 1], kNodeSlots, w, (int)w.ntag[l][slot] - 1, l - 1, &isnew);
+          if (isnew) w.nlist[l - 1][atomicAdd(&w.cnt[l - 1], 1u)] = (uint16_t)pslot;
+        }
+        for (int f = 0; f < nf; ++f) {
+          const uint32_t *hw = &w.nhist[l][(slot * nf + f) * 3];
+          uint32_t h[6];
+#pragma unroll
+          for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
+          const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
+          atomicAdd(&w.acc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
+          if (l > 1) atomicAdd(&w.nhist[l - 1][(pslot * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+        }
+      }
+      __syncwarp();
+    }
+    // clear the tables touched by this bucket
+    for (uint32_t i = lane; i < nleaf; i += 32) w.ltag[w.llist[i]] = 0;
+    for (int l = 1; l < K; ++l) {
+      const uint32_t nn = w.cnt[l];
+      for (uint32_t i = lane; i < nn; i += 32) {
+        const int slot = w.nlist[l][i];
+        w.ntag[l][slot] = 0;
+        for (int x = 0; x < nf * 3; ++x) w.nhist[l][slot * nf * 3 + x] = 0;
+      }
+    }
+    __syncwarp();
+    if (lane < 4) w.cnt[lane] = 0;
+    __syncwarp();
+  }
+  for (int i = lane; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += 32) {
+    const uint32_t v = w.acc[i];
+    const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), bb = i % 6;
+    if (v && f < nf && l >= 1 && l <= K) atomicAdd(&p.acc->hist[f][l][bb], (unsigned long long)v);
+  }
 }
 
 // ----------------------------------------------- global tables
@@ -829,17 +1053,31 @@ cudaError_t launch_bucket_scan(const uint32_t *count, uint32_t *off, uint32_t n,
   LTL4C_LAUNCH(kKBucketScan, bucket_scan_kernel<<<1, 1024, 0, L.stream>>>(count, off, n));
 }
 
-cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, const Launcher &L) {
+cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, false);
   switch (K) {
     case 1: cudaFuncSetAttribute(bucket_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<1><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
     case 2: cudaFuncSetAttribute(bucket_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<2><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<2><<<grid, kBucketThreads, sm, L.stream>>>(p));
     default: cudaFuncSetAttribute(bucket_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<3><<<p.n_buckets, kBucketThreads, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
   }
 }
+
+cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
+  const size_t sm = warp_cta_smem_bytes(K, nf);
+  switch (K) {
+    case 1: cudaFuncSetAttribute(bucket_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<1><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+    case 2: cudaFuncSetAttribute(bucket_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<2><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+    default: cudaFuncSetAttribute(bucket_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<3><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+  }
+}
+
+size_t bucket_warp_smem(int K, int nf) { return warp_cta_smem_bytes(K, nf); }
 
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, true);

@@ -8,9 +8,13 @@ namespace ltl4c {
 
 constexpr int kTileEv = 4096;        // events per partition tile
 constexpr int kPartThreads = 256;    // 8 warps x 16 rounds x 32 lanes
-constexpr int kMaxDigitBits = 7;     // <= 128 digits per stable partition pass
+constexpr int kMaxDigitBits = 8;     // <= 256 digits per stable partition pass
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory
 constexpr int kBucketThreads = 256;
+constexpr int kWarpCap = 512;        // events per warp-processed bucket
+constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
+constexpr int kNodeSlots = 512;      // warp node table per inner level (<= 512 nodes: never full)
+constexpr int kWarpsPerCta = 4;
 
 // One stable LSD pass of the hash(k0) bucket partition (a2, SortTrace).
 struct PartParams {
@@ -50,6 +54,8 @@ struct BucketParams {
   const uint32_t *list;                 // if set: CTA i processes bucket list[i]
   const unsigned long long *list_len;   // number of entries in list
   uint32_t *oversize_list;              // fast path: buckets larger than kCap
+  uint32_t *medium_list;                // warp path: buckets larger than kWarpCap
+  uint32_t *bucket_counter;             // warp path: dynamic bucket scheduler
   const DevProg *prog;
   DevAcc *acc;
   DevTables tab;
@@ -78,6 +84,7 @@ enum KernelId {
   kKBucketGlobal,
   kKFinalize,
   kKRehash,
+  kKBucketWarp,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -86,7 +93,9 @@ cudaError_t launch_part_count(const PartParams &p, const Launcher &L);
 cudaError_t launch_part_scan(const PartParams &p, const Launcher &L);
 cudaError_t launch_part_scatter(const PartParams &p, const Launcher &L);
 cudaError_t launch_bucket_scan(const uint32_t *count, uint32_t *off, uint32_t n, const Launcher &L);
-cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, const Launcher &L);
+cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+size_t bucket_warp_smem(int K, int nf);
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);

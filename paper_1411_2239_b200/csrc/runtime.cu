@@ -104,7 +104,8 @@ struct ltl4c_state {
   DevBuf<unsigned long long> d_nvalid;
   DevBuf<uint32_t> bufkey[2][kMaxLevels];
   DevBuf<uint8_t> buflet[2];
-  DevBuf<uint32_t> counts, totals, bucket_count, bucket_off, oversize_list;
+  DevBuf<uint32_t> counts, totals, bucket_count, bucket_off, oversize_list, medium_list, sched;
+  int n_sms = 148, warp_ctas_per_sm = 1;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
@@ -244,7 +245,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     if (r) return r;
   }
   if (N > 0) {
-    const uint64_t target = std::max<uint64_t>(2, (3 * N + kCap - 1) / kCap);
+    const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
     const int B = std::min(24, std::max(1, ceil_log2(target)));
     const int P = (B + kMaxDigitBits - 1) / kMaxDigitBits;
     const uint32_t NB = 1u << B;
@@ -258,7 +259,10 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     CU(st->bucket_count.ensure(NB));
     CU(st->bucket_off.ensure((size_t)NB + 1));
     CU(st->oversize_list.ensure(NB));
+    CU(st->medium_list.ensure(NB));
+    CU(st->sched.ensure(4));
     CU(cudaMemsetAsync(st->bucket_count.p, 0, sizeof(uint32_t) * NB, s));
+    CU(cudaMemsetAsync(st->sched.p, 0, sizeof(uint32_t) * 4, s));
     int lo = 0;
     for (int pass = 0; pass < P; ++pass) {
       const int width = (B - lo + (P - pass) - 1) / (P - pass);
@@ -295,10 +299,19 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     bp.bucket_off = st->bucket_off.p;
     bp.n_buckets = NB;
     bp.oversize_list = st->oversize_list.p;
+    bp.medium_list = st->medium_list.p;
+    bp.bucket_counter = st->sched.p;
     bp.prog = st->d_prog.p;
     bp.acc = st->d_acc.p;
     if (!online) {
-      CU(launch_bucket_fast(bp, K, (int)prog->n_formulas, L));
+      // warp per bucket; buckets above kWarpCap events go to the CTA kernel,
+      // above kCap to the chunked global path
+      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas,
+                            (uint32_t)std::min<uint64_t>(NB, (uint64_t)st->n_sms * st->warp_ctas_per_sm), L));
+      BucketParams mp = bp;
+      mp.list = st->medium_list.p;
+      mp.list_len = &st->d_acc.p->medium_buckets;
+      CU(launch_bucket_fast(mp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
       CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
       CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
@@ -475,6 +488,14 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
         if (st->bufkey[i][l].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
       if (st->buflet[i].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
     }
+  }
+  st->n_sms = dp.multiProcessorCount;
+  {
+    int occ = 1;
+    // occupancy of the warp-per-bucket kernel for this program's (K, F)
+    const size_t sm = bucket_warp_smem((int)prog->n_levels, (int)prog->n_formulas);
+    occ = (int)std::max<size_t>(1, std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024)));
+    st->warp_ctas_per_sm = occ;
   }
   cudaSetDevice(prev);
   *out = st;
