@@ -29,229 +29,15 @@
 #include <cstdint>
 
 #include "kernels.cuh"
+#include "util.cuh"
 
 namespace ltl4c {
 
-const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter",
-                                                "bucket_scan", "bucket_fast", "bucket_global",
-                                                "finalize", "rehash", "bucket_warp"};
+const char *const kKernelNames[kKNumKernels] = {"part_hist", "part_onesweep", "bucket_bounds",
+                                                "bucket_warp", "bucket_fast", "bucket_global",
+                                                "finalize", "rehash"};
 
 namespace {
-
-__device__ __forceinline__ uint32_t lanemask_lt() {
-  uint32_t m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// ------------------------------------------------------------------ scans
-// Exclusive scan of n (<= blockDim * per) values held in smem `a` (u32), in place.
-// Returns the total.  All threads of the block must call it.
-__device__ uint32_t block_exclusive_scan(uint32_t *a, int n, uint32_t *warp_tot) {
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5;
-  const int per = (n + nt - 1) / nt;
-  const int lo = min(n, tid * per), hi = min(n, lo + per);
-  uint32_t s = 0;
-  for (int i = lo; i < hi; ++i) s += a[i];
-  uint32_t x = s;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-    if (lane >= d) x += y;
-  }
-  if (lane == 31) warp_tot[wid] = x;
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = nt >> 5;
-    uint32_t w = lane < nw ? warp_tot[lane] : 0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
-      if (lane >= d) w += y;
-    }
-    if (lane < nw) warp_tot[lane] = w;  // inclusive
-  }
-  __syncthreads();
-  uint32_t base = (x - s) + (wid ? warp_tot[wid - 1] : 0);
-  for (int i = lo; i < hi; ++i) {
-    uint32_t v = a[i];
-    a[i] = base;
-    base += v;
-  }
-  uint32_t total = warp_tot[(nt >> 5) - 1];
-  __syncthreads();
-  return total;
-}
-
-// ------------------------------------------------------------------ partition
-__global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartParams p) {
-  extern __shared__ uint32_t bhist[];  // 1 << bits bins when small (pass 0)
-  __shared__ uint32_t dcnt[1 << kMaxDigitBits];
-  __shared__ uint32_t nvalid;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t ndig = 1u << p.width, dmask = ndig - 1u;
-  const bool small_hist = p.first && p.bits <= 13;
-  const uint32_t nb = 1u << p.bits;
-  for (uint32_t d = tid; d < ndig; d += blockDim.x) dcnt[d] = 0;
-  if (small_hist)
-    for (uint32_t b = tid; b < nb; b += blockDim.x) bhist[b] = 0;
-  if (tid == 0) nvalid = 0;
-  __syncthreads();
-  unsigned long long n = p.n;
-  if (p.n_dev) n = min(n, *p.n_dev);
-  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv + (unsigned long long)wid * 512;
-  uint32_t myvalid = 0;
-  for (int r = 0; r < 16; ++r) {
-    const unsigned long long j = base + r * 32 + lane;
-    bool valid = j < n;
-    uint32_t k0 = 0;
-    if (valid) {
-      k0 = p.in_key[0][j];
-      if (p.first)
-        for (int i = 0; i < p.K; ++i) valid &= p.in_key[i][j] != kAbsent;
-    }
-    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t b = bucket_of(k0, p.bits);
-      const uint32_t d = (b >> p.lo) & dmask;
-      const uint32_t peers = __match_any_sync(vm, d);
-      if ((peers & lanemask_lt()) == 0) atomicAdd(&dcnt[d], __popc(peers));
-      if (p.first) {
-        const uint32_t bp = __match_any_sync(vm, b);
-        if ((bp & lanemask_lt()) == 0) {
-          if (small_hist) atomicAdd(&bhist[b], __popc(bp));
-          else atomicAdd(&p.bucket_count[b], __popc(bp));
-        }
-      }
-    }
-    myvalid += valid;
-  }
-  if (p.first) {
-    for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
-    if (lane == 0) atomicAdd(&nvalid, myvalid);
-  }
-  __syncthreads();
-  for (uint32_t d = tid; d < ndig; d += blockDim.x)
-    p.counts[(size_t)d * p.n_tiles + blockIdx.x] = dcnt[d];
-  if (p.first) {
-    if (tid == 0 && nvalid) {
-      atomicAdd(&p.acc->events_bound, (unsigned long long)nvalid);
-      atomicAdd(p.nvalid, (unsigned long long)nvalid);
-    }
-    if (small_hist)
-      for (uint32_t b = tid; b < nb; b += blockDim.x)
-        if (bhist[b]) atomicAdd(&p.bucket_count[b], bhist[b]);
-  }
-}
-
-// exclusive scan of counts[d][0..n_tiles) (one CTA per digit), totals[d]
-__global__ void __launch_bounds__(1024) part_scan_kernel(PartParams p) {
-  __shared__ uint32_t buf[1024];
-  __shared__ uint32_t wt[32];
-  uint32_t *row = p.counts + (size_t)blockIdx.x * p.n_tiles;
-  uint32_t carry = 0;
-  for (uint32_t off = 0; off < p.n_tiles; off += 1024) {
-    const uint32_t i = off + threadIdx.x;
-    buf[threadIdx.x] = i < p.n_tiles ? row[i] : 0;
-    __syncthreads();
-    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
-    if (i < p.n_tiles) row[i] = buf[threadIdx.x] + carry;
-    carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) p.totals[blockIdx.x] = carry;
-}
-
-template <int K>
-__global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartParams p) {
-  __shared__ uint32_t dbase[1 << kMaxDigitBits];
-  __shared__ uint16_t wcnt[kPartThreads / 32][1 << kMaxDigitBits];
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const uint32_t ndig = 1u << p.width, dmask = ndig - 1u;
-  // digit bases: exclusive scan of the digit totals + this tile's prefix
-  if (tid == 0) {
-    uint32_t run = 0;
-    for (uint32_t d = 0; d < ndig; ++d) {
-      dbase[d] = run;
-      run += p.totals[d];
-    }
-  }
-  for (uint32_t d = tid; d < ndig * (kPartThreads / 32); d += blockDim.x)
-    wcnt[d / ndig][d % ndig] = 0;
-  __syncthreads();
-  for (uint32_t d = tid; d < ndig; d += blockDim.x)
-    dbase[d] += p.counts[(size_t)d * p.n_tiles + blockIdx.x];
-  unsigned long long n = p.n;
-  if (p.n_dev) n = min(n, *p.n_dev);
-  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv + (unsigned long long)wid * 512;
-  uint32_t kv[16][K];
-  uint8_t lv[16];
-  uint16_t dig[16], rank[16];
-  uint32_t validmask = 0;
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const unsigned long long j = base + r * 32 + lane;
-    bool valid = j < n;
-    if (valid) {
-#pragma unroll
-      for (int i = 0; i < K; ++i) kv[r][i] = p.in_key[i][j];
-      lv[r] = p.in_let[j];
-      if (p.first) {
-#pragma unroll
-        for (int i = 0; i < K; ++i) valid &= kv[r][i] != kAbsent;
-      }
-    }
-    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t d = (bucket_of(kv[r][0], p.bits) >> p.lo) & dmask;
-      const uint32_t peers = __match_any_sync(vm, d);
-      const uint32_t old = wcnt[wid][d];
-      rank[r] = (uint16_t)(old + __popc(peers & lanemask_lt()));
-      dig[r] = (uint16_t)d;
-      __syncwarp(vm);
-      if ((peers & lanemask_lt()) == 0) wcnt[wid][d] = (uint16_t)(old + __popc(peers));
-      __syncwarp(vm);
-      validmask |= 1u << r;
-    }
-  }
-  __syncthreads();
-  // exclusive prefix over warps, per digit (in place)
-  for (uint32_t d = tid; d < ndig; d += blockDim.x) {
-    uint32_t run = 0;
-    for (int w = 0; w < kPartThreads / 32; ++w) {
-      const uint32_t c = wcnt[w][d];
-      wcnt[w][d] = (uint16_t)run;
-      run += c;
-    }
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    if (!((validmask >> r) & 1)) continue;
-    const uint32_t d = dig[r];
-    const size_t pos = (size_t)dbase[d] + wcnt[wid][d] + rank[r];
-#pragma unroll
-    for (int i = 0; i < K; ++i) p.out_key[i][pos] = kv[r][i];
-    p.out_let[pos] = lv[r];
-  }
-}
-
-// exclusive scan of n bucket counts -> off[0..n] (single CTA)
-__global__ void __launch_bounds__(1024) bucket_scan_kernel(const uint32_t *count, uint32_t *off, uint32_t n) {
-  __shared__ uint32_t buf[1024];
-  __shared__ uint32_t wt[32];
-  uint32_t carry = 0;
-  for (uint32_t o = 0; o < n; o += 1024) {
-    const uint32_t i = o + threadIdx.x;
-    buf[threadIdx.x] = i < n ? count[i] : 0;
-    __syncthreads();
-    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
-    if (i < n) off[i] = buf[threadIdx.x] + carry;
-    carry += tot;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) off[n] = carry;
-}
 
 // ------------------------------------------------------------------ buckets
 struct Smem {
@@ -573,29 +359,33 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 // letters in lane order (so every slice u^D is stepped in trace order).  Leaves
 // and tree nodes live in warp-private shared-memory hash tables whose slots
 // store the index of a representative event (keys are compared in place).
+// The next bucket's events are loaded into registers while the current one is
+// processed.
+constexpr int kPerLane = kWarpCap / 32;
+
 struct WarpSmem {
-  uint32_t *key[kMaxLevels];  // [kWarpCap]
-  uint8_t *let;               // [kWarpCap]
-  uint32_t *ltag;             // [kLeafSlots]: 0 empty, else rep event + 1
-  uint8_t *lstate;            // [kLeafSlots]
-  uint16_t *llist;            // [kWarpCap]
-  uint32_t *ntag[kMaxLevels]; // level l in [1, K-1]: [kNodeSlots]
-  uint32_t *nhist[kMaxLevels];// [kNodeSlots][nf][3]: two u16 counters per word
-  uint16_t *nlist[kMaxLevels];// [kNodeSlots]
-  uint32_t *cnt;              // [4]: leaves, nodes per level
-  uint32_t *acc;              // [kMaxFormulas][kMaxLevels + 1][6]
+  uint32_t *key[kMaxLevels];   // [kWarpCap]
+  uint8_t *let;                // [kWarpCap]
+  uint16_t *ltag;              // [kLeafSlots]: 0 empty, else rep event + 1
+  uint8_t *lstate;             // [kLeafSlots]
+  uint16_t *llist;             // [kWarpCap]
+  uint16_t *ntag[kMaxLevels];  // level l in [1, K-1]: [kNodeSlots]
+  uint32_t *nhist[kMaxLevels]; // [kNodeSlots][nf][3]: two u16 counters per word
+  uint16_t *nlist[kMaxLevels]; // [kNodeSlots]
+  uint32_t *cnt;               // [4]: leaves, nodes per level
+  uint32_t *acc;               // [kMaxFormulas][kMaxLevels + 1][6]
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int K, int nf) {
-  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) +
+  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(2 * kLeafSlots) + align16(kLeafSlots) +
              align16(2 * kWarpCap);
-  b += (size_t)(K - 1) * (align16(4 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) + align16(2 * kNodeSlots));
+  b += (size_t)(K - 1) * (align16(2 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) + align16(2 * kNodeSlots));
   b += align16(16) + align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
   return b;
 }
 
-__host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf) {
-  return align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) + kWarpsPerCta * warp_smem_bytes(K, nf);
+__host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf, int warps) {
+  return align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) + (size_t)warps * warp_smem_bytes(K, nf);
 }
 
 __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
@@ -603,12 +393,12 @@ __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
   auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
   for (int i = 0; i < kMaxLevels; ++i) w.key[i] = i < K ? (uint32_t *)take(4 * kWarpCap) : nullptr;
   w.let = take(kWarpCap);
-  w.ltag = (uint32_t *)take(4 * kLeafSlots);
+  w.ltag = (uint16_t *)take(2 * kLeafSlots);
   w.lstate = take(kLeafSlots);
   w.llist = (uint16_t *)take(2 * kWarpCap);
   for (int l = 0; l < kMaxLevels; ++l) { w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; }
   for (int l = 1; l < K; ++l) {
-    w.ntag[l] = (uint32_t *)take(4 * kNodeSlots);
+    w.ntag[l] = (uint16_t *)take(2 * kNodeSlots);
     w.nhist[l] = (uint32_t *)take((size_t)4 * kNodeSlots * nf * 3);
     w.nlist[l] = (uint16_t *)take(2 * kNodeSlots);
   }
@@ -639,14 +429,14 @@ __device__ __forceinline__ bool warp_same(const WarpSmem &w, int a, int b, int m
 // Returns the slot; *isnew when this call created it.  Lock-free: a claimed
 // slot's keys are those of its rep event, already in shared memory.
 template <int K>
-__device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const WarpSmem &w, int e, int m,
+__device__ __forceinline__ int warp_probe(uint16_t *tag, int nslots, const WarpSmem &w, int e, int m,
                                           bool *isnew) {
   uint32_t h = warp_hash<K>(w, e, m) & (uint32_t)(nslots - 1);
-  volatile uint32_t *vt = tag;
+  volatile uint16_t *vt = tag;
   while (true) {
-    uint32_t t = vt[h];
+    unsigned short t = vt[h];
     if (t == 0) {
-      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
+      t = atomicCAS(&tag[h], (unsigned short)0, (unsigned short)(e + 1));
       if (t == 0) { *isnew = true; return (int)h; }
     }
     if (warp_same<K>(w, (int)t - 1, e, m)) { *isnew = false; return (int)h; }
@@ -655,7 +445,7 @@ __device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const WarpS
 }
 
 template <int K>
-__global__ void __launch_bounds__(32 * kWarpsPerCta) bucket_warp_kernel(BucketParams p) {
+__global__ void __launch_bounds__(128) bucket_warp_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nq = prog->nq, A = 1 << prog->na;
@@ -676,30 +466,53 @@ __global__ void __launch_bounds__(32 * kWarpsPerCta) bucket_warp_kernel(BucketPa
   if (lane < 4) w.cnt[lane] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
-  while (true) {
-    uint32_t b = 0;
-    if (lane == 0) b = atomicAdd(p.bucket_counter, 1u);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    if (b >= p.n_buckets) break;
-    const uint32_t start = p.bucket_off[b], cnt = p.bucket_off[b + 1] - start;
-    if (cnt == 0) continue;
-    if (cnt > (uint32_t)kWarpCap) {
-      if (lane == 0) {
-        const unsigned long long i = atomicAdd(&p.acc->medium_buckets, 1ull);
-        p.medium_list[i] = b;
+  // prefetch registers for the next bucket
+  uint32_t rk[K][kPerLane];
+  uint8_t rl[kPerLane];
+  auto grab = [&](uint32_t &b, uint32_t &start, uint32_t &cnt) {
+    while (true) {
+      b = 0;
+      if (lane == 0) b = atomicAdd(p.bucket_counter, 1u);
+      b = __shfl_sync(0xffffffffu, b, 0);
+      if (b >= p.n_buckets) { cnt = 0; return false; }
+      start = p.bucket_off[b];
+      cnt = p.bucket_off[b + 1] - start;
+      if (cnt == 0) continue;
+      if (cnt > (uint32_t)kWarpCap) {
+        if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = b;
+        continue;
       }
-      continue;
-    }
-    for (uint32_t i = lane; i < cnt; i += 32) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) w.key[k][i] = p.key[k][start + i];
-      w.let[i] = p.let[start + i];
+      for (int j = 0; j < kPerLane; ++j) {
+        const uint32_t i = j * 32 + lane;
+        if (i < cnt) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) rk[k][j] = p.key[k][start + i];
+          rl[j] = p.let[start + i];
+        }
+      }
+      return true;
+    }
+  };
+  uint32_t b, start, cnt;
+  bool have = grab(b, start, cnt);
+  while (have) {
+    const uint32_t cur_cnt = cnt;
+#pragma unroll
+    for (int j = 0; j < kPerLane; ++j) {
+      const uint32_t i = j * 32 + lane;
+      if (i < cur_cnt) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) w.key[k][i] = rk[k][j];
+        w.let[i] = rl[j];
+      }
     }
     __syncwarp();
+    have = grab(b, start, cnt);  // loads of the next bucket overlap the work below
     // a3 + a4: rounds of 32 events in trace order
-    for (uint32_t base = 0; base < cnt; base += 32) {
+    for (uint32_t base = 0; base < cur_cnt; base += 32) {
       const int e = (int)(base + lane);
-      const bool act = e < (int)cnt;
+      const bool act = e < (int)cur_cnt;
       const uint32_t am = __ballot_sync(0xffffffffu, act);
       if (act) {
         uint32_t peers;
@@ -1035,24 +848,6 @@ __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *
     return e_;                                         \
   } while (0)
 
-cudaError_t launch_part_count(const PartParams &p, const Launcher &L) {
-  const size_t sm = (p.first && p.bits <= 13) ? sizeof(uint32_t) << p.bits : 0;
-  LTL4C_LAUNCH(kKPartCount, part_count_kernel<<<p.n_tiles, kPartThreads, sm, L.stream>>>(p));
-}
-cudaError_t launch_part_scan(const PartParams &p, const Launcher &L) {
-  LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width, 1024, 0, L.stream>>>(p));
-}
-cudaError_t launch_part_scatter(const PartParams &p, const Launcher &L) {
-  switch (p.K) {
-    case 1: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<1><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
-    case 2: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<2><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
-    default: LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<3><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
-  }
-}
-cudaError_t launch_bucket_scan(const uint32_t *count, uint32_t *off, uint32_t n, const Launcher &L) {
-  LTL4C_LAUNCH(kKBucketScan, bucket_scan_kernel<<<1, 1024, 0, L.stream>>>(count, off, n));
-}
-
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, false);
   switch (K) {
@@ -1066,18 +861,19 @@ cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t gr
 }
 
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
-  const size_t sm = warp_cta_smem_bytes(K, nf);
+  const int warps = p.warps_per_cta;
+  const size_t sm = warp_cta_smem_bytes(K, nf, warps);
   switch (K) {
     case 1: cudaFuncSetAttribute(bucket_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<1><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<1><<<grid, 32 * warps, sm, L.stream>>>(p));
     case 2: cudaFuncSetAttribute(bucket_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<2><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<2><<<grid, 32 * warps, sm, L.stream>>>(p));
     default: cudaFuncSetAttribute(bucket_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<3><<<grid, 32 * kWarpsPerCta, sm, L.stream>>>(p));
+      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<3><<<grid, 32 * warps, sm, L.stream>>>(p));
   }
 }
 
-size_t bucket_warp_smem(int K, int nf) { return warp_cta_smem_bytes(K, nf); }
+size_t bucket_warp_smem(int K, int nf, int warps) { return warp_cta_smem_bytes(K, nf, warps); }
 
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, true);

@@ -7,31 +7,32 @@
 namespace ltl4c {
 
 constexpr int kTileEv = 4096;        // events per partition tile
-constexpr int kPartThreads = 256;    // 8 warps x 16 rounds x 32 lanes
+constexpr int kPartThreads = 512;    // 16 warps x 8 rounds x 32 lanes
 constexpr int kMaxDigitBits = 8;     // <= 256 digits per stable partition pass
-constexpr int kCap = 2048;           // events per bucket chunk held in shared memory
+constexpr int kMaxPasses = 3;        // bucket bits <= 24
+constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
 constexpr int kWarpCap = 512;        // events per warp-processed bucket
 constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
 constexpr int kNodeSlots = 512;      // warp node table per inner level (<= 512 nodes: never full)
-constexpr int kWarpsPerCta = 4;
 
-// One stable LSD pass of the hash(k0) bucket partition (a2, SortTrace).
-struct PartParams {
-  const uint32_t *in_key[kMaxLevels];
+// The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
+// (a1 + a2).  One histogram pass, then one decoupled-look-back scatter per
+// digit (onesweep): pass p sorts by digit bits [lo[p], lo[p] + width[p]).
+struct PartPlan {
+  const uint32_t *in_key[kMaxLevels];   // the batch (pass 0 input)
   const uint8_t *in_let;
-  uint32_t *out_key[kMaxLevels];
-  uint8_t *out_let;
-  unsigned long long n;                 // input events (upper bound)
-  const unsigned long long *n_dev;      // if set: input events = min(n, *n_dev)
-  int K, bits, lo, width;               // bucket bits; digit = bits [lo, lo + width)
-  int first;                            // pass 0: epsilon filter + bucket histogram
-  uint32_t n_tiles;
-  uint32_t *counts;                     // [1 << width][n_tiles], scanned in place
-  uint32_t *totals;                     // [1 << width]
-  uint32_t *bucket_count;               // [1 << bits] (pass 0)
+  uint32_t *buf_key[2][kMaxLevels];     // ping-pong outputs
+  uint8_t *buf_let[2];
+  unsigned long long n;                 // events in the batch
+  uint32_t n_tiles;                     // ceil(n / kTileEv)
+  int K, bits, passes;
+  int lo[kMaxPasses], width[kMaxPasses];
+  uint32_t *digit_hist;                 // [kMaxPasses][256] digit totals (bound events)
+  unsigned long long *status;           // [n_tiles][256] look-back words (zeroed per pass)
+  uint32_t *tile_ctr;                   // [kMaxPasses] dynamic tile ids
+  unsigned long long *nvalid;           // bound events of this batch
   DevAcc *acc;
-  unsigned long long *nvalid;           // per-verify count of bound events (pass 0 adds)
 };
 
 // Carried / per-verify global tables of the global (chunked) bucket path.
@@ -50,6 +51,7 @@ struct BucketParams {
   const uint32_t *key[kMaxLevels];      // partitioned events (bucket order, stable)
   const uint8_t *let;
   const uint32_t *bucket_off;           // [n_buckets + 1]
+  int warps_per_cta;
   uint32_t n_buckets;
   const uint32_t *list;                 // if set: CTA i processes bucket list[i]
   const unsigned long long *list_len;   // number of entries in list
@@ -76,26 +78,24 @@ struct Launcher {
 };
 
 enum KernelId {
-  kKPartCount = 0,
-  kKPartScan,
-  kKPartScatter,
-  kKBucketScan,
+  kKPartHist = 0,
+  kKPartOnesweep,
+  kKBucketBounds,
+  kKBucketWarp,
   kKBucketFast,
   kKBucketGlobal,
   kKFinalize,
   kKRehash,
-  kKBucketWarp,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
 
-cudaError_t launch_part_count(const PartParams &p, const Launcher &L);
-cudaError_t launch_part_scan(const PartParams &p, const Launcher &L);
-cudaError_t launch_part_scatter(const PartParams &p, const Launcher &L);
-cudaError_t launch_bucket_scan(const uint32_t *count, uint32_t *off, uint32_t n, const Launcher &L);
+cudaError_t launch_part_hist(const PartPlan &p, const Launcher &L);
+cudaError_t launch_part_onesweep(const PartPlan &p, int pass, const Launcher &L);
+cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
-size_t bucket_warp_smem(int K, int nf);
+size_t bucket_warp_smem(int K, int nf, int warps);
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);

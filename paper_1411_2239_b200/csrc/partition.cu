@@ -1,0 +1,291 @@
+// partition.cu -- a1 (epsilon) + a2 (SortTrace) of arXiv:1411.2239 Alg. 1
+// on sm_100a: a STABLE LSD partition of the bound events of a
+// batch by bucket = top `bits` bits of hash(k0).
+//
+//   part_hist      one read of the keys: epsilon filter (Eq. D: an event
+//                  binds a value vector only if every guard key is present) and
+//                  the digit totals of every pass.
+//   part_onesweep  one kernel per pass: a 4096-event tile is staged in shared
+//                  memory, ranked stably by digit (warp __match_any_sync rounds
+//                  in trace order + per-warp digit counters), its global offsets
+//                  come from a decoupled look-back over the preceding tiles
+//                  (dynamic tile ids keep the chain deadlock-free), and it is
+//                  written back digit run by digit run (coalesced).
+//   bucket_bounds  bucket offsets mu from the final order.
+//
+// Stability keeps every slice u^D in trace order (reading A15); a bucket holds
+// whole level-0 subtrees because every tree node's key starts with k0.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "util.cuh"
+
+namespace ltl4c {
+namespace {
+
+constexpr int kPWarps = kPartThreads / 32;
+constexpr int kRounds = kTileEv / kPartThreads;  // rounds of 32 events per warp
+constexpr unsigned long long kFlagA = 1ull << 62;  // tile aggregate published
+constexpr unsigned long long kFlagP = 2ull << 62;  // inclusive prefix published
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
+
+template <int K>
+__global__ void __launch_bounds__(kPartThreads) part_hist_kernel(PartPlan pl) {
+  __shared__ uint32_t h[kMaxPasses][256];
+  __shared__ uint32_t nv;
+  const int tid = threadIdx.x, lane = tid & 31;
+  for (int i = tid; i < kMaxPasses * 256; i += kPartThreads) (&h[0][0])[i] = 0;
+  if (tid == 0) nv = 0;
+  __syncthreads();
+  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv;
+  uint32_t myvalid = 0;
+  for (int r = 0; r < kRounds; ++r) {
+    const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
+    bool valid = j < pl.n;
+    uint32_t k0 = 0;
+    if (valid) {
+      k0 = pl.in_key[0][j];
+#pragma unroll
+      for (int i = 0; i < K; ++i) valid &= pl.in_key[i][j] != kAbsent;
+    }
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t b = bucket_of(k0, pl.bits);
+      for (int p = 0; p < pl.passes; ++p) {
+        const uint32_t d = (b >> pl.lo[p]) & ((1u << pl.width[p]) - 1u);
+        const uint32_t peers = __match_any_sync(vm, d);
+        if ((peers & lanemask_lt()) == 0) atomicAdd(&h[p][d], __popc(peers));
+      }
+    }
+    myvalid += valid;
+  }
+  for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
+  if (lane == 0 && myvalid) atomicAdd(&nv, myvalid);
+  __syncthreads();
+  for (int i = tid; i < pl.passes * 256; i += kPartThreads) {
+    const uint32_t c = (&h[0][0])[i];
+    if (c) atomicAdd(&pl.digit_hist[i], c);
+  }
+  if (tid == 0 && nv) {
+    atomicAdd(pl.nvalid, (unsigned long long)nv);
+    atomicAdd(&pl.acc->events_bound, (unsigned long long)nv);
+  }
+}
+
+template <int K>
+struct SweepSmem {
+  uint32_t kin[K][kTileEv];
+  uint32_t kout[K][kTileEv];
+  uint8_t lin[kTileEv];
+  uint8_t lout[kTileEv];
+  uint8_t dig[kTileEv];
+  uint8_t dout[kTileEv];
+  uint16_t rank[kTileEv];
+  uint16_t wcnt[kPWarps][256];
+  uint32_t loc[256];     // tile-local exclusive offset of each digit
+  uint32_t tcnt[256];    // tile count of each digit
+  uint32_t gbase[256];   // global position of the tile's digit run
+  uint32_t pbase[256];   // exclusive scan of the pass's digit totals
+  uint32_t wt[32];
+  uint32_t tile;
+  uint32_t ntile;        // bound events in this tile
+};
+
+template <int K>
+__global__ void __launch_bounds__(kPartThreads) part_onesweep_kernel(PartPlan pl, int pass) {
+  extern __shared__ __align__(16) uint8_t raw[];
+  SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const bool first = pass == 0;
+  const uint32_t *const *in_key = first ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
+  const uint8_t *in_let = first ? pl.in_let : pl.buf_let[(pass - 1) & 1];
+  uint32_t *const *out_key = pl.buf_key[pass & 1];
+  uint8_t *out_let = pl.buf_let[pass & 1];
+  const unsigned long long n = first ? pl.n : *pl.nvalid;
+  const uint32_t dmask = (1u << pl.width[pass]) - 1u;
+  const int lo = pl.lo[pass];
+  if (tid == 0) s.tile = atomicAdd(&pl.tile_ctr[pass], 1u);
+  if (tid < 256) {
+    s.pbase[tid] = pl.digit_hist[pass * 256 + tid];
+    s.loc[tid] = 0;
+  }
+  for (int i = tid; i < kPWarps * 256; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
+  __syncthreads();
+  const uint32_t tile = s.tile;
+  const unsigned long long base = (unsigned long long)tile * kTileEv;
+  // stage the tile (coalesced loads)
+  for (int i = tid; i < kTileEv; i += kPartThreads) {
+    const unsigned long long j = base + i;
+    if (j < n) {
+#pragma unroll
+      for (int k = 0; k < K; ++k) s.kin[k][i] = in_key[k][j];
+      s.lin[i] = in_let[j];
+    } else {
+#pragma unroll
+      for (int k = 0; k < K; ++k) s.kin[k][i] = kAbsent;
+    }
+  }
+  // pass base offsets: exclusive scan of the digit totals (first 256 threads)
+  if (tid < 256) {
+    uint32_t x = s.pbase[tid];
+    uint32_t inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) s.wt[wid] = inc;
+    s.pbase[tid] = inc - x;
+  }
+  __syncthreads();
+  if (tid < 256) {
+    uint32_t add = 0;
+    for (int w = 0; w < wid; ++w) add += s.wt[w];
+    s.pbase[tid] += add;
+  }
+  // stable rank: warp w owns events [w * 256, (w + 1) * 256) in rounds of 32
+  for (int r = 0; r < kRounds; ++r) {
+    const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
+    bool valid = true;
+#pragma unroll
+    for (int k = 0; k < K; ++k) valid &= s.kin[k][e] != kAbsent;
+    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
+    if (valid) {
+      const uint32_t d = (bucket_of(s.kin[0][e], pl.bits) >> lo) & dmask;
+      const uint32_t peers = __match_any_sync(vm, d);
+      const uint32_t old = s.wcnt[wid][d];
+      s.rank[e] = (uint16_t)(old + __popc(peers & lanemask_lt()));
+      s.dig[e] = (uint8_t)d;
+      __syncwarp(vm);
+      if ((peers & lanemask_lt()) == 0) s.wcnt[wid][d] = (uint16_t)(old + __popc(peers));
+      __syncwarp(vm);
+    } else {
+      s.rank[e] = 0xFFFF;
+    }
+  }
+  __syncthreads();
+  if (tid < 256) {  // per digit: exclusive over warps, tile total
+    uint32_t run = 0;
+    for (int w = 0; w < kPWarps; ++w) {
+      const uint32_t c = s.wcnt[w][tid];
+      s.wcnt[w][tid] = (uint16_t)run;
+      run += c;
+    }
+    s.tcnt[tid] = run;
+    s.loc[tid] = run;
+  }
+  __syncthreads();
+  if (tid < 256) {  // tile-local exclusive digit offsets
+    uint32_t x = s.loc[tid], inc = x;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) s.wt[wid] = inc;
+    s.loc[tid] = inc - x;
+  }
+  __syncthreads();
+  if (tid < 256) {
+    uint32_t add = 0;
+    for (int w = 0; w < wid; ++w) add += s.wt[w];
+    s.loc[tid] += add;
+    if (tid == 255) s.ntile = s.loc[255] + s.tcnt[255];
+    // decoupled look-back for digit tid over the preceding tiles
+    const uint32_t c = s.tcnt[tid];
+    unsigned long long *st = pl.status + (size_t)tile * 256 + tid;
+    unsigned long long excl = 0;
+    if (tile == 0) {
+      st_release_u64(st, kFlagP | c);
+    } else {
+      st_release_u64(st, kFlagA | c);
+      for (long long j = (long long)tile - 1; j >= 0; --j) {
+        const unsigned long long *sj = pl.status + (size_t)j * 256 + tid;
+        unsigned long long v = ld_acquire_u64(sj);
+        while (v == 0) v = ld_acquire_u64(sj);
+        excl += v & kValMask;
+        if (v & kFlagP) break;
+      }
+      st_release_u64(st, kFlagP | (excl + c));
+    }
+    s.gbase[tid] = s.pbase[tid] + (uint32_t)excl;
+  }
+  __syncthreads();
+  // local scatter into digit order
+  for (int e = tid; e < kTileEv; e += kPartThreads) {
+    const uint32_t rk = s.rank[e];
+    if (rk == 0xFFFF) continue;
+    const uint32_t d = s.dig[e];
+    const uint32_t lp = s.loc[d] + s.wcnt[e / (kTileEv / kPWarps)][d] + rk;
+#pragma unroll
+    for (int k = 0; k < K; ++k) s.kout[k][lp] = s.kin[k][e];
+    s.lout[lp] = s.lin[e];
+    s.dout[lp] = (uint8_t)d;
+  }
+  __syncthreads();
+  // coalesced write-out, digit run by digit run
+  const uint32_t nt = s.ntile;
+  for (uint32_t i = tid; i < nt; i += kPartThreads) {
+    const uint32_t d = s.dout[i];
+    const uint32_t g = s.gbase[d] + (i - s.loc[d]);
+#pragma unroll
+    for (int k = 0; k < K; ++k) out_key[k][g] = s.kout[k][i];
+    out_let[g] = s.lout[i];
+  }
+}
+
+// off[c] = first position of bucket c in the final order, off[NB] = n.
+__global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, int bits,
+                                     uint32_t *off, uint32_t nb) {
+  const unsigned long long n = *nvalid;
+  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const long long prev = i == 0 ? -1 : (long long)bucket_of(k0[i - 1], bits);
+    const long long cur = i == n ? (long long)nb : (long long)bucket_of(k0[i], bits);
+    for (long long c = prev + 1; c <= cur; ++c) off[c] = (uint32_t)i;
+  }
+}
+
+}  // namespace
+
+#define LTL4C_LAUNCH(ID, ...)           \
+  do {                                   \
+    if (L.before) L.before(L.ctx, ID);   \
+    __VA_ARGS__;                         \
+    cudaError_t e_ = cudaGetLastError(); \
+    if (L.after) L.after(L.ctx, ID);     \
+    return e_;                           \
+  } while (0)
+
+cudaError_t launch_part_hist(const PartPlan &p, const Launcher &L) {
+  switch (p.K) {
+    case 1: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<1><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+    case 2: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<2><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+    default: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<3><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+  }
+}
+
+template <int K>
+static cudaError_t sweep(const PartPlan &p, int pass, const Launcher &L) {
+  const size_t sm = sizeof(SweepSmem<K>);
+  cudaFuncSetAttribute(part_onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKPartOnesweep, part_onesweep_kernel<K><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
+}
+
+cudaError_t launch_part_onesweep(const PartPlan &p, int pass, const Launcher &L) {
+  switch (p.K) {
+    case 1: return sweep<1>(p, pass, L);
+    case 2: return sweep<2>(p, pass, L);
+    default: return sweep<3>(p, pass, L);
+  }
+}
+
+cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
+  const uint32_t *k0 = p.buf_key[(p.passes - 1) & 1][0];
+  const unsigned grid = (unsigned)((p.n + 1 + 255) / 256 > 148 * 16 ? 148 * 16 : (p.n + 1 + 255) / 256);
+  LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(k0, p.nvalid, p.bits, off, n_buckets));
+}
+
+}  // namespace ltl4c

@@ -104,8 +104,9 @@ struct ltl4c_state {
   DevBuf<unsigned long long> d_nvalid;
   DevBuf<uint32_t> bufkey[2][kMaxLevels];
   DevBuf<uint8_t> buflet[2];
-  DevBuf<uint32_t> counts, totals, bucket_count, bucket_off, oversize_list, medium_list, sched;
-  int n_sms = 148, warp_ctas_per_sm = 1;
+  DevBuf<uint32_t> totals, bucket_off, oversize_list, medium_list, sched;
+  DevBuf<unsigned long long> status;
+  int n_sms = 148, warp_ctas_per_sm = 1, warps_per_cta = 4;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
@@ -246,7 +247,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   }
   if (N > 0) {
     const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
-    const int B = std::min(24, std::max(1, ceil_log2(target)));
+    const int B = std::min(kMaxPasses * kMaxDigitBits, std::max(1, ceil_log2(target)));
     const int P = (B + kMaxDigitBits - 1) / kMaxDigitBits;
     const uint32_t NB = 1u << B;
     const uint32_t n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
@@ -254,44 +255,46 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
       for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
       CU(st->buflet[i].ensure(N));
     }
-    CU(st->counts.ensure((size_t)(1u << kMaxDigitBits) * n_tiles));
-    CU(st->totals.ensure(1u << kMaxDigitBits));
-    CU(st->bucket_count.ensure(NB));
+    CU(st->status.ensure((size_t)256 * n_tiles * P));
+    CU(st->totals.ensure(kMaxPasses * 256 + 16));
     CU(st->bucket_off.ensure((size_t)NB + 1));
     CU(st->oversize_list.ensure(NB));
     CU(st->medium_list.ensure(NB));
     CU(st->sched.ensure(4));
-    CU(cudaMemsetAsync(st->bucket_count.p, 0, sizeof(uint32_t) * NB, s));
-    CU(cudaMemsetAsync(st->sched.p, 0, sizeof(uint32_t) * 4, s));
+    // one memset: digit totals [3][256] + tile counters [3] + bucket counter
+    CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
+    CU(cudaMemsetAsync(st->status.p, 0, sizeof(unsigned long long) * 256 * n_tiles * P, s));
+    PartPlan pl{};
+    for (int l = 0; l < K; ++l) {
+      pl.in_key[l] = keys[l];
+      pl.buf_key[0][l] = st->bufkey[0][l].p;
+      pl.buf_key[1][l] = st->bufkey[1][l].p;
+    }
+    pl.in_let = letters;
+    pl.buf_let[0] = st->buflet[0].p;
+    pl.buf_let[1] = st->buflet[1].p;
+    pl.n = N;
+    pl.n_tiles = n_tiles;
+    pl.K = K;
+    pl.bits = B;
+    pl.passes = P;
     int lo = 0;
     for (int pass = 0; pass < P; ++pass) {
       const int width = (B - lo + (P - pass) - 1) / (P - pass);
-      PartParams pp{};
-      for (int l = 0; l < K; ++l) {
-        pp.in_key[l] = pass == 0 ? keys[l] : st->bufkey[(pass - 1) & 1][l].p;
-        pp.out_key[l] = st->bufkey[pass & 1][l].p;
-      }
-      pp.in_let = pass == 0 ? letters : st->buflet[(pass - 1) & 1].p;
-      pp.out_let = st->buflet[pass & 1].p;
-      pp.n = N;
-      pp.n_dev = pass == 0 ? nullptr : st->d_nvalid.p;
-      pp.K = K;
-      pp.bits = B;
-      pp.lo = lo;
-      pp.width = width;
-      pp.first = pass == 0;
-      pp.n_tiles = n_tiles;
-      pp.counts = st->counts.p;
-      pp.totals = st->totals.p;
-      pp.bucket_count = st->bucket_count.p;
-      pp.acc = st->d_acc.p;
-      pp.nvalid = st->d_nvalid.p;
-      CU(launch_part_count(pp, L));
-      CU(launch_part_scan(pp, L));
-      CU(launch_part_scatter(pp, L));
+      pl.lo[pass] = lo;
+      pl.width[pass] = width;
       lo += width;
     }
-    CU(launch_bucket_scan(st->bucket_count.p, st->bucket_off.p, NB, L));
+    pl.digit_hist = st->totals.p;
+    pl.tile_ctr = st->totals.p + kMaxPasses * 256;
+    pl.nvalid = st->d_nvalid.p;
+    pl.acc = st->d_acc.p;
+    CU(launch_part_hist(pl, L));
+    for (int pass = 0; pass < P; ++pass) {
+      pl.status = st->status.p + (size_t)256 * n_tiles * pass;
+      CU(launch_part_onesweep(pl, pass, L));
+    }
+    CU(launch_bucket_bounds(pl, st->bucket_off.p, NB, L));
     BucketParams bp{};
     const int fin = (P - 1) & 1;
     for (int l = 0; l < K; ++l) bp.key[l] = st->bufkey[fin][l].p;
@@ -300,7 +303,8 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     bp.n_buckets = NB;
     bp.oversize_list = st->oversize_list.p;
     bp.medium_list = st->medium_list.p;
-    bp.bucket_counter = st->sched.p;
+    bp.bucket_counter = st->totals.p + kMaxPasses * 256 + 8;
+    bp.warps_per_cta = st->warps_per_cta;
     bp.prog = st->d_prog.p;
     bp.acc = st->d_acc.p;
     if (!online) {
@@ -491,11 +495,14 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   }
   st->n_sms = dp.multiProcessorCount;
   {
-    int occ = 1;
-    // occupancy of the warp-per-bucket kernel for this program's (K, F)
-    const size_t sm = bucket_warp_smem((int)prog->n_levels, (int)prog->n_formulas);
-    occ = (int)std::max<size_t>(1, std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024)));
-    st->warp_ctas_per_sm = occ;
+    // warp-per-bucket kernel: 4 warps per CTA (fewer if the (K, F) tables are
+    // large), as many CTAs per SM as shared memory allows
+    const int K = (int)prog->n_levels, F = (int)prog->n_formulas;
+    int warps = 4;
+    while (warps > 1 && bucket_warp_smem(K, F, warps) > 200 * 1024) --warps;
+    st->warps_per_cta = warps;
+    const size_t sm = bucket_warp_smem(K, F, warps);
+    st->warp_ctas_per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024)));
   }
   cudaSetDevice(prev);
   *out = st;
@@ -549,11 +556,12 @@ void ltl4c_state_free(ltl4c_state *st) {
     for (int l = 0; l < kMaxLevels; ++l) st->bufkey[i][l].release();
     st->buflet[i].release();
   }
-  st->counts.release();
+  st->status.release();
   st->totals.release();
-  st->bucket_count.release();
   st->bucket_off.release();
   st->oversize_list.release();
+  st->medium_list.release();
+  st->sched.release();
   for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
   st->hlet.release();
   st->tab.release();
