@@ -33,7 +33,7 @@
 
 namespace ltl4c {
 
-const char *const kKernelNames[kKNumKernels] = {"part_hist", "part_onesweep", "bucket_bounds",
+const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast", "bucket_global",
                                                 "finalize", "rehash"};
 

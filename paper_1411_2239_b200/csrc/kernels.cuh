@@ -17,8 +17,8 @@ constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
 constexpr int kNodeSlots = 512;      // warp node table per inner level (<= 512 nodes: never full)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
-// (a1 + a2).  One histogram pass, then one decoupled-look-back scatter per
-// digit (onesweep): pass p sorts by digit bits [lo[p], lo[p] + width[p]).
+// (a1 + a2).  Per pass p (digit bits [lo[p], lo[p] + width[p])): count per
+// tile, scan per digit, stable scatter.
 struct PartPlan {
   const uint32_t *in_key[kMaxLevels];   // the batch (pass 0 input)
   const uint8_t *in_let;
@@ -29,8 +29,7 @@ struct PartPlan {
   int K, bits, passes;
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][256] digit totals (bound events)
-  unsigned long long *status;           // [n_tiles][256] look-back words (zeroed per pass)
-  uint32_t *tile_ctr;                   // [kMaxPasses] dynamic tile ids
+  uint32_t *counts;                     // [256][n_tiles] tile counts, scanned in place
   unsigned long long *nvalid;           // bound events of this batch
   DevAcc *acc;
 };
@@ -78,8 +77,9 @@ struct Launcher {
 };
 
 enum KernelId {
-  kKPartHist = 0,
-  kKPartOnesweep,
+  kKPartCount = 0,
+  kKPartScan,
+  kKPartScatter,
   kKBucketBounds,
   kKBucketWarp,
   kKBucketFast,
@@ -90,8 +90,9 @@ enum KernelId {
 };
 extern const char *const kKernelNames[kKNumKernels];
 
-cudaError_t launch_part_hist(const PartPlan &p, const Launcher &L);
-cudaError_t launch_part_onesweep(const PartPlan &p, int pass, const Launcher &L);
+cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L);
+cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
+cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);

@@ -2,15 +2,13 @@
 // on sm_100a: a STABLE LSD partition of the bound events of a
 // batch by bucket = top `bits` bits of hash(k0).
 //
-//   part_hist      one read of the keys: epsilon filter (Eq. D: an event
-//                  binds a value vector only if every guard key is present) and
-//                  the digit totals of every pass.
-//   part_onesweep  one kernel per pass: a 4096-event tile is staged in shared
-//                  memory, ranked stably by digit (warp __match_any_sync rounds
-//                  in trace order + per-warp digit counters), its global offsets
-//                  come from a decoupled look-back over the preceding tiles
-//                  (dynamic tile ids keep the chain deadlock-free), and it is
-//                  written back digit run by digit run (coalesced).
+//   part_count     per 4096-event tile: digit counts (pass 0 reads every key:
+//                  epsilon filter, Eq. D P:530 -- an event binds a value vector
+//                  only if every guard key is present; later passes read k0).
+//   part_scan      exclusive scan of each digit's row of tile counts.
+//   part_scatter   the tile is staged in shared memory, ranked stably by digit
+//                  (warp __match_any_sync rounds in trace order + per-warp digit
+//                  counters) and written back digit run by digit run (coalesced).
 //   bucket_bounds  bucket offsets mu from the final order.
 //
 // Stability keeps every slice u^D in trace order (reading A15); a bucket holds
@@ -27,51 +25,69 @@ namespace {
 
 constexpr int kPWarps = kPartThreads / 32;
 constexpr int kRounds = kTileEv / kPartThreads;  // rounds of 32 events per warp
-constexpr unsigned long long kFlagA = 1ull << 62;  // tile aggregate published
-constexpr unsigned long long kFlagP = 2ull << 62;  // inclusive prefix published
-constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
-template <int K>
-__global__ void __launch_bounds__(kPartThreads) part_hist_kernel(PartPlan pl) {
-  __shared__ uint32_t h[kMaxPasses][256];
+// Digit counts of one tile (counts[d][tile]).  Pass 0 reads the batch and
+// applies the epsilon filter; later passes read k0 of the previous pass.
+template <int K, bool kFirst>
+__global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, int pass) {
+  __shared__ uint32_t h[256];
   __shared__ uint32_t nv;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < kMaxPasses * 256; i += kPartThreads) (&h[0][0])[i] = 0;
+  for (int i = tid; i < 256; i += kPartThreads) h[i] = 0;
   if (tid == 0) nv = 0;
   __syncthreads();
+  const uint32_t *const *in_key = kFirst ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
+  const unsigned long long n = kFirst ? pl.n : *pl.nvalid;
   const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv;
-  uint32_t myvalid = 0;
-  for (int r = 0; r < kRounds; ++r) {
-    const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
-    bool valid = j < pl.n;
-    uint32_t k0 = 0;
-    if (valid) {
-      k0 = pl.in_key[0][j];
+  const uint32_t dmask = (1u << pl.width[pass]) - 1u;
+  const int lo = pl.lo[pass];
+  uint32_t k0[kRounds];
+  bool ok[kRounds];
 #pragma unroll
-      for (int i = 0; i < K; ++i) valid &= pl.in_key[i][j] != kAbsent;
+  for (int r = 0; r < kRounds; ++r) {  // all loads first (memory-level parallelism)
+    const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
+    ok[r] = j < n;
+    k0[r] = ok[r] ? in_key[0][j] : 0u;
+    if (kFirst) {
+#pragma unroll
+      for (int i = 1; i < K; ++i) ok[r] &= !(ok[r] && in_key[i][j] == kAbsent);
     }
-    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t b = bucket_of(k0, pl.bits);
-      for (int p = 0; p < pl.passes; ++p) {
-        const uint32_t d = (b >> pl.lo[p]) & ((1u << pl.width[p]) - 1u);
-        const uint32_t peers = __match_any_sync(vm, d);
-        if ((peers & lanemask_lt()) == 0) atomicAdd(&h[p][d], __popc(peers));
-      }
-    }
-    myvalid += valid;
   }
-  for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
-  if (lane == 0 && myvalid) atomicAdd(&nv, myvalid);
+  uint32_t myvalid = 0;
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const bool v = ok[r] && (!kFirst || k0[r] != kAbsent);
+    if (v) atomicAdd(&h[(bucket_of(k0[r], pl.bits) >> lo) & dmask], 1u);
+    myvalid += v;
+  }
+  if (kFirst) {
+    for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
+    if (lane == 0 && myvalid) atomicAdd(&nv, myvalid);
+  }
   __syncthreads();
-  for (int i = tid; i < pl.passes * 256; i += kPartThreads) {
-    const uint32_t c = (&h[0][0])[i];
-    if (c) atomicAdd(&pl.digit_hist[i], c);
-  }
-  if (tid == 0 && nv) {
+  for (int d = tid; d < (1 << pl.width[pass]); d += kPartThreads) pl.counts[(size_t)d * pl.n_tiles + blockIdx.x] = h[d];
+  if (kFirst && tid == 0 && nv) {
     atomicAdd(pl.nvalid, (unsigned long long)nv);
     atomicAdd(&pl.acc->events_bound, (unsigned long long)nv);
   }
+}
+
+// exclusive scan of counts[d][0..n_tiles) in place (one CTA per digit), totals[d]
+__global__ void __launch_bounds__(1024) part_scan_kernel(PartPlan pl, int pass) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  uint32_t *row = pl.counts + (size_t)blockIdx.x * pl.n_tiles;
+  uint32_t carry = 0;
+  for (uint32_t off = 0; off < pl.n_tiles; off += 1024) {
+    const uint32_t i = off + threadIdx.x;
+    buf[threadIdx.x] = i < pl.n_tiles ? row[i] : 0;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < pl.n_tiles) row[i] = buf[threadIdx.x] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) pl.digit_hist[pass * 256 + blockIdx.x] = carry;
 }
 
 template <int K>
@@ -89,12 +105,11 @@ struct SweepSmem {
   uint32_t gbase[256];   // global position of the tile's digit run
   uint32_t pbase[256];   // exclusive scan of the pass's digit totals
   uint32_t wt[32];
-  uint32_t tile;
   uint32_t ntile;        // bound events in this tile
 };
 
 template <int K>
-__global__ void __launch_bounds__(kPartThreads) part_onesweep_kernel(PartPlan pl, int pass) {
+__global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -106,14 +121,13 @@ __global__ void __launch_bounds__(kPartThreads) part_onesweep_kernel(PartPlan pl
   const unsigned long long n = first ? pl.n : *pl.nvalid;
   const uint32_t dmask = (1u << pl.width[pass]) - 1u;
   const int lo = pl.lo[pass];
-  if (tid == 0) s.tile = atomicAdd(&pl.tile_ctr[pass], 1u);
   if (tid < 256) {
     s.pbase[tid] = pl.digit_hist[pass * 256 + tid];
     s.loc[tid] = 0;
   }
   for (int i = tid; i < kPWarps * 256; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t tile = s.tile;
+  const uint32_t tile = blockIdx.x;
   const unsigned long long base = (unsigned long long)tile * kTileEv;
   // stage the tile (coalesced loads)
   for (int i = tid; i < kTileEv; i += kPartThreads) {
@@ -193,24 +207,7 @@ __global__ void __launch_bounds__(kPartThreads) part_onesweep_kernel(PartPlan pl
     for (int w = 0; w < wid; ++w) add += s.wt[w];
     s.loc[tid] += add;
     if (tid == 255) s.ntile = s.loc[255] + s.tcnt[255];
-    // decoupled look-back for digit tid over the preceding tiles
-    const uint32_t c = s.tcnt[tid];
-    unsigned long long *st = pl.status + (size_t)tile * 256 + tid;
-    unsigned long long excl = 0;
-    if (tile == 0) {
-      st_release_u64(st, kFlagP | c);
-    } else {
-      st_release_u64(st, kFlagA | c);
-      for (long long j = (long long)tile - 1; j >= 0; --j) {
-        const unsigned long long *sj = pl.status + (size_t)j * 256 + tid;
-        unsigned long long v = ld_acquire_u64(sj);
-        while (v == 0) v = ld_acquire_u64(sj);
-        excl += v & kValMask;
-        if (v & kFlagP) break;
-      }
-      st_release_u64(st, kFlagP | (excl + c));
-    }
-    s.gbase[tid] = s.pbase[tid] + (uint32_t)excl;
+    s.gbase[tid] = s.pbase[tid] + (tid < (1 << pl.width[pass]) ? pl.counts[(size_t)tid * pl.n_tiles + tile] : 0u);
   }
   __syncthreads();
   // local scatter into digit order
@@ -259,26 +256,33 @@ __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long lon
     return e_;                           \
   } while (0)
 
-cudaError_t launch_part_hist(const PartPlan &p, const Launcher &L) {
-  switch (p.K) {
-    case 1: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<1><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
-    case 2: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<2><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
-    default: LTL4C_LAUNCH(kKPartHist, part_hist_kernel<3><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p));
+cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
+  if (pass == 0) {
+    switch (p.K) {
+      case 1: LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+      case 2: LTL4C_LAUNCH(kKPartCount, part_count_kernel<2, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+      default: LTL4C_LAUNCH(kKPartCount, part_count_kernel<3, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+    }
   }
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+}
+
+cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {
+  LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width[pass], 1024, 0, L.stream>>>(p, pass));
 }
 
 template <int K>
-static cudaError_t sweep(const PartPlan &p, int pass, const Launcher &L) {
+static cudaError_t scatter(const PartPlan &p, int pass, const Launcher &L) {
   const size_t sm = sizeof(SweepSmem<K>);
-  cudaFuncSetAttribute(part_onesweep_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  LTL4C_LAUNCH(kKPartOnesweep, part_onesweep_kernel<K><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
+  cudaFuncSetAttribute(part_scatter_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
 }
 
-cudaError_t launch_part_onesweep(const PartPlan &p, int pass, const Launcher &L) {
+cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) {
   switch (p.K) {
-    case 1: return sweep<1>(p, pass, L);
-    case 2: return sweep<2>(p, pass, L);
-    default: return sweep<3>(p, pass, L);
+    case 1: return scatter<1>(p, pass, L);
+    case 2: return scatter<2>(p, pass, L);
+    default: return scatter<3>(p, pass, L);
   }
 }
 

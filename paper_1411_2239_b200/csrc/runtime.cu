@@ -104,8 +104,7 @@ struct ltl4c_state {
   DevBuf<unsigned long long> d_nvalid;
   DevBuf<uint32_t> bufkey[2][kMaxLevels];
   DevBuf<uint8_t> buflet[2];
-  DevBuf<uint32_t> totals, bucket_off, oversize_list, medium_list, sched;
-  DevBuf<unsigned long long> status;
+  DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, sched;
   int n_sms = 148, warp_ctas_per_sm = 1, warps_per_cta = 4;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
@@ -255,15 +254,13 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
       for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
       CU(st->buflet[i].ensure(N));
     }
-    CU(st->status.ensure((size_t)256 * n_tiles * P));
+    CU(st->counts.ensure((size_t)256 * n_tiles));
     CU(st->totals.ensure(kMaxPasses * 256 + 16));
     CU(st->bucket_off.ensure((size_t)NB + 1));
     CU(st->oversize_list.ensure(NB));
     CU(st->medium_list.ensure(NB));
-    CU(st->sched.ensure(4));
-    // one memset: digit totals [3][256] + tile counters [3] + bucket counter
+    // one memset: digit totals [3][256] + scheduler counters
     CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
-    CU(cudaMemsetAsync(st->status.p, 0, sizeof(unsigned long long) * 256 * n_tiles * P, s));
     PartPlan pl{};
     for (int l = 0; l < K; ++l) {
       pl.in_key[l] = keys[l];
@@ -286,13 +283,13 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
       lo += width;
     }
     pl.digit_hist = st->totals.p;
-    pl.tile_ctr = st->totals.p + kMaxPasses * 256;
+    pl.counts = st->counts.p;
     pl.nvalid = st->d_nvalid.p;
     pl.acc = st->d_acc.p;
-    CU(launch_part_hist(pl, L));
     for (int pass = 0; pass < P; ++pass) {
-      pl.status = st->status.p + (size_t)256 * n_tiles * pass;
-      CU(launch_part_onesweep(pl, pass, L));
+      CU(launch_part_count(pl, pass, L));
+      CU(launch_part_scan(pl, pass, L));
+      CU(launch_part_scatter(pl, pass, L));
     }
     CU(launch_bucket_bounds(pl, st->bucket_off.p, NB, L));
     BucketParams bp{};
@@ -556,7 +553,7 @@ void ltl4c_state_free(ltl4c_state *st) {
     for (int l = 0; l < kMaxLevels; ++l) st->bufkey[i][l].release();
     st->buflet[i].release();
   }
-  st->status.release();
+  st->counts.release();
   st->totals.release();
   st->bucket_off.release();
   st->oversize_list.release();
