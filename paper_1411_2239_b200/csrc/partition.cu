@@ -129,16 +129,25 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
   __syncthreads();
   const uint32_t tile = blockIdx.x;
   const unsigned long long base = (unsigned long long)tile * kTileEv;
-  // stage the tile (coalesced loads)
-  for (int i = tid; i < kTileEv; i += kPartThreads) {
-    const unsigned long long j = base + i;
-    if (j < n) {
+  // stage the tile: every load of this thread first (memory-level parallelism),
+  // then the shared-memory stores
+  {
+    uint32_t rk[kRounds][K];
+    uint8_t rl[kRounds];
 #pragma unroll
-      for (int k = 0; k < K; ++k) s.kin[k][i] = in_key[k][j];
-      s.lin[i] = in_let[j];
-    } else {
+    for (int r = 0; r < kRounds; ++r) {
+      const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
+      const bool in = j < n;
 #pragma unroll
-      for (int k = 0; k < K; ++k) s.kin[k][i] = kAbsent;
+      for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
+      rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
+    }
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const int i = r * kPartThreads + tid;
+#pragma unroll
+      for (int k = 0; k < K; ++k) s.kin[k][i] = rk[r][k];
+      s.lin[i] = rl[r];
     }
   }
   // pass base offsets: exclusive scan of the digit totals (first 256 threads)
