@@ -358,28 +358,27 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 // in a round are grouped with __match_any_sync and their leader applies the
 // letters in lane order (so every slice u^D is stepped in trace order).  Leaves
 // and tree nodes live in warp-private shared-memory hash tables whose slots
-// store the index of a representative event (keys are compared in place).
-// The next bucket's events are loaded into registers while the current one is
-// processed.
-constexpr int kPerLane = kWarpCap / 32;
-
+// store the index of a representative event; keys are compared in place in the
+// (L1-resident) partitioned arrays.  The next bucket is prefetched into L1
+// while the current one is processed.
 struct WarpSmem {
-  uint32_t *key[kMaxLevels];   // [kWarpCap]
   uint8_t *let;                // [kWarpCap]
-  uint16_t *ltag;              // [kLeafSlots]: 0 empty, else rep event + 1
+  uint32_t *ltag;              // [kLeafSlots]: 0 empty, else rep event + 1
   uint8_t *lstate;             // [kLeafSlots]
   uint16_t *llist;             // [kWarpCap]
-  uint16_t *ntag[kMaxLevels];  // level l in [1, K-1]: [kNodeSlots]
+  uint16_t *lnode[kMaxLevels]; // [kWarpCap]: slot of each leaf's depth-l ancestor
+  uint32_t *ntag[kMaxLevels];  // level l in [1, K-1]: [kNodeSlots]
   uint32_t *nhist[kMaxLevels]; // [kNodeSlots][nf][3]: two u16 counters per word
   uint16_t *nlist[kMaxLevels]; // [kNodeSlots]
+  uint16_t *npar[kMaxLevels];  // [kNodeSlots]: parent slot (depth l - 1)
   uint32_t *cnt;               // [4]: leaves, nodes per level
   uint32_t *acc;               // [kMaxFormulas][kMaxLevels + 1][6]
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int K, int nf) {
-  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(2 * kLeafSlots) + align16(kLeafSlots) +
-             align16(2 * kWarpCap);
-  b += (size_t)(K - 1) * (align16(2 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) + align16(2 * kNodeSlots));
+  size_t b = align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) + align16(2 * kWarpCap);
+  b += (size_t)(K - 1) * (align16(2 * kWarpCap) + align16(4 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) +
+                          2 * align16(2 * kNodeSlots));
   b += align16(16) + align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
   return b;
 }
@@ -391,16 +390,19 @@ __host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf, int warps) 
 __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
   WarpSmem w;
   auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
-  for (int i = 0; i < kMaxLevels; ++i) w.key[i] = i < K ? (uint32_t *)take(4 * kWarpCap) : nullptr;
   w.let = take(kWarpCap);
-  w.ltag = (uint16_t *)take(2 * kLeafSlots);
+  w.ltag = (uint32_t *)take(4 * kLeafSlots);
   w.lstate = take(kLeafSlots);
   w.llist = (uint16_t *)take(2 * kWarpCap);
-  for (int l = 0; l < kMaxLevels; ++l) { w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; }
+  for (int l = 0; l < kMaxLevels; ++l) {
+    w.lnode[l] = nullptr; w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; w.npar[l] = nullptr;
+  }
   for (int l = 1; l < K; ++l) {
-    w.ntag[l] = (uint16_t *)take(2 * kNodeSlots);
+    w.lnode[l] = (uint16_t *)take(2 * kWarpCap);
+    w.ntag[l] = (uint32_t *)take(4 * kNodeSlots);
     w.nhist[l] = (uint32_t *)take((size_t)4 * kNodeSlots * nf * 3);
     w.nlist[l] = (uint16_t *)take(2 * kNodeSlots);
+    w.npar[l] = (uint16_t *)take(2 * kNodeSlots);
   }
   w.cnt = (uint32_t *)take(16);
   w.acc = (uint32_t *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
@@ -408,44 +410,52 @@ __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
 }
 
 template <int K>
-__device__ __forceinline__ uint32_t warp_hash(const WarpSmem &w, int e, int m) {
-  uint32_t h = 0x2545F491u;
+struct BucketKeys {
+  const uint32_t *k[K];
+  __device__ __forceinline__ uint32_t get(int i, int e) const { return __ldg(k[i] + e); }
+  __device__ __forceinline__ uint32_t hash(int e, int m) const {
+    uint32_t h = 0x2545F491u;
 #pragma unroll
-  for (int i = 0; i < K; ++i)
-    if (i < m) h = fmix32(h ^ w.key[i][e]) + 0x9e3779b9u * (i + 1);
-  return h;
-}
-
-template <int K>
-__device__ __forceinline__ bool warp_same(const WarpSmem &w, int a, int b, int m) {
-  bool eq = true;
+    for (int i = 0; i < K; ++i)
+      if (i < m) h = fmix32(h ^ get(i, e)) + 0x9e3779b9u * (i + 1);
+    return h;
+  }
+  __device__ __forceinline__ bool same(int a, int b, int m) const {
+    bool eq = true;
 #pragma unroll
-  for (int i = 0; i < K; ++i)
-    if (i < m) eq &= w.key[i][a] == w.key[i][b];
-  return eq;
-}
+    for (int i = 0; i < K; ++i)
+      if (i < m) eq &= get(i, a) == get(i, b);
+    return eq;
+  }
+};
 
 // find-or-insert of the m-key prefix of event e; slots store rep event + 1.
-// Returns the slot; *isnew when this call created it.  Lock-free: a claimed
-// slot's keys are those of its rep event, already in shared memory.
+// Returns the slot (-1 when `limit` claims are exceeded); *isnew when this call
+// created it.  Lock-free: a claimed slot's keys are those of its rep event.
 template <int K>
-__device__ __forceinline__ int warp_probe(uint16_t *tag, int nslots, const WarpSmem &w, int e, int m,
-                                          bool *isnew) {
-  uint32_t h = warp_hash<K>(w, e, m) & (uint32_t)(nslots - 1);
-  volatile uint16_t *vt = tag;
+__device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const BucketKeys<K> &bk, int e, int m,
+                                          uint32_t hsh, bool *isnew, uint32_t *claims, uint32_t limit,
+                                          uint16_t *list) {
+  uint32_t h = hsh & (uint32_t)(nslots - 1);
+  volatile uint32_t *vt = tag;
   while (true) {
-    unsigned short t = vt[h];
+    uint32_t t = vt[h];
     if (t == 0) {
-      t = atomicCAS(&tag[h], (unsigned short)0, (unsigned short)(e + 1));
-      if (t == 0) { *isnew = true; return (int)h; }
+      if (*(volatile uint32_t *)claims >= limit) return -1;
+      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
+      if (t == 0) {
+        *isnew = true;
+        list[atomicAdd(claims, 1u)] = (uint16_t)h;
+        return (int)h;
+      }
     }
-    if (warp_same<K>(w, (int)t - 1, e, m)) { *isnew = false; return (int)h; }
+    if (bk.same((int)t - 1, e, m)) { *isnew = false; return (int)h; }
     h = (h + 1) & (uint32_t)(nslots - 1);
   }
 }
 
 template <int K>
-__global__ void __launch_bounds__(128) bucket_warp_kernel(BucketParams p) {
+__global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nq = prog->nq, A = 1 << prog->na;
@@ -466,9 +476,7 @@ __global__ void __launch_bounds__(128) bucket_warp_kernel(BucketParams p) {
   if (lane < 4) w.cnt[lane] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
-  // prefetch registers for the next bucket
-  uint32_t rk[K][kPerLane];
-  uint8_t rl[kPerLane];
+  const uint32_t node_limit = kNodeSlots / 2;
   auto grab = [&](uint32_t &b, uint32_t &start, uint32_t &cnt) {
     while (true) {
       b = 0;
@@ -482,50 +490,48 @@ __global__ void __launch_bounds__(128) bucket_warp_kernel(BucketParams p) {
         if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = b;
         continue;
       }
+      // warm L1 with the bucket's keys and letters (128-byte lines)
+      for (uint32_t off = lane * 32; off < cnt; off += 32 * 32) {
 #pragma unroll
-      for (int j = 0; j < kPerLane; ++j) {
-        const uint32_t i = j * 32 + lane;
-        if (i < cnt) {
-#pragma unroll
-          for (int k = 0; k < K; ++k) rk[k][j] = p.key[k][start + i];
-          rl[j] = p.let[start + i];
-        }
+        for (int k = 0; k < K; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.key[k] + start + off));
       }
+      if (lane * 128 < cnt) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.let + start + lane * 128));
       return true;
     }
   };
   uint32_t b, start, cnt;
   bool have = grab(b, start, cnt);
   while (have) {
-    const uint32_t cur_cnt = cnt;
+    const uint32_t cur_b = b, cur_start = start, cur_cnt = cnt;
+    BucketKeys<K> bk;
 #pragma unroll
-    for (int j = 0; j < kPerLane; ++j) {
-      const uint32_t i = j * 32 + lane;
-      if (i < cur_cnt) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) w.key[k][i] = rk[k][j];
-        w.let[i] = rl[j];
-      }
-    }
+    for (int k = 0; k < K; ++k) bk.k[k] = p.key[k] + cur_start;
+    for (uint32_t i = lane; i < cur_cnt; i += 32) w.let[i] = p.let[cur_start + i];
     __syncwarp();
-    have = grab(b, start, cnt);  // loads of the next bucket overlap the work below
+    have = grab(b, start, cnt);  // prefetch of the next bucket overlaps the work below
     // a3 + a4: rounds of 32 events in trace order
     for (uint32_t base = 0; base < cur_cnt; base += 32) {
       const int e = (int)(base + lane);
       const bool act = e < (int)cur_cnt;
       const uint32_t am = __ballot_sync(0xffffffffu, act);
       if (act) {
+        uint32_t kk[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) kk[k] = bk.get(k, e);
         uint32_t peers;
         if (K == 1) {
-          peers = __match_any_sync(am, w.key[0][e]);
+          peers = __match_any_sync(am, kk[0]);
         } else {
-          const unsigned long long k01 = ((unsigned long long)w.key[1][e] << 32) | w.key[0][e];
+          const unsigned long long k01 = ((unsigned long long)kk[1] << 32) | kk[0];
           peers = __match_any_sync(am, k01);
-          if (K == 3) peers &= __match_any_sync(am, w.key[K - 1][e]);
+          if (K == 3) peers &= __match_any_sync(am, kk[K - 1]);
         }
         if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
+          uint32_t hsh = 0x2545F491u;
+#pragma unroll
+          for (int k = 0; k < K; ++k) hsh = fmix32(hsh ^ kk[k]) + 0x9e3779b9u * (k + 1);
           bool isnew;
-          const int slot = warp_probe<K>(w.ltag, kLeafSlots, w, e, K, &isnew);
+          const int slot = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
           uint32_t q = isnew ? q0 : w.lstate[slot];
           uint32_t m = peers;
           while (m) {
@@ -534,59 +540,70 @@ __global__ void __launch_bounds__(128) bucket_warp_kernel(BucketParams p) {
             q = sdelta[q * A + w.let[base + i]];
           }
           w.lstate[slot] = (uint8_t)q;
-          if (isnew) w.llist[atomicAdd(&w.cnt[0], 1u)] = (uint16_t)slot;
         }
       }
       __syncwarp();
     }
-    // a5: leaf verdicts, depth K-1 grouping
     const uint32_t nleaf = w.cnt[0];
-    for (uint32_t i = lane; i < nleaf; i += 32) {
-      const int slot = w.llist[i];
-      const int q = w.lstate[slot];
-      int nslot = -1;
-      if (K > 1) {
-        bool isnew;
-        nslot = warp_probe<K>(w.ntag[K - 1], kNodeSlots, w, (int)w.ltag[slot] - 1, K - 1, &isnew);
-        if (isnew) w.nlist[K - 1][atomicAdd(&w.cnt[K - 1], 1u)] = (uint16_t)nslot;
-      }
-      for (int f = 0; f < nf; ++f) {
-        const int v = slab[f * kMaxStates + q];
-        atomicAdd(&w.acc[(f * (kMaxLevels + 1) + K) * 6 + v], 1u);
-        if (K > 1) atomicAdd(&w.nhist[K - 1][(nslot * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+    // a5 (i): the ancestors of every leaf at depths 1 .. K-1 (P)
+    bool ovf = false;
+    if (K > 1) {
+      for (uint32_t i = lane; i < nleaf && !ovf; i += 32) {
+        const int rep = (int)w.ltag[w.llist[i]] - 1;
+        int parent = -1;
+        for (int l = 1; l < K; ++l) {
+          bool isnew;
+          const int ns = warp_probe<K>(w.ntag[l], kNodeSlots, bk, rep, l, bk.hash(rep, l), &isnew, &w.cnt[l],
+                                       node_limit, w.nlist[l]);
+          if (ns < 0) { ovf = true; break; }
+          w.lnode[l][i] = (uint16_t)ns;
+          if (isnew && l > 1) w.npar[l][ns] = (uint16_t)parent;
+          parent = ns;
+        }
       }
     }
+    ovf = __any_sync(0xffffffffu, ovf);
     __syncwarp();
-    for (int l = K - 1; l >= 1; --l) {
-      const uint32_t nn = w.cnt[l];
-      for (uint32_t i = lane; i < nn; i += 32) {
-        const int slot = w.nlist[l][i];
-        int pslot = -1;
-        if (l > 1) {
-          bool isnew;
-          pslot = warp_probe<K>(w.ntag[l - 1], kNodeSlots, w, (int)w.ntag[l][slot] - 1, l - 1, &isnew);
-          if (isnew) w.nlist[l - 1][atomicAdd(&w.cnt[l - 1], 1u)] = (uint16_t)pslot;
-        }
+    if (ovf) {
+      // too many distinct prefixes for the warp tables: hand the bucket to the CTA path
+      if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = cur_b;
+    } else {
+      // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B)
+      for (uint32_t i = lane; i < nleaf; i += 32) {
+        const int q = w.lstate[w.llist[i]];
         for (int f = 0; f < nf; ++f) {
-          const uint32_t *hw = &w.nhist[l][(slot * nf + f) * 3];
-          uint32_t h[6];
-#pragma unroll
-          for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
-          const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
-          atomicAdd(&w.acc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
-          if (l > 1) atomicAdd(&w.nhist[l - 1][(pslot * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+          const int v = slab[f * kMaxStates + q];
+          atomicAdd(&w.acc[(f * (kMaxLevels + 1) + K) * 6 + v], 1u);
+          if (K > 1) atomicAdd(&w.nhist[K - 1][(w.lnode[K - 1][i] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
         }
       }
       __syncwarp();
+      // a5 (iii): node verdicts by Def. 6, depth K-1 .. 1
+      for (int l = K - 1; l >= 1; --l) {
+        const uint32_t nn = w.cnt[l];
+        for (uint32_t i = lane; i < nn; i += 32) {
+          const int slot = w.nlist[l][i];
+          for (int f = 0; f < nf; ++f) {
+            const uint32_t *hw = &w.nhist[l][(slot * nf + f) * 3];
+            uint32_t h[6];
+#pragma unroll
+            for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
+            const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
+            atomicAdd(&w.acc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
+            if (l > 1) atomicAdd(&w.nhist[l - 1][(w.npar[l][slot] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+          }
+        }
+        __syncwarp();
+      }
     }
     // clear the tables touched by this bucket
     for (uint32_t i = lane; i < nleaf; i += 32) w.ltag[w.llist[i]] = 0;
     for (int l = 1; l < K; ++l) {
-      const uint32_t nn = w.cnt[l];
-      for (uint32_t i = lane; i < nn; i += 32) {
-        const int slot = w.nlist[l][i];
-        w.ntag[l][slot] = 0;
-        for (int x = 0; x < nf * 3; ++x) w.nhist[l][slot * nf * 3 + x] = 0;
+      for (uint32_t i = lane; i < kNodeSlots; i += 32) {
+        if (w.ntag[l][i]) {
+          w.ntag[l][i] = 0;
+          for (int x = 0; x < nf * 3; ++x) w.nhist[l][i * nf * 3 + x] = 0;
+        }
       }
     }
     __syncwarp();

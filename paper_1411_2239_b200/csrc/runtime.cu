@@ -492,14 +492,16 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   }
   st->n_sms = dp.multiProcessorCount;
   {
-    // warp-per-bucket kernel: 4 warps per CTA (fewer if the (K, F) tables are
-    // large), as many CTAs per SM as shared memory allows
+    // warp-per-bucket kernel: the (warps per CTA, CTAs per SM) pair that keeps
+    // the most warps resident for this program's (K, F) shared-memory plan
     const int K = (int)prog->n_levels, F = (int)prog->n_formulas;
-    int warps = 4;
-    while (warps > 1 && bucket_warp_smem(K, F, warps) > 200 * 1024) --warps;
-    st->warps_per_cta = warps;
-    const size_t sm = bucket_warp_smem(K, F, warps);
-    st->warp_ctas_per_sm = (int)std::max<size_t>(1, std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024)));
+    int best = 0;
+    for (int w = 1; w <= 8; ++w) {
+      const size_t sm = bucket_warp_smem(K, F, w);
+      if (sm > 200 * 1024) break;
+      const int ctas = (int)std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024));
+      if (ctas * w > best) { best = ctas * w; st->warps_per_cta = w; st->warp_ctas_per_sm = ctas; }
+    }
   }
   cudaSetDevice(prev);
   *out = st;
