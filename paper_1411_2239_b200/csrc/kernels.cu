@@ -362,9 +362,11 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 // (L1-resident) partitioned arrays.  The next bucket is prefetched into L1
 // while the current one is processed.
 struct WarpSmem {
+  uint32_t *key[kMaxLevels];   // [kWarpCap] staged keys of the bucket
   uint8_t *let;                // [kWarpCap]
   uint32_t *ltag;              // [kLeafSlots]: 0 empty, else rep event + 1
   uint8_t *lstate;             // [kLeafSlots]
+  uint16_t *lmark;             // [kLeafSlots]: last event of the round that probed the slot
   uint16_t *llist;             // [kWarpCap]
   uint16_t *lnode[kMaxLevels]; // [kWarpCap]: slot of each leaf's depth-l ancestor
   uint32_t *ntag[kMaxLevels];  // level l in [1, K-1]: [kNodeSlots]
@@ -376,7 +378,8 @@ struct WarpSmem {
 };
 
 __host__ __device__ inline size_t warp_smem_bytes(int K, int nf) {
-  size_t b = align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) + align16(2 * kWarpCap);
+  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) +
+             align16(2 * kLeafSlots) + align16(2 * kWarpCap);
   b += (size_t)(K - 1) * (align16(2 * kWarpCap) + align16(4 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) +
                           2 * align16(2 * kNodeSlots));
   b += align16(16) + align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
@@ -390,9 +393,11 @@ __host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf, int warps) 
 __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
   WarpSmem w;
   auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
+  for (int i = 0; i < kMaxLevels; ++i) w.key[i] = i < K ? (uint32_t *)take(4 * kWarpCap) : nullptr;
   w.let = take(kWarpCap);
   w.ltag = (uint32_t *)take(4 * kLeafSlots);
   w.lstate = take(kLeafSlots);
+  w.lmark = (uint16_t *)take(2 * kLeafSlots);
   w.llist = (uint16_t *)take(2 * kWarpCap);
   for (int l = 0; l < kMaxLevels; ++l) {
     w.lnode[l] = nullptr; w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; w.npar[l] = nullptr;
@@ -412,7 +417,7 @@ __device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
 template <int K>
 struct BucketKeys {
   const uint32_t *k[K];
-  __device__ __forceinline__ uint32_t get(int i, int e) const { return __ldg(k[i] + e); }
+  __device__ __forceinline__ uint32_t get(int i, int e) const { return k[i][e]; }
   __device__ __forceinline__ uint32_t hash(int e, int m) const {
     uint32_t h = 0x2545F491u;
 #pragma unroll
@@ -477,6 +482,8 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   __syncthreads();
   const uint32_t q0 = prog->q0;
   const uint32_t node_limit = kNodeSlots / 2;
+  uint32_t rk[K][kWarpCap / 32];
+  uint8_t rl[kWarpCap / 32];
   auto grab = [&](uint32_t &b, uint32_t &start, uint32_t &cnt) {
     while (true) {
       b = 0;
@@ -490,23 +497,34 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = b;
         continue;
       }
-      // warm L1 with the bucket's keys and letters (128-byte lines)
-      for (uint32_t off = lane * 32; off < cnt; off += 32 * 32) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.key[k] + start + off));
+      for (int j = 0; j < kWarpCap / 32; ++j) {
+        const uint32_t i = j * 32 + lane;
+        if (i < cnt) {
+#pragma unroll
+          for (int k = 0; k < K; ++k) rk[k][j] = p.key[k][start + i];
+          rl[j] = p.let[start + i];
+        }
       }
-      if (lane * 128 < cnt) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.let + start + lane * 128));
       return true;
     }
   };
   uint32_t b, start, cnt;
   bool have = grab(b, start, cnt);
   while (have) {
-    const uint32_t cur_b = b, cur_start = start, cur_cnt = cnt;
+    const uint32_t cur_b = b, cur_cnt = cnt;
     BucketKeys<K> bk;
 #pragma unroll
-    for (int k = 0; k < K; ++k) bk.k[k] = p.key[k] + cur_start;
-    for (uint32_t i = lane; i < cur_cnt; i += 32) w.let[i] = p.let[cur_start + i];
+    for (int k = 0; k < K; ++k) bk.k[k] = w.key[k];
+#pragma unroll
+    for (int j = 0; j < kWarpCap / 32; ++j) {
+      const uint32_t i = j * 32 + lane;
+      if (i < cur_cnt) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) w.key[k][i] = rk[k][j];
+        w.let[i] = rl[j];
+      }
+    }
     __syncwarp();
     have = grab(b, start, cnt);  // prefetch of the next bucket overlaps the work below
     // a3 + a4: rounds of 32 events in trace order
@@ -514,25 +532,31 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       const int e = (int)(base + lane);
       const bool act = e < (int)cur_cnt;
       const uint32_t am = __ballot_sync(0xffffffffu, act);
+      // every lane probes its own vector; a round needs the ordered (match) path
+      // only if two of its lanes carry the same vector
+      uint32_t kk[K];
+      int slot = -1;
+      bool isnew = false;
       if (act) {
-        uint32_t kk[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) kk[k] = bk.get(k, e);
-        uint32_t peers;
-        if (K == 1) {
-          peers = __match_any_sync(am, kk[0]);
-        } else {
-          const unsigned long long k01 = ((unsigned long long)kk[1] << 32) | kk[0];
-          peers = __match_any_sync(am, k01);
-          if (K == 3) peers &= __match_any_sync(am, kk[K - 1]);
-        }
-        if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
-          uint32_t hsh = 0x2545F491u;
+        uint32_t hsh = 0x2545F491u;
 #pragma unroll
-          for (int k = 0; k < K; ++k) hsh = fmix32(hsh ^ kk[k]) + 0x9e3779b9u * (k + 1);
-          bool isnew;
-          const int slot = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
-          uint32_t q = isnew ? q0 : w.lstate[slot];
+        for (int k = 0; k < K; ++k) hsh = fmix32(hsh ^ kk[k]) + 0x9e3779b9u * (k + 1);
+        slot = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
+        w.lmark[slot] = (uint16_t)e;
+      }
+      __syncwarp();
+      // two lanes with one slot: at least one of them sees the other's mark
+      const bool dup_here = act && w.lmark[slot] != (uint16_t)e;
+      const bool any_dup = __any_sync(0xffffffffu, dup_here);
+      if (!any_dup) {
+        if (act) w.lstate[slot] = sdelta[(isnew ? q0 : (uint32_t)w.lstate[slot]) * A + w.let[e]];
+      } else if (act) {
+        const uint32_t peers = __match_any_sync(am, (uint32_t)slot);
+        if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
+          const int rep = (int)w.ltag[slot] - 1;
+          uint32_t q = rep >= (int)base ? q0 : w.lstate[slot];  // created in this round?
           uint32_t m = peers;
           while (m) {
             const int i = __ffs(m) - 1;
