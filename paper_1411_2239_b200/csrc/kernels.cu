@@ -418,11 +418,12 @@ template <int K>
 struct BucketKeys {
   const uint32_t *k[K];
   __device__ __forceinline__ uint32_t get(int i, int e) const { return k[i][e]; }
+  // multiplicative hash of the m-key prefix (table index = top bits)
   __device__ __forceinline__ uint32_t hash(int e, int m) const {
-    uint32_t h = 0x2545F491u;
+    uint32_t h = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i)
-      if (i < m) h = fmix32(h ^ get(i, e)) + 0x9e3779b9u * (i + 1);
+      if (i < m) h = (h ^ get(i, e)) * (0x9E3779B1u + 0x7F4A7C16u * i);
     return h;
   }
   __device__ __forceinline__ bool same(int a, int b, int m) const {
@@ -441,7 +442,8 @@ template <int K>
 __device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const BucketKeys<K> &bk, int e, int m,
                                           uint32_t hsh, bool *isnew, uint32_t *claims, uint32_t limit,
                                           uint16_t *list) {
-  uint32_t h = hsh & (uint32_t)(nslots - 1);
+  const int shift = 32 - __popc((uint32_t)nslots - 1u);
+  uint32_t h = hsh >> shift;
   volatile uint32_t *vt = tag;
   while (true) {
     uint32_t t = vt[h];
@@ -540,9 +542,9 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       if (act) {
 #pragma unroll
         for (int k = 0; k < K; ++k) kk[k] = bk.get(k, e);
-        uint32_t hsh = 0x2545F491u;
+        uint32_t hsh = 0;
 #pragma unroll
-        for (int k = 0; k < K; ++k) hsh = fmix32(hsh ^ kk[k]) + 0x9e3779b9u * (k + 1);
+        for (int k = 0; k < K; ++k) hsh = (hsh ^ kk[k]) * (0x9E3779B1u + 0x7F4A7C16u * k);
         slot = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
         w.lmark[slot] = (uint16_t)e;
       }
@@ -620,14 +622,15 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         __syncwarp();
       }
     }
-    // clear the tables touched by this bucket
+    // clear the tables touched by this bucket (claims beyond the list on overflow
+    // are still listed: every claim appends)
     for (uint32_t i = lane; i < nleaf; i += 32) w.ltag[w.llist[i]] = 0;
     for (int l = 1; l < K; ++l) {
-      for (uint32_t i = lane; i < kNodeSlots; i += 32) {
-        if (w.ntag[l][i]) {
-          w.ntag[l][i] = 0;
-          for (int x = 0; x < nf * 3; ++x) w.nhist[l][i * nf * 3 + x] = 0;
-        }
+      const uint32_t nn = min(w.cnt[l], (uint32_t)kNodeSlots);
+      for (uint32_t i = lane; i < nn; i += 32) {
+        const int slot = w.nlist[l][i];
+        w.ntag[l][slot] = 0;
+        for (int x = 0; x < nf * 3; ++x) w.nhist[l][slot * nf * 3 + x] = 0;
       }
     }
     __syncwarp();

@@ -14,7 +14,7 @@ constexpr int kCap = 2048;           // events per bucket chunk held in shared m
 constexpr int kBucketThreads = 256;
 constexpr int kWarpCap = 512;        // events per warp-processed bucket
 constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
-constexpr int kNodeSlots = 512;      // warp node table per inner level (<= 512 nodes: never full)
+constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
 // (a1 + a2).  Per pass p (digit bits [lo[p], lo[p] + width[p])): count per
