@@ -96,8 +96,21 @@ class Clocks:
                 "samples": len(rows)}
 
 
+CONFIGS = {
+    "C1": ("C1: A_{>=0.95} s:socket(s) => G(receive(s) -> F respond(s)), 10k events, 100 sockets",
+           lambda r: tracegen.socket_trace(seed=r), 5),
+    "C2": (WORKLOAD, lambda r: tracegen.login_trace(seed=r), 9),
+    "C3": ("C3: socket formula, 100M events, keys Zipf(1.1) over 2^20 ids",
+           lambda r: tracegen.zipf_socket_trace(seed=r), 5),
+    "C4": ("C4 (single-GPU slice): A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), "
+           "125M events, 10^6 videos Zipf(0.8)",
+           lambda r: tracegen.proxy_trace(seed=r, n=125_000_000), 9),
+}
+CONFIG = "C2"
+
+
 def make_trace(rank: int):
-    return tracegen.login_trace(seed=rank)
+    return CONFIGS[CONFIG][1](rank)
 
 
 def run_ours(args, rank, world, local_rank):
@@ -187,7 +200,15 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + ["C5"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    global CONFIG, WORKLOAD, ALG_BYTES_PER_EVENT
+    if args.config == "C5":
+        return run_c5(args)
+    CONFIG = args.config
+    WORKLOAD = CONFIGS[CONFIG][0]
+    ALG_BYTES_PER_EVENT = CONFIGS[CONFIG][2]
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -221,7 +242,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (tracegen, seeded)",
-            "config": {"workload": WORKLOAD, "events_per_gpu": r["n"], "users": 100_000,
+            "config": {"workload": WORKLOAD, "events_per_gpu": r["n"], "name": CONFIG,
                        "l2": "flushed between steps (256 MiB write, untimed)",
                        "parallelism": f"{world} independent traces (weak)" if world > 1 else "1 GPU",
                        "root_verdict": r["verdict"]},
@@ -235,12 +256,49 @@ def main():
             "gpu_launches": int(r["stats"]["launches"]),
             "clocks": r["clocks"],
         }
-        if world == 1:
+        if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(r["tr"])
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def run_c5(args):
+    """C5: three C5 formulas (one product monitor) in online mode over 1M-event
+    batches with carried state; value = events/s over the timed batches."""
+    import torch
+    import paper_1411_2239_b200 as ltl4c
+    dev = torch.device("cuda", 0)
+    batch = 1_000_000
+    nb = args.warmup + args.steps
+    tr = tracegen.c5_trace(seed=0, n=batch * nb)
+    keys = [torch.from_numpy(k.view(np.int32)).to(dev) for k in tr.keys]
+    letters = torch.from_numpy(tr.letters).to(dev)
+    st = ltl4c.compile_batch(tracegen.C5_FORMULAS).state(0, online=True, capacity=batch)
+    stream = torch.cuda.current_stream(dev)
+    for i in range(args.warmup):
+        st.verify([k[i * batch:(i + 1) * batch] for k in keys], letters[i * batch:(i + 1) * batch], stream=stream)
+    torch.cuda.synchronize(dev)
+    st.stats_reset()
+    st.profile(True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for i in range(args.warmup, nb):
+        res = st.verify([k[i * batch:(i + 1) * batch] for k in keys], letters[i * batch:(i + 1) * batch],
+                        stream=stream)
+    b.record(stream)
+    torch.cuda.synchronize(dev)
+    ms = a.elapsed_time(b)
+    stats = st.stats()
+    line = {"metric": METRIC, "value": batch * args.steps / (ms / 1e3), "unit": UNIT, "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (tracegen, seeded)",
+            "config": {"workload": "C5: 3 three-level formulas, online, 1M-event batches, carried state",
+                       "name": "C5", "verdicts": [r.verdict for r in res]},
+            "kernels": stats["kernels"], "gpu_launches": stats["launches"]}
+    print(json.dumps(line), flush=True)
 
 
 def run_reference(args, rank, world):

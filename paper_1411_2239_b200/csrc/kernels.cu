@@ -35,7 +35,7 @@ namespace ltl4c {
 
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast", "bucket_global",
-                                                "finalize", "rehash"};
+                                                "finalize", "rehash", "heavy"};
 
 namespace {
 
@@ -57,6 +57,7 @@ struct Smem {
   uint8_t *nv;                // [kMaxFormulas][kCap] node verdicts
   uint8_t *nov;               // [kMaxFormulas][kCap] node old verdicts (global path)
   uint32_t *sortbuf;          // [kCap]
+  unsigned long long *lmap;   // [kCap] heavy path: composed map per leaf
   uint8_t *delta;             // [kMaxStates * 256]
   unsigned long long *map;    // [256]
   uint8_t *lab;               // [kMaxFormulas * kMaxStates]
@@ -68,17 +69,19 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 
 // Shared-memory plan of a bucket CTA: K key words and nf formulas; the global
 // path additionally keeps the old verdicts (ov, nov).
-__host__ __device__ inline size_t smem_bytes(int K, int nf, bool global) {
+__host__ __device__ inline size_t smem_bytes(int K, int nf, int mode) {
+  const bool global = mode == 1;
   const size_t fv = align16((size_t)nf * kCap);
-  return align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
+  return (mode == 2 ? align16(8 * kCap) : 0) + align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
          align16(2 * 2 * kCap) + align16(2 * kCap) + 2 * align16(4 * (kCap + 1)) + align16(2 * kCap) +
          align16(kCap) + (global ? 4 : 2) * fv + align16(4 * kCap) + align16(kMaxStates * 256) +
          align16(8 * 256) + align16(kMaxFormulas * kMaxStates) +
          align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6) + align16(4 * 64);
 }
 
-__device__ Smem carve(uint8_t *base, int K, int nf, bool global) {
+__device__ Smem carve(uint8_t *base, int K, int nf, int mode) {
   Smem s;
+  const bool global = mode == 1;
   uint8_t *p = base;
   auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
   for (int i = 0; i < kMaxLevels; ++i) s.key[i] = i < K ? (uint32_t *)take(sizeof(uint32_t) * kCap) : nullptr;
@@ -102,6 +105,7 @@ __device__ Smem carve(uint8_t *base, int K, int nf, bool global) {
   s.lab = take(kMaxFormulas * kMaxStates);
   s.acc = (int *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
   s.misc = (uint32_t *)take(4 * 64);
+  s.lmap = mode == 2 ? (unsigned long long *)take(8 * kCap) : nullptr;
   return s;
 }
 
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
-  const Smem s = carve(smem_raw, K, nf, false);
+  const Smem s = carve(smem_raw, K, nf, 0);
   load_prog(s, prog);
   const int tid = threadIdx.x, nt = blockDim.x;
   const unsigned long long len = *p.list_len;
@@ -709,7 +713,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
   if (total == 0) return;
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
-  const Smem s = carve(smem_raw, K, nf, true);
+  const Smem s = carve(smem_raw, K, nf, 1);
   const int tid = threadIdx.x, nt = blockDim.x;
   const DevTables &T = p.tab;
   load_prog(s, prog);
@@ -853,6 +857,351 @@ __global__ void rehash_kernel(DevTables from, DevTables to, int nl, int nf, unsi
   }
 }
 
+
+// ----------------------------------------------- heavy path (offline, skewed buckets)
+// H0: segments per oversize bucket -> seg_base (exclusive scan), total in ctr[1]
+__global__ void __launch_bounds__(1024) heavy_plan_kernel(HeavyParams h) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  const uint32_t L = (uint32_t)*h.list_len;
+  uint32_t carry = 0;
+  for (uint32_t o = 0; o < L; o += 1024) {
+    const uint32_t i = o + threadIdx.x;
+    uint32_t v = 0;
+    if (i < L) {
+      const uint32_t b = h.list[i];
+      v = (h.bucket_off[b + 1] - h.bucket_off[b] + kCap - 1) / kCap;
+    }
+    buf[threadIdx.x] = v;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < L) h.seg_base[i] = buf[threadIdx.x] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { h.seg_base[L] = carry; h.ctr[1] = carry; }
+}
+
+// H1: per segment, per leaf: composed transition map of its events (in order)
+template <int K>
+__global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const DevProg *prog = h.prog;
+  const int nf = prog->nf, nq = prog->nq;
+  const Smem s = carve(smem_raw, K, nf, 2);
+  load_prog(s, prog);
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+  const DevTables &T = h.tab;
+  unsigned long long ident = 0;
+  for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
+  BucketParams bp{};
+  for (int k = 0; k < K; ++k) bp.key[k] = h.key[k];
+  bp.let = h.let;
+  const uint32_t L = (uint32_t)*h.list_len;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) {
+      const uint32_t item = atomicAdd(&h.ctr[0], 1u);
+      s.misc[50] = item;
+      if (item < h.ctr[1]) {  // bucket of the item: last i with seg_base[i] <= item
+        uint32_t lo = 0, hi = L;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (h.seg_base[mid] <= item) lo = mid; else hi = mid;
+        }
+        s.misc[51] = lo;
+      }
+    }
+    __syncthreads();
+    const uint32_t item = s.misc[50];
+    if (item >= h.ctr[1]) break;
+    const uint32_t i = s.misc[51];
+    const uint32_t b = h.list[i];
+    const uint32_t j = item - h.seg_base[i];
+    const uint32_t boff = h.bucket_off[b], bcnt = h.bucket_off[b + 1] - boff;
+    const uint32_t start = boff + j * kCap;
+    const int n = (int)min((uint32_t)kCap, bcnt - j * kCap);
+    load_chunk<K>(s, bp, start, n);
+    const int C = dedup<K>(s, n, K);
+    group_by_class(s, n, C);
+    order_segments(s, n, C);
+    for (int c = tid; c < C; c += nt) {
+      const int a = s.scan[c], e = s.scan[c + 1];
+      if (e - a > 32) continue;
+      unsigned long long m = ident;
+      for (int x = a; x < e; ++x) m = map_apply(s.map[s.let[s.perm[x]]], m, nq);
+      s.lmap[c] = m;
+    }
+    for (int c = wid; c < C; c += nw) {
+      const int a = s.scan[c], e = s.scan[c + 1], len = e - a;
+      if (len <= 32) continue;
+      const int per = (len + 31) / 32;
+      const int lo = a + min(len, lane * per), hi = a + min(len, (lane + 1) * per);
+      unsigned long long m = ident;
+      for (int x = lo; x < hi; ++x) m = map_apply(s.map[s.let[s.perm[x]]], m, nq);
+      unsigned long long total = ident;
+      for (int l = 0; l < 32; ++l) total = map_apply(__shfl_sync(0xffffffffu, m, l), total, nq);
+      if (lane == 0) s.lmap[c] = total;
+      __syncwarp();
+    }
+    __syncthreads();
+    for (int c = tid; c < C; c += nt) {
+      uint32_t k[kMaxLevels] = {0, 0, 0};
+      for (int x = 0; x < K; ++x) k[x] = s.key[x][s.rep[c]];
+      int ins;
+      const unsigned long long slot = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &h.acc->table_overflow);
+      if (ins < 0) continue;
+      uint32_t dense;
+      if (ins == 1) {
+        dense = (uint32_t)atomicAdd(h.n_leaves, 1ull);
+        T.leaf_aux[slot] = dense;
+        h.leaf_slot_of[dense] = (uint32_t)slot;
+        table_publish(T.leaf_slot, slot, T.epoch);
+      } else {
+        dense = *(volatile uint32_t *)&T.leaf_aux[slot];
+      }
+      atomicAdd(&h.leaf_npart[dense], 1u);
+      const unsigned long long pi = atomicAdd(h.n_part, 1ull);
+      const unsigned long long m = s.lmap[c];
+      h.part[pi] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
+    }
+  }
+}
+
+// H2: exclusive scan of leaf_npart[0 .. n_leaves) -> leaf_off (3 kernels)
+__global__ void __launch_bounds__(1024) heavy_scan_blocks(HeavyParams h) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  const unsigned long long n = *h.n_leaves;
+  const unsigned long long i = (unsigned long long)blockIdx.x * 1024 + threadIdx.x;
+  buf[threadIdx.x] = i < n ? h.leaf_npart[i] : 0u;
+  __syncthreads();
+  const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+  if (i < n) h.leaf_off[i] = buf[threadIdx.x];
+  if (threadIdx.x == 0) h.scan_tmp[blockIdx.x] = tot;
+}
+__global__ void __launch_bounds__(1024) heavy_scan_sums(HeavyParams h, uint32_t nblk) {
+  __shared__ uint32_t buf[1024];
+  __shared__ uint32_t wt[32];
+  uint32_t carry = 0;
+  for (uint32_t o = 0; o < nblk; o += 1024) {
+    const uint32_t i = o + threadIdx.x;
+    buf[threadIdx.x] = i < nblk ? h.scan_tmp[i] : 0u;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < nblk) h.scan_tmp[i] = buf[threadIdx.x] + carry;
+    carry += tot;
+    __syncthreads();
+  }
+}
+__global__ void __launch_bounds__(1024) heavy_scan_add(HeavyParams h) {
+  const unsigned long long n = *h.n_leaves;
+  const unsigned long long i = (unsigned long long)blockIdx.x * 1024 + threadIdx.x;
+  if (i < n) h.leaf_off[i] += h.scan_tmp[blockIdx.x];
+}
+
+// H3: partials grouped by leaf (order inside a group restored in H4)
+__global__ void heavy_group_kernel(HeavyParams h) {
+  const unsigned long long n = *h.n_part;
+  for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
+       p += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint4 r = h.part[p];
+    const uint32_t pos = h.leaf_off[r.x] + atomicAdd(&h.leaf_fill[r.x], 1u);
+    h.lists[pos] = make_uint4(r.y, r.z, r.w, 0u);
+  }
+}
+
+// leaf verdict + its depth-(K-1) parent's child histogram (or the depth-1 counts)
+template <int K>
+__device__ void heavy_leaf_done(const HeavyParams &h, uint32_t dense, int q, int *acc) {
+  const DevProg *prog = h.prog;
+  const DevTables &T = h.tab;
+  const int nf = prog->nf;
+  unsigned long long nslot = 0;
+  bool ok = true;
+  if (K > 1) {
+    const uint4 ks = T.leaf_slot[h.leaf_slot_of[dense]];
+    const uint32_t k[3] = {ks.y, ks.z, ks.w};
+    int ins;
+    nslot = table_find_insert(T.node_slot[K - 1], T.node_cap[K - 1], T.epoch, k, K - 1, &ins, &h.acc->table_overflow);
+    if (ins == 1) {
+      for (int x = 0; x < kMaxFormulas * 6; ++x) T.node_hist[K - 1][nslot * kMaxFormulas * 6 + x] = 0;
+      const uint32_t d = (uint32_t)atomicAdd(&h.n_nodes[K - 1], 1ull);
+      T.node_aux[K - 1][nslot] = d;
+      h.node_list[K - 1][d] = (uint32_t)nslot;
+      table_publish(T.node_slot[K - 1], nslot, T.epoch);
+    }
+    ok = ins >= 0;
+  }
+  for (int f = 0; f < nf; ++f) {
+    const int v = prog->lab[f][q];
+    atomicAdd(&acc[acc_idx(f, K, v)], 1);
+    if (K > 1 && ok) atomicAdd(&T.node_hist[K - 1][nslot * kMaxFormulas * 6 + f * 6 + v], 1u);
+  }
+}
+
+// H4: leaves with <= 32 partials (thread per leaf); longer ones are listed
+template <int K>
+__global__ void __launch_bounds__(256) heavy_short_kernel(HeavyParams h) {
+  __shared__ int acc[kMaxFormulas * (kMaxLevels + 1) * 6];
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  const DevProg *prog = h.prog;
+  const int nq = prog->nq;
+  const unsigned long long n = *h.n_leaves;
+  for (unsigned long long d = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; d < n;
+       d += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t off = h.leaf_off[d], len = h.leaf_npart[d];
+    if (len > 32) {
+      h.long_list[atomicAdd(&h.ctr[2], 1u)] = (uint32_t)d;
+      continue;
+    }
+    // insertion sort of the leaf's partials by segment item, then ordered composition
+    uint4 *l = h.lists + off;
+    for (uint32_t a = 1; a < len; ++a) {
+      const uint4 x = l[a];
+      int bb = (int)a - 1;
+      while (bb >= 0 && l[bb].x > x.x) { l[bb + 1] = l[bb]; --bb; }
+      l[bb + 1] = x;
+    }
+    int q = prog->q0;
+    for (uint32_t a = 0; a < len; ++a) {
+      const unsigned long long m = (unsigned long long)l[a].y | ((unsigned long long)l[a].z << 32);
+      q = (int)((m >> (4 * q)) & 15ull);
+    }
+    (void)nq;
+    heavy_leaf_done<K>(h, (uint32_t)d, q, acc);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const int v = acc[i];
+    const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), b = i % 6;
+    if (v) atomicAdd(&h.acc->hist[f][l][b], (unsigned long long)(long long)v);
+  }
+}
+
+// H4b: long leaves, one CTA each: the segment items of a leaf lie in one
+// bucket's contiguous item range, so partial maps are placed by item and
+// composed with an ordered tree reduction in shared memory.
+constexpr int kLongWin = 4096;
+template <int K>
+__global__ void __launch_bounds__(1024) heavy_long_kernel(HeavyParams h) {
+  __shared__ unsigned long long M[kLongWin];
+  __shared__ int acc[kMaxFormulas * (kMaxLevels + 1) * 6];
+  __shared__ uint32_t red[32];
+  __shared__ uint32_t leaf_i;
+  const DevProg *prog = h.prog;
+  const int nq = prog->nq, tid = threadIdx.x;
+  unsigned long long ident = 0;
+  for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
+  for (int i = tid; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) acc[i] = 0;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) leaf_i = atomicAdd(&h.ctr[3], 1u);
+    __syncthreads();
+    if (leaf_i >= h.ctr[2]) break;
+    const uint32_t d = h.long_list[leaf_i];
+    const uint32_t off = h.leaf_off[d], len = h.leaf_npart[d];
+    // minimum item of the leaf
+    uint32_t mn = 0xFFFFFFFFu;
+    for (uint32_t a = tid; a < len; a += blockDim.x) mn = min(mn, h.lists[off + a].x);
+    for (int o = 16; o; o >>= 1) mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    if ((tid & 31) == 0) red[tid >> 5] = mn;
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t v = tid < (int)(blockDim.x >> 5) ? red[tid] : 0xFFFFFFFFu;
+      for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (tid == 0) red[0] = v;
+    }
+    __syncthreads();
+    const uint32_t base = red[0];
+    unsigned long long total = ident;  // valid in thread 0
+    // items span at most the bucket's segment count; windows of kLongWin items
+    uint32_t span = 0;
+    for (uint32_t a = tid; a < len; a += blockDim.x) span = max(span, h.lists[off + a].x - base + 1);
+    for (int o = 16; o; o >>= 1) span = max(span, __shfl_xor_sync(0xffffffffu, span, o));
+    __syncthreads();
+    if ((tid & 31) == 0) red[tid >> 5] = span;
+    __syncthreads();
+    if (tid < 32) {
+      uint32_t v = tid < (int)(blockDim.x >> 5) ? red[tid] : 0u;
+      for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+      if (tid == 0) red[1] = v;
+    }
+    __syncthreads();
+    const uint32_t nspan = red[1];
+    for (uint32_t w0 = 0; w0 < nspan; w0 += kLongWin) {
+      for (int x = tid; x < kLongWin; x += blockDim.x) M[x] = ident;
+      __syncthreads();
+      for (uint32_t a = tid; a < len; a += blockDim.x) {
+        const uint4 r = h.lists[off + a];
+        const uint32_t pos = r.x - base;
+        if (pos >= w0 && pos < w0 + kLongWin)
+          M[pos - w0] = (unsigned long long)r.y | ((unsigned long long)r.z << 32);
+      }
+      __syncthreads();
+      for (int stride = 1; stride < kLongWin; stride <<= 1) {  // ordered tree: M[i] = M[i+s] o M[i]
+        for (int x = tid * 2 * stride; x + stride < kLongWin; x += blockDim.x * 2 * stride)
+          M[x] = map_apply(M[x + stride], M[x], nq);
+        __syncthreads();
+      }
+      if (tid == 0) total = map_apply(M[0], total, nq);
+      __syncthreads();
+    }
+    if (tid == 0) heavy_leaf_done<K>(h, d, (int)((total >> (4 * prog->q0)) & 15ull), acc);
+  }
+  __syncthreads();
+  for (int i = tid; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const int v = acc[i];
+    const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), b = i % 6;
+    if (v) atomicAdd(&h.acc->hist[f][l][b], (unsigned long long)(long long)v);
+  }
+}
+
+// H5: node verdicts of depth l (Def. 6) and their parents' child histograms
+template <int K>
+__global__ void __launch_bounds__(256) heavy_nodes_kernel(HeavyParams h, int l) {
+  __shared__ int acc[kMaxFormulas * (kMaxLevels + 1) * 6];
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) acc[i] = 0;
+  __syncthreads();
+  const DevProg *prog = h.prog;
+  const DevTables &T = h.tab;
+  const int nf = prog->nf;
+  const unsigned long long n = h.n_nodes[l];
+  for (unsigned long long d = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; d < n;
+       d += (unsigned long long)gridDim.x * blockDim.x) {
+    const uint32_t slot = h.node_list[l][d];
+    unsigned long long pslot = 0;
+    bool ok = true;
+    if (l > 1) {
+      const uint4 ks = T.node_slot[l][slot];
+      const uint32_t k[3] = {ks.y, ks.z, ks.w};
+      int ins;
+      pslot = table_find_insert(T.node_slot[l - 1], T.node_cap[l - 1], T.epoch, k, l - 1, &ins, &h.acc->table_overflow);
+      if (ins == 1) {
+        for (int x = 0; x < kMaxFormulas * 6; ++x) T.node_hist[l - 1][pslot * kMaxFormulas * 6 + x] = 0;
+        const uint32_t dd = (uint32_t)atomicAdd(&h.n_nodes[l - 1], 1ull);
+        T.node_aux[l - 1][pslot] = dd;
+        h.node_list[l - 1][dd] = (uint32_t)pslot;
+        table_publish(T.node_slot[l - 1], pslot, T.epoch);
+      }
+      ok = ins >= 0;
+    }
+    for (int f = 0; f < nf; ++f) {
+      const uint32_t *hh = T.node_hist[l] + (size_t)slot * kMaxFormulas * 6 + f * 6;
+      const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], hh);
+      atomicAdd(&acc[acc_idx(f, l, v)], 1);
+      if (l > 1 && ok) atomicAdd(&T.node_hist[l - 1][pslot * kMaxFormulas * 6 + f * 6 + v], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const int v = acc[i];
+    const int f = i / ((kMaxLevels + 1) * 6), ll = (i / 6) % (kMaxLevels + 1), b = i % 6;
+    if (v) atomicAdd(&h.acc->hist[f][ll][b], (unsigned long long)(long long)v);
+  }
+}
+
 // ----------------------------------------------- finalize
 __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *out) {
   const int f = threadIdx.x;
@@ -893,7 +1242,7 @@ __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *
   } while (0)
 
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
-  const size_t sm = smem_bytes(K, nf, false);
+  const size_t sm = smem_bytes(K, nf, 0);
   switch (K) {
     case 1: cudaFuncSetAttribute(bucket_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
@@ -920,7 +1269,7 @@ cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t gr
 size_t bucket_warp_smem(int K, int nf, int warps) { return warp_cta_smem_bytes(K, nf, warps); }
 
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
-  const size_t sm = smem_bytes(K, nf, true);
+  const size_t sm = smem_bytes(K, nf, 1);
   switch (K) {
     case 1: cudaFuncSetAttribute(bucket_global_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
@@ -937,6 +1286,35 @@ cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_leve
   for (int l = 1; l < n_levels; ++l) mx = mx > from.node_cap[l] ? mx : from.node_cap[l];
   dim3 grid((unsigned)((mx + 255) / 256), (unsigned)n_levels);
   LTL4C_LAUNCH(kKRehash, rehash_kernel<<<grid, 256, 0, L.stream>>>(from, to, n_levels, nf, overflow));
+}
+
+
+template <int K>
+static cudaError_t heavy_all(const HeavyParams &h, int nf, int n_sms, const Launcher &L) {
+  if (L.before) L.before(L.ctx, kKHeavy);
+  heavy_plan_kernel<<<1, 1024, 0, L.stream>>>(h);
+  const size_t sm = smem_bytes(K, nf, 2);
+  cudaFuncSetAttribute(heavy_seg_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  heavy_seg_kernel<K><<<2 * n_sms, kBucketThreads, sm, L.stream>>>(h);
+  const uint32_t nblk = (uint32_t)((h.cap_leaves + 1023) / 1024);
+  heavy_scan_blocks<<<nblk ? nblk : 1, 1024, 0, L.stream>>>(h);
+  heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h, nblk ? nblk : 1);
+  heavy_scan_add<<<nblk ? nblk : 1, 1024, 0, L.stream>>>(h);
+  heavy_group_kernel<<<4 * n_sms, 256, 0, L.stream>>>(h);
+  heavy_short_kernel<K><<<4 * n_sms, 256, 0, L.stream>>>(h);
+  heavy_long_kernel<K><<<n_sms, 1024, 0, L.stream>>>(h);
+  for (int l = K - 1; l >= 1; --l) heavy_nodes_kernel<K><<<4 * n_sms, 256, 0, L.stream>>>(h, l);
+  cudaError_t e = cudaGetLastError();
+  if (L.after) L.after(L.ctx, kKHeavy);
+  return e;
+}
+
+cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L) {
+  switch (K) {
+    case 1: return heavy_all<1>(h, nf, n_sms, L);
+    case 2: return heavy_all<2>(h, nf, n_sms, L);
+    default: return heavy_all<3>(h, nf, n_sms, L);
+  }
 }
 
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L) {

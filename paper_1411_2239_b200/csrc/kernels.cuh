@@ -44,6 +44,39 @@ struct DevTables {
   uint4 *node_slot[kMaxLevels];         // level l in [1, n-1]
   uint32_t *node_verdict[kMaxLevels];   // 4 x u8 packed, 0xFF = none
   uint32_t *node_hist[kMaxLevels];      // [cap][F][6]
+  uint32_t *leaf_aux;                   // heavy path: dense leaf id per slot
+  uint32_t *node_aux[kMaxLevels];       // heavy path: dense node id per slot
+};
+
+// Heavy path (buckets larger than one shared-memory chunk, offline): segments of
+// kCap events are processed in parallel; each emits, per leaf, the ordered
+// composition of its transition maps (a "partial"); partials are grouped by leaf
+// and composed in segment order (the segmented transition-map scan of SURVEY
+// §8(a) a4); leaves and nodes are then aggregated through the global tables.
+struct HeavyParams {
+  const uint32_t *key[kMaxLevels];
+  const uint8_t *let;
+  const uint32_t *bucket_off;
+  const uint32_t *list;                 // oversize buckets
+  const unsigned long long *list_len;
+  const DevProg *prog;
+  DevAcc *acc;
+  DevTables tab;
+  uint32_t *seg_base;                   // [list_len + 1]
+  uint32_t *ctr;                        // [8] work counters (zeroed)
+  uint4 *part;                          // {dense leaf, segment item, map lo, map hi}
+  unsigned long long *n_part;
+  unsigned long long *n_leaves;
+  uint32_t *leaf_slot_of;               // dense leaf -> table slot
+  uint32_t *leaf_npart;                 // [dense] (zeroed)
+  uint32_t *leaf_off;                   // [dense] exclusive scan of leaf_npart
+  uint32_t *leaf_fill;                  // [dense] (zeroed)
+  uint4 *lists;                         // partials grouped by leaf
+  uint32_t *long_list;                  // dense leaves with > 32 partials
+  uint32_t *node_list[kMaxLevels];      // dense node -> slot, per level
+  unsigned long long *n_nodes;          // [kMaxLevels]
+  uint32_t *scan_tmp;                   // block sums of the leaf_npart scan
+  unsigned long long cap_leaves;        // upper bound of dense leaves (host)
 };
 
 struct BucketParams {
@@ -86,6 +119,7 @@ enum KernelId {
   kKBucketGlobal,
   kKFinalize,
   kKRehash,
+  kKHeavy,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -98,6 +132,7 @@ cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t gr
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 size_t bucket_warp_smem(int K, int nf, int warps);
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L);
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);

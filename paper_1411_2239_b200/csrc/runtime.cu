@@ -63,13 +63,17 @@ struct Tables {
   DevTables d{};
   DevBuf<uint4> leaf_slot;
   DevBuf<uint8_t> leaf_state;
+  DevBuf<uint32_t> leaf_aux;
+  DevBuf<uint32_t> node_aux[kMaxLevels];
   DevBuf<uint4> node_slot[kMaxLevels];
   DevBuf<uint32_t> node_verdict[kMaxLevels];
   DevBuf<uint32_t> node_hist[kMaxLevels];
   void release() {
     leaf_slot.release();
     leaf_state.release();
+    leaf_aux.release();
     for (int l = 0; l < kMaxLevels; ++l) {
+      node_aux[l].release();
       node_slot[l].release();
       node_verdict[l].release();
       node_hist[l].release();
@@ -109,6 +113,10 @@ struct ltl4c_state {
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
+  // heavy path buffers
+  DevBuf<uint4> h_part, h_lists;
+  DevBuf<uint32_t> h_u32;  // seg_base | leaf_slot_of | leaf_npart | leaf_off | leaf_fill | long_list | scan_tmp | node lists
+  DevBuf<unsigned long long> h_cnt;
   // stats / profiling
   bool profiling = false;
   uint64_t verifies = 0, launches = 0;
@@ -171,10 +179,15 @@ int ceil_log2(uint64_t x) {
   return b;
 }
 
-ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_t node_cap, cudaStream_t s) {
+ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_t node_cap, cudaStream_t s,
+                          bool aux = false) {
   const int nl = (int)st->prog->n_levels;
   CU(t.leaf_slot.ensure(leaf_cap));
   CU(t.leaf_state.ensure(leaf_cap));
+  if (aux) {
+    CU(t.leaf_aux.ensure(leaf_cap));
+    t.d.leaf_aux = t.leaf_aux.p;
+  }
   CU(cudaMemsetAsync(t.leaf_slot.p, 0, sizeof(uint4) * leaf_cap, s));
   t.d.leaf_cap = leaf_cap;
   t.d.leaf_slot = t.leaf_slot.p;
@@ -184,6 +197,10 @@ ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_
     CU(t.node_verdict[l].ensure(node_cap));
     CU(t.node_hist[l].ensure(node_cap * kMaxFormulas * 6));
     CU(cudaMemsetAsync(t.node_slot[l].p, 0, sizeof(uint4) * node_cap, s));
+    if (aux) {
+      CU(t.node_aux[l].ensure(node_cap));
+      t.d.node_aux[l] = t.node_aux[l].p;
+    }
     t.d.node_cap[l] = node_cap;
     t.d.node_slot[l] = t.node_slot[l].p;
     t.d.node_verdict[l] = t.node_verdict[l].p;
@@ -223,6 +240,60 @@ ltl4c_status ensure_online_tables(ltl4c_state *st, uint64_t extra, cudaStream_t 
   t.release();
   t = nt;
   nt = Tables{};  // ownership moved (DevBuf members copied; prevent double free)
+  return LTL4C_OK;
+}
+
+
+// Heavy path for the oversize buckets of an offline verify (sizes known on the
+// host from the first result copy).
+ltl4c_status run_heavy(ltl4c_state *st, const BucketParams &bp, int K, cudaStream_t s, const Launcher &L) {
+  const uint64_t ev = st->h_out->oversize_events;
+  const uint64_t nb = st->h_out->oversize_buckets;
+  const uint64_t cap = 1ull << std::max(12, ceil_log2(2 * ev + 1));
+  if (st->tab.d.leaf_cap < cap || !st->tab.d.leaf_aux || (K > 1 && st->tab.d.node_cap[1] < cap)) {
+    st->tab.release();
+    ltl4c_status r = alloc_tables(st, st->tab, cap, cap, s, true);
+    if (r) return r;
+  }
+  st->tab.d.epoch = ++st->epoch;
+  const uint64_t nblk = (ev + 1023) / 1024 + 1;
+  const size_t nseg = nb + 1;
+  const size_t u32_need = nseg + 5 * ev + nblk + (size_t)(K - 1) * cap + 16;
+  CU(st->h_part.ensure(ev + 1));
+  CU(st->h_lists.ensure(ev + 1));
+  CU(st->h_u32.ensure(u32_need));
+  CU(st->h_cnt.ensure(16));
+  HeavyParams h{};
+  for (int k = 0; k < K; ++k) h.key[k] = bp.key[k];
+  h.let = bp.let;
+  h.bucket_off = bp.bucket_off;
+  h.list = bp.oversize_list;
+  h.list_len = &st->d_acc.p->oversize_buckets;
+  h.prog = bp.prog;
+  h.acc = bp.acc;
+  h.tab = st->tab.d;
+  uint32_t *u = st->h_u32.p;
+  h.seg_base = u; u += nseg;
+  h.leaf_slot_of = u; u += ev;
+  h.leaf_npart = u; u += ev;
+  h.leaf_off = u; u += ev;
+  h.leaf_fill = u; u += ev;
+  h.long_list = u; u += ev;
+  h.scan_tmp = u; u += nblk;
+  for (int l = 1; l < K; ++l) { h.node_list[l] = u; u += cap; }
+  h.ctr = u; u += 8;
+  h.part = st->h_part.p;
+  h.lists = st->h_lists.p;
+  unsigned long long *c = st->h_cnt.p;
+  h.n_part = c;
+  h.n_leaves = c + 1;
+  h.n_nodes = c + 4;  // [kMaxLevels]
+  h.cap_leaves = ev;
+  CU(cudaMemsetAsync(h.leaf_npart, 0, sizeof(uint32_t) * 2 * ev, s));  // npart, off
+  CU(cudaMemsetAsync(h.leaf_fill, 0, sizeof(uint32_t) * ev, s));
+  CU(cudaMemsetAsync(h.ctr, 0, sizeof(uint32_t) * 8, s));
+  CU(cudaMemsetAsync(c, 0, sizeof(unsigned long long) * 16, s));
+  CU(launch_heavy(h, K, (int)st->prog->n_formulas, st->n_sms, L));
   return LTL4C_OK;
 }
 
@@ -317,20 +388,9 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
       CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       if (st->h_out->oversize_buckets > 0) {
-        // buckets larger than one shared-memory chunk: chunked path with
-        // per-verify tables (fresh epoch, no clearing needed)
-        const uint64_t ev = st->h_out->oversize_events;
-        const uint64_t want = 1ull << std::max(12, ceil_log2(2 * ev + 1));
-        if (st->tab.d.leaf_cap < want || (K > 1 && st->tab.d.node_cap[1] < want)) {
-          st->tab.release();
-          ltl4c_status r = alloc_tables(st, st->tab, want, want, s);
-          if (r) return r;
-        }
-        st->tab.d.epoch = ++st->epoch;
-        bp.tab = st->tab.d;
-        bp.list = st->oversize_list.p;
-        bp.list_len = &st->d_acc.p->oversize_buckets;
-        CU(launch_bucket_global(bp, K, (int)prog->n_formulas, (uint32_t)st->h_out->oversize_buckets, L));
+        // buckets larger than one shared-memory chunk: segmented heavy path
+        ltl4c_status r = run_heavy(st, bp, K, s, L);
+        if (r) return r;
         CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
         CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
@@ -564,6 +624,10 @@ void ltl4c_state_free(ltl4c_state *st) {
   for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
   st->hlet.release();
   st->tab.release();
+  st->h_part.release();
+  st->h_lists.release();
+  st->h_u32.release();
+  st->h_cnt.release();
   for (auto &t : st->pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
