@@ -125,6 +125,13 @@ struct ltl4c_state {
   std::vector<PendingTiming> pending;
   std::vector<cudaEvent_t> event_pool;
   cudaStream_t cur_stream = nullptr;
+  // CUDA graph of the offline launch sequence
+  bool graphs = true;
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<uintptr_t> graph_key;
+  uint64_t graph_kernels = 0;
+  uint64_t k_launches_saved[kKNumKernels] = {};
 };
 
 namespace {
@@ -297,40 +304,64 @@ ltl4c_status run_heavy(ltl4c_state *st, const BucketParams &bp, int K, cudaStrea
   return LTL4C_OK;
 }
 
-ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, ltl4c_result *out,
-                        const uint32_t *const *keys, const uint8_t *letters) {
+struct Plan {
+  uint64_t N = 0;
+  int B = 0, P = 0;
+  uint32_t NB = 0, n_tiles = 0;
+};
+
+// Buffer sizes for a batch of N events (all allocation happens here, outside
+// any stream capture).
+ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
+  const int K = (int)st->prog->n_levels;
+  pl->N = N;
+  if (N == 0) return LTL4C_OK;
+  const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
+  pl->B = std::min(kMaxPasses * kMaxDigitBits, std::max(1, ceil_log2(target)));
+  pl->P = (pl->B + kMaxDigitBits - 1) / kMaxDigitBits;
+  pl->NB = 1u << pl->B;
+  pl->n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
+  for (int i = 0; i < 2; ++i) {
+    for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
+    CU(st->buflet[i].ensure(N));
+  }
+  CU(st->counts.ensure((size_t)256 * pl->n_tiles));
+  CU(st->totals.ensure(kMaxPasses * 256 + 16));
+  CU(st->bucket_off.ensure((size_t)pl->NB + 1));
+  CU(st->oversize_list.ensure(pl->NB));
+  CU(st->medium_list.ensure(pl->NB));
+  return LTL4C_OK;
+}
+
+BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
+  const int K = (int)st->prog->n_levels;
+  BucketParams bp{};
+  const int fin = (pl.P - 1) & 1;
+  for (int l = 0; l < K; ++l) bp.key[l] = st->bufkey[fin][l].p;
+  bp.let = st->buflet[fin].p;
+  bp.bucket_off = st->bucket_off.p;
+  bp.n_buckets = pl.NB;
+  bp.oversize_list = st->oversize_list.p;
+  bp.medium_list = st->medium_list.p;
+  bp.bucket_counter = st->totals.p + kMaxPasses * 256 + 8;
+  bp.warps_per_cta = st->warps_per_cta;
+  bp.prog = st->d_prog.p;
+  bp.acc = st->d_acc.p;
+  bp.tab = st->tab.d;
+  return bp;
+}
+
+// Everything of one verify up to the first result copy, enqueued on s:
+// memsets, SortTrace (count / scan / scatter per pass), mu, the bucket kernels,
+// finalize and the D2H copy of the result record.
+ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *const *keys, const uint8_t *letters,
+                          cudaStream_t s, const Launcher &L) {
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
-  const uint64_t N = b->n_events;
-  st->cur_stream = s;
-  Launcher L{s, before_launch, after_launch, st};
-  if (!online) {
-    CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
-    st->events_seen = 0;
-  }
-  st->events_seen += N;
+  if (!online) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
   CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
-  if (online) {
-    ltl4c_status r = ensure_online_tables(st, N, s, L);
-    if (r) return r;
-  }
-  if (N > 0) {
-    const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
-    const int B = std::min(kMaxPasses * kMaxDigitBits, std::max(1, ceil_log2(target)));
-    const int P = (B + kMaxDigitBits - 1) / kMaxDigitBits;
-    const uint32_t NB = 1u << B;
-    const uint32_t n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
-    for (int i = 0; i < 2; ++i) {
-      for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
-      CU(st->buflet[i].ensure(N));
-    }
-    CU(st->counts.ensure((size_t)256 * n_tiles));
-    CU(st->totals.ensure(kMaxPasses * 256 + 16));
-    CU(st->bucket_off.ensure((size_t)NB + 1));
-    CU(st->oversize_list.ensure(NB));
-    CU(st->medium_list.ensure(NB));
-    // one memset: digit totals [3][256] + scheduler counters
+  if (plan.N > 0) {
     CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
     PartPlan pl{};
     for (int l = 0; l < K; ++l) {
@@ -341,14 +372,14 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     pl.in_let = letters;
     pl.buf_let[0] = st->buflet[0].p;
     pl.buf_let[1] = st->buflet[1].p;
-    pl.n = N;
-    pl.n_tiles = n_tiles;
+    pl.n = plan.N;
+    pl.n_tiles = plan.n_tiles;
     pl.K = K;
-    pl.bits = B;
-    pl.passes = P;
+    pl.bits = plan.B;
+    pl.passes = plan.P;
     int lo = 0;
-    for (int pass = 0; pass < P; ++pass) {
-      const int width = (B - lo + (P - pass) - 1) / (P - pass);
+    for (int pass = 0; pass < plan.P; ++pass) {
+      const int width = (plan.B - lo + (plan.P - pass) - 1) / (plan.P - pass);
       pl.lo[pass] = lo;
       pl.width[pass] = width;
       lo += width;
@@ -357,56 +388,100 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     pl.counts = st->counts.p;
     pl.nvalid = st->d_nvalid.p;
     pl.acc = st->d_acc.p;
-    for (int pass = 0; pass < P; ++pass) {
+    for (int pass = 0; pass < plan.P; ++pass) {
       CU(launch_part_count(pl, pass, L));
       CU(launch_part_scan(pl, pass, L));
       CU(launch_part_scatter(pl, pass, L));
     }
-    CU(launch_bucket_bounds(pl, st->bucket_off.p, NB, L));
-    BucketParams bp{};
-    const int fin = (P - 1) & 1;
-    for (int l = 0; l < K; ++l) bp.key[l] = st->bufkey[fin][l].p;
-    bp.let = st->buflet[fin].p;
-    bp.bucket_off = st->bucket_off.p;
-    bp.n_buckets = NB;
-    bp.oversize_list = st->oversize_list.p;
-    bp.medium_list = st->medium_list.p;
-    bp.bucket_counter = st->totals.p + kMaxPasses * 256 + 8;
-    bp.warps_per_cta = st->warps_per_cta;
-    bp.prog = st->d_prog.p;
-    bp.acc = st->d_acc.p;
+    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L));
+    BucketParams bp = bucket_params(st, plan);
     if (!online) {
       // warp per bucket; buckets above kWarpCap events go to the CTA kernel,
-      // above kCap to the chunked global path
+      // above kCap to the heavy path (after the first result copy)
       CU(launch_bucket_warp(bp, K, (int)prog->n_formulas,
-                            (uint32_t)std::min<uint64_t>(NB, (uint64_t)st->n_sms * st->warp_ctas_per_sm), L));
+                            (uint32_t)std::min<uint64_t>(plan.NB, (uint64_t)st->n_sms * st->warp_ctas_per_sm), L));
       BucketParams mp = bp;
       mp.list = st->medium_list.p;
       mp.list_len = &st->d_acc.p->medium_buckets;
       CU(launch_bucket_fast(mp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
-      CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
-      CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
-      CU(cudaStreamSynchronize(s));
-      if (st->h_out->oversize_buckets > 0) {
-        // buckets larger than one shared-memory chunk: segmented heavy path
-        ltl4c_status r = run_heavy(st, bp, K, s, L);
-        if (r) return r;
-        CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
-        CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
-        CU(cudaStreamSynchronize(s));
-      }
     } else {
-      bp.tab = st->tab.d;
-      CU(launch_bucket_global(bp, K, (int)prog->n_formulas, NB, L));
-      CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
-      CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
-      CU(cudaStreamSynchronize(s));
+      CU(launch_bucket_global(bp, K, (int)prog->n_formulas, plan.NB, L));
     }
+  }
+  CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+  CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+  return LTL4C_OK;
+}
+
+void drop_graph(ltl4c_state *st) {
+  if (st->graph_exec) cudaGraphExecDestroy(st->graph_exec);
+  st->graph_exec = nullptr;
+  st->graph_key.clear();
+}
+
+ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, ltl4c_result *out,
+                        const uint32_t *const *keys, const uint8_t *letters) {
+  const ltl4c_program *prog = st->prog;
+  const int K = (int)prog->n_levels;
+  const bool online = st->flags & LTL4C_STATE_ONLINE;
+  const uint64_t N = b->n_events;
+  st->cur_stream = s;
+  Launcher L{s, before_launch, after_launch, st};
+  if (!online) st->events_seen = 0;
+  st->events_seen += N;
+  if (online) {
+    ltl4c_status r = ensure_online_tables(st, N, s, L);
+    if (r) return r;
+  }
+  Plan plan;
+  {
+    ltl4c_status r = plan_batch(st, N, &plan);
+    if (r) return r;
+  }
+  // Offline batches replay a captured CUDA graph of the launch sequence (one
+  // graph per input pointers / size); profiling runs the sequence directly so
+  // every kernel can be bracketed by events.
+  const bool use_graph = !online && !st->profiling && st->graphs && N > 0;
+  if (use_graph) {
+    std::vector<uintptr_t> key = {(uintptr_t)N, (uintptr_t)letters};
+    for (int l = 0; l < K; ++l) key.push_back((uintptr_t)keys[l]);
+    if (st->graph_key != key || !st->graph_exec) {
+      drop_graph(st);
+      if (!st->cap_stream) CU(cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking));
+      const uint64_t before = st->launches;
+      Launcher LC{st->cap_stream, nullptr, after_launch, st};
+      st->cur_stream = st->cap_stream;
+      CU(cudaStreamBeginCapture(st->cap_stream, cudaStreamCaptureModeThreadLocal));
+      ltl4c_status r = enqueue_main(st, plan, keys, letters, st->cap_stream, LC);
+      cudaGraph_t g = nullptr;
+      cudaError_t ec = cudaStreamEndCapture(st->cap_stream, &g);
+      st->cur_stream = s;
+      if (r) { if (g) cudaGraphDestroy(g); return r; }
+      CU(ec);
+      cudaError_t ei = cudaGraphInstantiate(&st->graph_exec, g, 0);
+      cudaGraphDestroy(g);
+      CU(ei);
+      st->graph_kernels = st->launches - before;
+      st->launches = before;  // counted per replay below
+      for (int k = 0; k < kKNumKernels; ++k) st->k_launches[k] = st->k_launches_saved[k];
+      st->graph_key = key;
+    }
+    CU(cudaGraphLaunch(st->graph_exec, s));
+    st->launches += st->graph_kernels;
   } else {
+    ltl4c_status r = enqueue_main(st, plan, keys, letters, s, L);
+    if (r) return r;
+  }
+  CU(cudaStreamSynchronize(s));
+  if (!online && N > 0 && st->h_out->oversize_buckets > 0) {
+    // buckets larger than one shared-memory chunk: segmented heavy path
+    ltl4c_status r = run_heavy(st, bucket_params(st, plan), K, s, L);
+    if (r) return r;
     CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
     CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
   }
+  for (int k = 0; k < kKNumKernels; ++k) st->k_launches_saved[k] = st->k_launches[k];
   if (st->h_out->table_overflow)
     return fail(LTL4C_E_OOM, "carried table overflow");
   for (uint32_t f = 0; f < prog->n_formulas; ++f) {
@@ -505,6 +580,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   st->prog = prog;
   st->device = device;
   st->flags = flags;
+  st->graphs = std::getenv("LTL4C_NO_GRAPH") == nullptr;
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;
@@ -633,6 +709,8 @@ void ltl4c_state_free(ltl4c_state *st) {
     cudaEventDestroy(t.b);
   }
   for (auto e : st->event_pool) cudaEventDestroy(e);
+  drop_graph(st);
+  if (st->cap_stream) cudaStreamDestroy(st->cap_stream);
   if (st->h_out) cudaFreeHost(st->h_out);
   cudaSetDevice(prev);
   delete st;
@@ -665,6 +743,7 @@ ltl4c_status ltl4c_state_stats_reset(ltl4c_state *st) {
   st->verifies = st->launches = 0;
   for (int k = 0; k < kKNumKernels; ++k) {
     st->k_launches[k] = 0;
+    st->k_launches_saved[k] = 0;
     st->k_ms[k] = 0.0;
   }
   return LTL4C_OK;
