@@ -365,6 +365,8 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 // store the index of a representative event; keys are compared in place in the
 // (L1-resident) partitioned arrays.  The next bucket is prefetched into L1
 // while the current one is processed.
+constexpr int kIlp = 4;  // events per lane per window
+
 struct WarpSmem {
   uint32_t *key[kMaxLevels];   // [kWarpCap] staged keys of the bucket
   uint8_t *let;                // [kWarpCap]
@@ -533,43 +535,58 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     }
     __syncwarp();
     have = grab(b, start, cnt);  // prefetch of the next bucket overlaps the work below
-    // a3 + a4: rounds of 32 events in trace order
-    for (uint32_t base = 0; base < cur_cnt; base += 32) {
-      const int e = (int)(base + lane);
-      const bool act = e < (int)cur_cnt;
-      const uint32_t am = __ballot_sync(0xffffffffu, act);
-      // every lane probes its own vector; a round needs the ordered (match) path
-      // only if two of its lanes carry the same vector
-      uint32_t kk[K];
-      int slot = -1;
-      bool isnew = false;
-      if (act) {
+    // a3 + a4: windows of 32 x kIlp events in trace order.  Every lane probes
+    // kIlp events (independent, for memory-level parallelism); new slots start at
+    // q0.  If no vector repeats inside the window each slot is stepped once;
+    // otherwise the window is replayed as kIlp sub-rounds of 32 in which lanes
+    // sharing a slot are grouped with __match_any_sync and their leader applies
+    // the letters in lane order (so every slice u^D is stepped in trace order).
+    for (uint32_t base = 0; base < cur_cnt; base += 32 * kIlp) {
+      int slot[kIlp];
 #pragma unroll
-        for (int k = 0; k < K; ++k) kk[k] = bk.get(k, e);
-        uint32_t hsh = 0;
+      for (int r = 0; r < kIlp; ++r) {
+        const int e = (int)(base + 32 * r + lane);
+        slot[r] = -1;
+        if (e < (int)cur_cnt) {
+          uint32_t hsh = 0;
 #pragma unroll
-        for (int k = 0; k < K; ++k) hsh = (hsh ^ kk[k]) * (0x9E3779B1u + 0x7F4A7C16u * k);
-        slot = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
-        w.lmark[slot] = (uint16_t)e;
+          for (int k = 0; k < K; ++k) hsh = (hsh ^ bk.get(k, e)) * (0x9E3779B1u + 0x7F4A7C16u * k);
+          bool isnew;
+          slot[r] = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
+          if (isnew) w.lstate[slot[r]] = (uint8_t)q0;
+        }
       }
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r)
+        if (slot[r] >= 0) w.lmark[slot[r]] = (uint16_t)(base + 32 * r + lane);
       __syncwarp();
-      // two lanes with one slot: at least one of them sees the other's mark
-      const bool dup_here = act && w.lmark[slot] != (uint16_t)e;
-      const bool any_dup = __any_sync(0xffffffffu, dup_here);
-      if (!any_dup) {
-        if (act) w.lstate[slot] = sdelta[(isnew ? q0 : (uint32_t)w.lstate[slot]) * A + w.let[e]];
-      } else if (act) {
-        const uint32_t peers = __match_any_sync(am, (uint32_t)slot);
-        if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
-          const int rep = (int)w.ltag[slot] - 1;
-          uint32_t q = rep >= (int)base ? q0 : w.lstate[slot];  // created in this round?
-          uint32_t m = peers;
-          while (m) {
-            const int i = __ffs(m) - 1;
-            m &= m - 1;
-            q = sdelta[q * A + w.let[base + i]];
+      bool dup = false;
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r)
+        if (slot[r] >= 0) dup |= w.lmark[slot[r]] != (uint16_t)(base + 32 * r + lane);
+      if (!__any_sync(0xffffffffu, dup)) {
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r)
+          if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[w.lstate[slot[r]] * A + w.let[base + 32 * r + lane]];
+      } else {
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r) {
+          const bool act = slot[r] >= 0;
+          const uint32_t am = __ballot_sync(0xffffffffu, act);
+          if (act) {
+            const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
+            if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
+              uint32_t q = w.lstate[slot[r]];
+              uint32_t m = peers;
+              while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1;
+                q = sdelta[q * A + w.let[base + 32 * r + i]];
+              }
+              w.lstate[slot[r]] = (uint8_t)q;
+            }
           }
-          w.lstate[slot] = (uint8_t)q;
+          __syncwarp();
         }
       }
       __syncwarp();
