@@ -507,6 +507,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       }
 #pragma unroll
       for (int j = 0; j < kWarpCap / 32; ++j) {
+        if ((uint32_t)j * 32 >= cnt) break;
         const uint32_t i = j * 32 + lane;
         if (i < cnt) {
 #pragma unroll
@@ -526,6 +527,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     for (int k = 0; k < K; ++k) bk.k[k] = w.key[k];
 #pragma unroll
     for (int j = 0; j < kWarpCap / 32; ++j) {
+      if ((uint32_t)j * 32 >= cur_cnt) break;
       const uint32_t i = j * 32 + lane;
       if (i < cur_cnt) {
 #pragma unroll
@@ -595,18 +597,30 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     // a5 (i): the ancestors of every leaf at depths 1 .. K-1 (P)
     bool ovf = false;
     if (K > 1) {
+      // per-lane cache of the last ancestor per depth (leaves of a bucket share few)
+      int cslot[kMaxLevels] = {-1, -1, -1};
+      uint32_t ck0 = 0, ck1 = 0;
       for (uint32_t i = lane; i < nleaf && !ovf; i += 32) {
         const int rep = (int)w.ltag[w.llist[i]] - 1;
+        const uint32_t k0 = bk.get(0, rep), k1 = K > 2 ? bk.get(1, rep) : 0u;
         int parent = -1;
         for (int l = 1; l < K; ++l) {
-          bool isnew;
-          const int ns = warp_probe<K>(w.ntag[l], kNodeSlots, bk, rep, l, bk.hash(rep, l), &isnew, &w.cnt[l],
-                                       node_limit, w.nlist[l]);
-          if (ns < 0) { ovf = true; break; }
+          int ns;
+          if (cslot[l] >= 0 && k0 == ck0 && (l < 2 || k1 == ck1)) {
+            ns = cslot[l];
+          } else {
+            bool isnew;
+            ns = warp_probe<K>(w.ntag[l], kNodeSlots, bk, rep, l, bk.hash(rep, l), &isnew, &w.cnt[l], node_limit,
+                               w.nlist[l]);
+            if (ns < 0) { ovf = true; break; }
+            if (isnew && l > 1) w.npar[l][ns] = (uint16_t)parent;
+          }
           w.lnode[l][i] = (uint16_t)ns;
-          if (isnew && l > 1) w.npar[l][ns] = (uint16_t)parent;
+          cslot[l] = ns;
           parent = ns;
         }
+        ck0 = k0;
+        ck1 = k1;
       }
     }
     ovf = __any_sync(0xffffffffu, ovf);
