@@ -424,13 +424,14 @@ template <int K>
 struct BucketKeys {
   const uint32_t *k[K];
   __device__ __forceinline__ uint32_t get(int i, int e) const { return k[i][e]; }
-  // multiplicative hash of the m-key prefix (table index = top bits)
+  // hash of the m-key prefix (table index = top bits): one multiply per key
+  // word, then a murmur finaliser
   __device__ __forceinline__ uint32_t hash(int e, int m) const {
     uint32_t h = 0;
 #pragma unroll
     for (int i = 0; i < K; ++i)
-      if (i < m) h = (h ^ get(i, e)) * (0x9E3779B1u + 0x7F4A7C16u * i);
-    return h;
+      if (i < m) h += get(i, e) * (0x9E3779B1u + 0x7F4A7C16u * i);
+    return fmix32(h);
   }
   __device__ __forceinline__ bool same(int a, int b, int m) const {
     bool eq = true;
@@ -550,9 +551,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         const int e = (int)(base + 32 * r + lane);
         slot[r] = -1;
         if (e < (int)cur_cnt) {
-          uint32_t hsh = 0;
-#pragma unroll
-          for (int k = 0; k < K; ++k) hsh = (hsh ^ bk.get(k, e)) * (0x9E3779B1u + 0x7F4A7C16u * k);
+          const uint32_t hsh = bk.hash(e, K);
           bool isnew;
           slot[r] = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
           if (isnew) w.lstate[slot[r]] = (uint8_t)q0;

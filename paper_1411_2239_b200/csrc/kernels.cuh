@@ -13,7 +13,7 @@ constexpr int kMaxPasses = 3;        // bucket bits <= 24
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
 constexpr int kWarpCap = 512;        // events per warp-processed bucket
-constexpr int kLeafSlots = 512;      // warp leaf table (<= kWarpCap leaves: never full)
+constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
 constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
