@@ -150,11 +150,16 @@ void ltl4c_program_free(ltl4c_program *prog);
 ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t capacity_hint,
                                 uint32_t flags, ltl4c_state **out);
 
-/* Multi-GPU: join a communicator of n_ranks processes (one per GPU).  nccl_id is
- * the 128-byte ncclUniqueId, created by rank 0 and broadcast by the caller.
- * Afterwards ltl4c_verify shards events by hash(k0) across ranks (all-to-all)
- * and sums the per-level counts (all-reduce); every rank returns the global
- * result.  Not yet implemented in this build: returns LTL4C_E_INVALID. */
+/* Multi-GPU: rank 0 creates a 128-byte ncclUniqueId with
+ * ltl4c_nccl_unique_id and the caller broadcasts it (e.g. torch.distributed);
+ * every rank then calls ltl4c_state_comm before its first verify.  n_ranks must
+ * be a power of two <= 256.  Afterwards each ltl4c_verify call takes this rank's
+ * contiguous slice of the trace (rank r's events precede rank r+1's), routes
+ * every bound event to its owner rank (a hash of k0: every tree node below the
+ * root lives on one rank), exchanges them with NCCL send/recv over NVLink, runs
+ * the local pipeline on the owned events and all-reduces the per-level counts;
+ * every rank returns the global result.  Errors: E_INVALID, E_NCCL, E_OOM. */
+ltl4c_status ltl4c_nccl_unique_id(void *out128);
 ltl4c_status ltl4c_state_comm(ltl4c_state *st, const void *nccl_id, int n_ranks, int rank);
 
 /* Run Algorithm 1 on one batch of device-resident events.  Work is enqueued on

@@ -86,6 +86,8 @@ _lib.ltl4c_program_free.argtypes = [_P]
 _lib.ltl4c_program_free.restype = None
 _lib.ltl4c_state_create.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, ctypes.POINTER(_P)]
 _lib.ltl4c_state_comm.argtypes = [_P, ctypes.c_void_p, ctypes.c_int, ctypes.c_int]
+_lib.ltl4c_nccl_unique_id.argtypes = [ctypes.c_void_p]
+_lib.ltl4c_nccl_unique_id.restype = ctypes.c_int
 _lib.ltl4c_verify.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
 _lib.ltl4c_verify_host.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
 _lib.ltl4c_state_reset.argtypes = [_P]
@@ -109,6 +111,13 @@ def _check(st: int):
 
 def version() -> str:
     return _lib.ltl4c_version().decode()
+
+
+def nccl_unique_id() -> bytes:
+    """128-byte ncclUniqueId for ltl4c_state_comm (call on rank 0, broadcast)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.ltl4c_nccl_unique_id(buf))
+    return buf.raw
 
 
 @dataclass
@@ -255,6 +264,11 @@ class State:
         _check(_lib.ltl4c_verify_host(self._h, ctypes.byref(b), _stream_handle(stream), res))
         self.next_index = b.first_index + n
         return self._results(res)
+
+    def comm(self, nccl_id: bytes, n_ranks: int, rank: int):
+        """Join an NCCL communicator (multi-GPU sharded verification)."""
+        buf = ctypes.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
+        _check(_lib.ltl4c_state_comm(self._h, buf, n_ranks, rank))
 
     def reset(self):
         _check(_lib.ltl4c_state_reset(self._h))

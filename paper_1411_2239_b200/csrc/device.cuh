@@ -64,9 +64,12 @@ __host__ __device__ inline uint32_t fmix32(uint32_t h) {
 }
 
 // bucket of an event: top `bits` bits of a hash of its level-0 key
-__host__ __device__ inline uint32_t bucket_of(uint32_t k0, int bits) {
-  return fmix32(k0 ^ 0x9e3779b9u) >> (32 - bits);
+constexpr uint32_t kBucketSalt = 0x9e3779b9u;
+constexpr uint32_t kOwnerSalt = 0x5bd1e995u;  // multi-GPU owner rank (independent of buckets)
+__host__ __device__ inline uint32_t salted_bucket(uint32_t k0, int bits, uint32_t salt) {
+  return bits == 0 ? 0u : fmix32(k0 ^ salt) >> (32 - bits);
 }
+__host__ __device__ inline uint32_t bucket_of(uint32_t k0, int bits) { return salted_bucket(k0, bits, kBucketSalt); }
 
 // Def. 6 node verdict from the child histogram (readings A1-A3, A9; DESIGN.md
 // "Node rule").  Integer only: A compares count*den ~ num*N (num/den reduced,

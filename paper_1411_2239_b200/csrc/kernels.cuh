@@ -27,6 +27,7 @@ struct PartPlan {
   unsigned long long n;                 // events in the batch
   uint32_t n_tiles;                     // ceil(n / kTileEv)
   int K, bits, passes;
+  uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][256] digit totals (bound events)
   uint32_t *counts;                     // [256][n_tiles] tile counts, scanned in place

@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const bool v = ok[r] && (!kFirst || k0[r] != kAbsent);
-    if (v) atomicAdd(&h[(bucket_of(k0[r], pl.bits) >> lo) & dmask], 1u);
+    if (v) atomicAdd(&h[(salted_bucket(k0[r], pl.bits, pl.salt) >> lo) & dmask], 1u);
     myvalid += v;
   }
   if (kFirst) {
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
     for (int k = 0; k < K; ++k) valid &= s.kin[k][e] != kAbsent;
     const uint32_t vm = __ballot_sync(0xffffffffu, valid);
     if (valid) {
-      const uint32_t d = (bucket_of(s.kin[0][e], pl.bits) >> lo) & dmask;
+      const uint32_t d = (salted_bucket(s.kin[0][e], pl.bits, pl.salt) >> lo) & dmask;
       const uint32_t peers = __match_any_sync(vm, d);
       const uint32_t old = s.wcnt[wid][d];
       s.rank[e] = (uint16_t)(old + __popc(peers & lanemask_lt()));

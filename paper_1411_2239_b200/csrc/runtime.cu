@@ -9,6 +9,7 @@
 //                      buckets larger than one shared-memory chunk)  (a3-a5)
 //   return           -> finalize + one <= 1 KB D2H copy              (a6)
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -87,6 +88,59 @@ struct PendingTiming {
   cudaEvent_t a, b;
 };
 
+// NCCL, resolved at run time (the copy torch already loaded, else the system one)
+struct NcclId { char internal[128]; };
+struct Nccl {
+  void *h = nullptr;
+  int (*GetUniqueId)(NcclId *) = nullptr;
+  int (*CommInitRank)(void **, int, NcclId, int) = nullptr;
+  int (*CommDestroy)(void *) = nullptr;
+  int (*Send)(const void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*Recv)(void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*GroupStart)() = nullptr;
+  int (*GroupEnd)() = nullptr;
+  int (*AllReduce)(const void *, void *, size_t, int, int, void *, cudaStream_t) = nullptr;
+  int (*AllGather)(const void *, void *, size_t, int, void *, cudaStream_t) = nullptr;
+  const char *(*ErrStr)(int) = nullptr;
+};
+enum { kNcclUint8 = 1, kNcclUint32 = 3, kNcclUint64 = 5, kNcclSum = 0 };
+
+Nccl *nccl() {
+  static Nccl n;
+  static bool tried = false;
+  if (tried) return n.h ? &n : nullptr;
+  tried = true;
+  const char *names[] = {"libnccl.so.2", "libnccl.so", "/usr/lib/x86_64-linux-gnu/libnccl.so.2"};
+  for (const char *nm : names) {
+    n.h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (n.h) break;
+  }
+  if (!n.h) return nullptr;
+  n.GetUniqueId = (decltype(n.GetUniqueId))dlsym(n.h, "ncclGetUniqueId");
+  n.CommInitRank = (decltype(n.CommInitRank))dlsym(n.h, "ncclCommInitRank");
+  n.CommDestroy = (decltype(n.CommDestroy))dlsym(n.h, "ncclCommDestroy");
+  n.Send = (decltype(n.Send))dlsym(n.h, "ncclSend");
+  n.Recv = (decltype(n.Recv))dlsym(n.h, "ncclRecv");
+  n.GroupStart = (decltype(n.GroupStart))dlsym(n.h, "ncclGroupStart");
+  n.GroupEnd = (decltype(n.GroupEnd))dlsym(n.h, "ncclGroupEnd");
+  n.AllReduce = (decltype(n.AllReduce))dlsym(n.h, "ncclAllReduce");
+  n.AllGather = (decltype(n.AllGather))dlsym(n.h, "ncclAllGather");
+  n.ErrStr = (decltype(n.ErrStr))dlsym(n.h, "ncclGetErrorString");
+  if (!n.GetUniqueId || !n.CommInitRank || !n.Send || !n.Recv || !n.GroupStart || !n.GroupEnd || !n.AllReduce ||
+      !n.AllGather) {
+    dlclose(n.h);
+    n.h = nullptr;
+    return nullptr;
+  }
+  return &n;
+}
+
+#define NC(expr)                                                                                   \
+  do {                                                                                             \
+    int r_ = (expr);                                                                               \
+    if (r_ != 0) return fail(LTL4C_E_NCCL, std::string(#expr) + ": " + (nccl()->ErrStr ? nccl()->ErrStr(r_) : "error")); \
+  } while (0)
+
 }  // namespace ltl4c
 
 using namespace ltl4c;
@@ -113,6 +167,15 @@ struct ltl4c_state {
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
+  // multi-GPU (ltl4c_state_comm)
+  void *comm = nullptr;
+  int n_ranks = 1, rank = 0, owner_bits = 0;
+  bool force_exchange = false;  // LTL4C_FORCE_EXCHANGE: run the exchange path with 1 rank (tests)
+  DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
+  DevBuf<uint32_t> exkey[kMaxLevels];
+  DevBuf<uint8_t> exlet;
+  DevBuf<unsigned long long> dc_cnt;             // [G] own counts, [G][G] all-gathered
+  unsigned long long *hc_cnt = nullptr;          // pinned [G + G*G]
   // heavy path buffers
   DevBuf<uint4> h_part, h_lists;
   DevBuf<uint32_t> h_u32;  // seg_base | leaf_slot_of | leaf_npart | leaf_off | leaf_fill | long_list | scan_tmp | node lists
@@ -355,7 +418,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
 // memsets, SortTrace (count / scan / scatter per pass), mu, the bucket kernels,
 // finalize and the D2H copy of the result record.
 ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *const *keys, const uint8_t *letters,
-                          cudaStream_t s, const Launcher &L) {
+                          cudaStream_t s, const Launcher &L, bool finalize_now = true) {
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
@@ -376,6 +439,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.n_tiles = plan.n_tiles;
     pl.K = K;
     pl.bits = plan.B;
+    pl.salt = kBucketSalt;
     pl.passes = plan.P;
     int lo = 0;
     for (int pass = 0; pass < plan.P; ++pass) {
@@ -408,8 +472,108 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       CU(launch_bucket_global(bp, K, (int)prog->n_formulas, plan.NB, L));
     }
   }
-  CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+  if (finalize_now) {
+    CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+    CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+  }
+  return LTL4C_OK;
+}
+
+// Multi-GPU step 1: route this rank's bound events to their
+// owner rank = top bits of an (independent) hash of k0, with one stable
+// partition pass, then exchange them with grouped NCCL send/recv.  Receive
+// buffers are concatenated in source-rank order; rank r holds the trace range
+// preceding rank r+1's, so every slice keeps its trace order.
+ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_t *letters, uint64_t N,
+                      cudaStream_t s, const Launcher &L, uint64_t *M) {
+  const int K = (int)st->prog->n_levels, G = st->n_ranks;
+  Nccl *nc = nccl();
+  if (!nc) return fail(LTL4C_E_NCCL, "NCCL library not found");
+  const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
+  for (int l = 0; l < K; ++l) CU(st->bufkey[0][l].ensure(N));
+  CU(st->buflet[0].ensure(N));
+  CU(st->counts.ensure((size_t)256 * n_tiles));
+  CU(st->totals.ensure(kMaxPasses * 256 + 16));
+  CU(st->dc_cnt.ensure((size_t)G + (size_t)G * G));
+  CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
+  CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(st->d_sacc.p, 0, sizeof(DevAcc), s));
+  if (N > 0) {
+    PartPlan pl{};
+    for (int l = 0; l < K; ++l) {
+      pl.in_key[l] = keys[l];
+      pl.buf_key[0][l] = st->bufkey[0][l].p;
+      pl.buf_key[1][l] = st->bufkey[1][l].p;
+    }
+    pl.in_let = letters;
+    pl.buf_let[0] = st->buflet[0].p;
+    pl.buf_let[1] = st->buflet[1].p;
+    pl.n = N;
+    pl.n_tiles = n_tiles;
+    pl.K = K;
+    pl.bits = st->owner_bits;
+    pl.passes = 1;
+    pl.salt = kOwnerSalt;
+    pl.lo[0] = 0;
+    pl.width[0] = st->owner_bits;
+    pl.digit_hist = st->totals.p;
+    pl.counts = st->counts.p;
+    pl.nvalid = st->d_nvalid.p;
+    pl.acc = st->d_sacc.p;
+    CU(launch_part_count(pl, 0, L));
+    CU(launch_part_scan(pl, 0, L));
+    CU(launch_part_scatter(pl, 0, L));
+  }
+  // per-owner counts -> all-gathered G x G matrix (row = source rank)
+  uint32_t own[256];
+  CU(cudaMemcpyAsync(own, st->totals.p, sizeof(uint32_t) * G, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  for (int r = 0; r < G; ++r) st->hc_cnt[r] = own[r];
+  CU(cudaMemcpyAsync(st->dc_cnt.p, st->hc_cnt, sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, s));
+  NC(nc->AllGather(st->dc_cnt.p, st->dc_cnt.p + G, (size_t)G, kNcclUint64, st->comm, s));
+  CU(cudaMemcpyAsync(st->hc_cnt + G, st->dc_cnt.p + G, sizeof(unsigned long long) * G * G, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  const unsigned long long *mat = st->hc_cnt + G;
+  std::vector<uint64_t> soff(G), scnt(G), roff(G), rcnt(G);
+  uint64_t so = 0, ro = 0;
+  for (int r = 0; r < G; ++r) {
+    scnt[r] = mat[(size_t)st->rank * G + r];
+    soff[r] = so;
+    so += scnt[r];
+    rcnt[r] = mat[(size_t)r * G + st->rank];
+    roff[r] = ro;
+    ro += rcnt[r];
+  }
+  *M = ro;
+  for (int l = 0; l < K; ++l) CU(st->exkey[l].ensure(ro));
+  CU(st->exlet.ensure(ro));
+  NC(nc->GroupStart());
+  for (int r = 0; r < G; ++r) {
+    for (int l = 0; l < K; ++l) {
+      if (scnt[r]) NC(nc->Send(st->bufkey[0][l].p + soff[r], scnt[r], kNcclUint32, r, st->comm, s));
+      if (rcnt[r]) NC(nc->Recv(st->exkey[l].p + roff[r], rcnt[r], kNcclUint32, r, st->comm, s));
+    }
+    if (scnt[r]) NC(nc->Send(st->buflet[0].p + soff[r], scnt[r], kNcclUint8, r, st->comm, s));
+    if (rcnt[r]) NC(nc->Recv(st->exlet.p + roff[r], rcnt[r], kNcclUint8, r, st->comm, s));
+  }
+  NC(nc->GroupEnd());
+  return LTL4C_OK;
+}
+
+// Multi-GPU step 2: every node below the root lives on exactly one rank, so the
+// per-level histograms (and the root's child histogram hist[1]) are sums over
+// ranks: one all-reduce, then every rank applies the root rule.
+ltl4c_status reduce_and_finalize(ltl4c_state *st, cudaStream_t s, const Launcher &L) {
+  Nccl *nc = nccl();
+  const size_t nsum = (sizeof(((DevAcc *)0)->hist) / sizeof(unsigned long long)) + 2;  // + events_seen, bound
+  unsigned long long seen = st->events_seen;
+  CU(cudaMemcpyAsync(&st->d_acc.p->events_seen, &seen, sizeof seen, cudaMemcpyHostToDevice, s));
+  NC(nc->AllReduce(st->d_acc.p, st->d_gacc.p, nsum, kNcclUint64, kNcclSum, st->comm, s));
+  CU(cudaMemcpyAsync(&st->d_gacc.p->medium_buckets, &st->d_acc.p->medium_buckets,
+                     sizeof(DevAcc) - offsetof(DevAcc, medium_buckets), cudaMemcpyDeviceToDevice, s));
+  CU(launch_finalize(st->d_prog.p, st->d_gacc.p, st->d_out.p, L));
   CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
   return LTL4C_OK;
 }
 
@@ -433,11 +597,40 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     ltl4c_status r = ensure_online_tables(st, N, s, L);
     if (r) return r;
   }
+  const bool comm = st->comm && (st->n_ranks > 1 || st->force_exchange);
+  uint64_t Nloc = N;
+  const uint32_t *lkeys[kMaxLevels] = {keys[0], K > 1 ? keys[1] : nullptr, K > 2 ? keys[2] : nullptr};
+  const uint8_t *llet = letters;
+  if (comm) {
+    ltl4c_status r = exchange(st, keys, letters, N, s, L, &Nloc);
+    if (r) return r;
+    for (int l = 0; l < K; ++l) lkeys[l] = st->exkey[l].p;
+    llet = st->exlet.p;
+  }
   Plan plan;
   {
-    ltl4c_status r = plan_batch(st, N, &plan);
+    ltl4c_status r = plan_batch(st, Nloc, &plan);
     if (r) return r;
   }
+  if (comm) {
+    ltl4c_status r = enqueue_main(st, plan, lkeys, llet, s, L, false);
+    if (r) return r;
+    if (!online && Nloc > 0) {
+      unsigned long long ov = 0;
+      CU(cudaMemcpyAsync(&ov, &st->d_acc.p->oversize_buckets, sizeof ov, cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      if (ov) {
+        st->h_out->oversize_buckets = ov;
+        CU(cudaMemcpyAsync(&st->h_out->oversize_events, &st->d_acc.p->oversize_events, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        ltl4c_status r2 = run_heavy(st, bucket_params(st, plan), K, s, L);
+        if (r2) return r2;
+      }
+    }
+    ltl4c_status r3 = reduce_and_finalize(st, s, L);
+    if (r3) return r3;
+  } else {
   // Offline batches replay a captured CUDA graph of the launch sequence (one
   // graph per input pointers / size); profiling runs the sequence directly so
   // every kernel can be bracketed by events.
@@ -481,6 +674,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
     CU(cudaStreamSynchronize(s));
   }
+  }
   for (int k = 0; k < kKNumKernels; ++k) st->k_launches_saved[k] = st->k_launches[k];
   if (st->h_out->table_overflow)
     return fail(LTL4C_E_OOM, "carried table overflow");
@@ -492,7 +686,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     o.n_levels = r.n_levels;
     for (int l = 0; l <= kMaxLevels; ++l)
       for (int v = 0; v < 6; ++v) o.hist[l][v] = r.hist[l][v];
-    o.events_seen = st->events_seen;
+    o.events_seen = comm ? r.events_seen : st->events_seen;
     o.events_bound = r.events_bound;
   }
   st->verifies++;
@@ -581,6 +775,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   st->device = device;
   st->flags = flags;
   st->graphs = std::getenv("LTL4C_NO_GRAPH") == nullptr;
+  st->force_exchange = std::getenv("LTL4C_FORCE_EXCHANGE") != nullptr;
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;
@@ -644,12 +839,49 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   return LTL4C_OK;
 }
 
+ltl4c_status ltl4c_nccl_unique_id(void *out128) {
+  if (!out128) return fail(LTL4C_E_INVALID, "null argument");
+  Nccl *nc = nccl();
+  if (!nc) return fail(LTL4C_E_NCCL, "NCCL library not found");
+  NcclId id;
+  NC(nc->GetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof id);
+  return LTL4C_OK;
+}
+
 ltl4c_status ltl4c_state_comm(ltl4c_state *st, const void *nccl_id, int n_ranks, int rank) {
-  (void)nccl_id;
-  (void)rank;
   if (!st) return fail(LTL4C_E_INVALID, "null state");
-  if (n_ranks == 1) return LTL4C_OK;
-  return fail(LTL4C_E_INVALID, "multi-GPU sharding is not implemented in this build");
+  if (n_ranks < 1 || rank < 0 || rank >= n_ranks) return fail(LTL4C_E_INVALID, "bad rank / size");
+  if (n_ranks > 256 || (n_ranks & (n_ranks - 1)))
+    return fail(LTL4C_E_INVALID, "the number of ranks must be a power of two <= 256");
+  if (n_ranks > 1 && !nccl_id) return fail(LTL4C_E_INVALID, "null NCCL id");
+  if (st->verifies) return fail(LTL4C_E_INVALID, "join the communicator before the first verify");
+  Nccl *nc = nccl();
+  if (!nc) return fail(LTL4C_E_NCCL, "NCCL library not found");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  NcclId id;
+  if (n_ranks > 1) std::memcpy(&id, nccl_id, sizeof id);
+  else NC(nc->GetUniqueId(&id));
+  void *comm = nullptr;
+  const int rc = nc->CommInitRank(&comm, n_ranks, id, rank);
+  if (rc != 0) {
+    cudaSetDevice(prev);
+    return fail(LTL4C_E_NCCL, std::string("ncclCommInitRank: ") + (nc->ErrStr ? nc->ErrStr(rc) : "error"));
+  }
+  st->comm = comm;
+  st->n_ranks = n_ranks;
+  st->rank = rank;
+  st->owner_bits = 0;
+  while ((1 << st->owner_bits) < n_ranks) ++st->owner_bits;
+  if (st->d_gacc.ensure(1) || st->d_sacc.ensure(1) ||
+      (!st->hc_cnt && cudaMallocHost((void **)&st->hc_cnt, sizeof(unsigned long long) * (256 + 256 * 256)) != cudaSuccess)) {
+    cudaSetDevice(prev);
+    return fail(LTL4C_E_OOM, "allocation failed");
+  }
+  cudaSetDevice(prev);
+  return LTL4C_OK;
 }
 
 ltl4c_status ltl4c_verify(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream, ltl4c_result *out) {
@@ -711,6 +943,13 @@ void ltl4c_state_free(ltl4c_state *st) {
   for (auto e : st->event_pool) cudaEventDestroy(e);
   drop_graph(st);
   if (st->cap_stream) cudaStreamDestroy(st->cap_stream);
+  if (st->comm && nccl() && nccl()->CommDestroy) nccl()->CommDestroy(st->comm);
+  st->d_gacc.release();
+  st->d_sacc.release();
+  for (int l = 0; l < kMaxLevels; ++l) st->exkey[l].release();
+  st->exlet.release();
+  st->dc_cnt.release();
+  if (st->hc_cnt) cudaFreeHost(st->hc_cnt);
   if (st->h_out) cudaFreeHost(st->h_out);
   cudaSetDevice(prev);
   delete st;

@@ -228,3 +228,31 @@ def test_profiling_counts_launches(env):
     s = st.stats()
     assert s["launches"] >= 5 and s["kernels"]["bucket_fast"]["launches"] == 1
     assert s["kernels"]["bucket_fast"]["ms"] > 0
+
+
+def test_exchange_path_single_rank(env):
+    """The multi-GPU path (owner partition, NCCL all-gather of counts, grouped
+    send/recv, local pipeline, all-reduce, root rule) forced with one rank."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import oracle, tracegen, paper_1411_2239_b200 as ltl4c
+dev = torch.device("cuda:0")
+for tr in (tracegen.login_trace(seed=8, n=200_000, users=2000, rid_events=2, p_unauth=0.05),
+           tracegen.zipf_socket_trace(seed=9, n=300_000, support=1 << 12)):
+    st = ltl4c.compile(tr.formula).state(0)
+    st.comm(None, 1, 0)
+    k = [torch.from_numpy(x.view(np.int32)).to(dev) for x in tr.keys]
+    got = st.verify(k, torch.from_numpy(tr.letters).to(dev))[0]
+    want = oracle.run_offline(tr.formula, tr.keys, tr.letters)
+    assert got.verdict == want["verdict"], (got.verdict, want["verdict"])
+    assert np.array_equal(got.hist, want["hist"]), (got.hist, want["hist"])
+    assert got.events_seen == tr.n and got.events_bound == want["events_bound"]
+print("ok")
+'''
+    env_ = dict(__import__("os").environ, LTL4C_FORCE_EXCHANGE="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env_, capture_output=True, text=True, timeout=300,
+                       cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
