@@ -285,8 +285,12 @@ ltl4c_status ensure_online_tables(ltl4c_state *st, uint64_t extra, cudaStream_t 
   const uint64_t have = st->h_out->leaves;
   uint64_t need_nodes = 0;
   for (int l = 1; l < (int)st->prog->n_levels; ++l) need_nodes = std::max<uint64_t>(need_nodes, st->h_out->nodes[l]);
-  const uint64_t want_leaf = 1ull << std::max(16, ceil_log2(2 * (have + extra) + 1));
-  const uint64_t want_node = 1ull << std::max(14, ceil_log2(2 * (need_nodes + extra) + 1));
+  // load <= 1/2 after this batch; grow 4x at a time (rehash = alloc + copy + sync)
+  const uint64_t need_leaf = 2 * (have + extra) + 1, need_node = 2 * (need_nodes + extra) + 1;
+  uint64_t want_leaf = 1ull << std::max(20, ceil_log2(need_leaf));
+  uint64_t want_node = 1ull << std::max(16, ceil_log2(need_node));
+  if (st->tab.d.leaf_cap && st->tab.d.leaf_cap < want_leaf) want_leaf = std::max<uint64_t>(want_leaf, 4 * st->tab.d.leaf_cap);
+  if (st->tab.d.leaf_cap == 0) want_leaf = std::max<uint64_t>(want_leaf, 1ull << ceil_log2(8 * extra + 1));
   Tables &t = st->tab;
   bool fresh = t.d.leaf_cap == 0;
   if (!fresh && t.d.leaf_cap >= want_leaf) {
