@@ -160,9 +160,12 @@ class Program:
             self.quantifiers.append(row)
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.ltl4c_program_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.ltl4c_program_free(self._h)
+        except Exception:
+            pass
+        self._h = None
 
     def state(self, device: int = 0, online: bool = False, capacity: int = 0) -> "State":
         return State(self, device, online, capacity)
@@ -211,9 +214,12 @@ class State:
         self.next_index = 0
 
     def __del__(self):
-        if getattr(self, "_h", None):
-            _lib.ltl4c_state_free(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.ltl4c_state_free(self._h)
+        except Exception:
+            pass
+        self._h = None
 
     def _results(self, res) -> list[Result]:
         n = self.prog.n_levels
