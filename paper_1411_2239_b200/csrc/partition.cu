@@ -168,24 +168,40 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
     for (int w = 0; w < wid; ++w) add += s.wt[w];
     s.pbase[tid] += add;
   }
-  // stable rank: warp w owns events [w * 256, (w + 1) * 256) in rounds of 32
-  for (int r = 0; r < kRounds; ++r) {
-    const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
-    bool valid = true;
+  // stable rank: warp w owns events [w * 256, (w + 1) * 256) in rounds of 32.
+  // Digits and match masks of all rounds first (independent, so they pipeline),
+  // then the per-warp digit counters in round order.
+  {
+    uint32_t dg[kRounds], pm[kRounds];
+    bool vd[kRounds];
 #pragma unroll
-    for (int k = 0; k < K; ++k) valid &= s.kin[k][e] != kAbsent;
-    const uint32_t vm = __ballot_sync(0xffffffffu, valid);
-    if (valid) {
-      const uint32_t d = (salted_bucket(s.kin[0][e], pl.bits, pl.salt) >> lo) & dmask;
-      const uint32_t peers = __match_any_sync(vm, d);
-      const uint32_t old = s.wcnt[wid][d];
-      s.rank[e] = (uint16_t)(old + __popc(peers & lanemask_lt()));
-      s.dig[e] = (uint8_t)d;
-      __syncwarp(vm);
-      if ((peers & lanemask_lt()) == 0) s.wcnt[wid][d] = (uint16_t)(old + __popc(peers));
-      __syncwarp(vm);
-    } else {
-      s.rank[e] = 0xFFFF;
+    for (int r = 0; r < kRounds; ++r) {
+      const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
+      bool valid = true;
+#pragma unroll
+      for (int k = 0; k < K; ++k) valid &= s.kin[k][e] != kAbsent;
+      vd[r] = valid;
+      dg[r] = valid ? (salted_bucket(s.kin[0][e], pl.bits, pl.salt) >> lo) & dmask : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
+      pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
+      uint32_t old = 0;
+      if (vd[r]) {
+        old = s.wcnt[wid][dg[r]];
+        s.rank[e] = (uint16_t)(old + __popc(pm[r] & lanemask_lt()));
+        s.dig[e] = (uint8_t)dg[r];
+      } else {
+        s.rank[e] = 0xFFFF;
+      }
+      __syncwarp();
+      if (vd[r] && (pm[r] & lanemask_lt()) == 0) s.wcnt[wid][dg[r]] = (uint16_t)(old + __popc(pm[r]));
+      __syncwarp();
     }
   }
   __syncthreads();
