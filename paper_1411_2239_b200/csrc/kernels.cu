@@ -35,7 +35,7 @@ namespace ltl4c {
 
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast", "bucket_global",
-                                                "finalize", "rehash", "heavy"};
+                                                "finalize", "rehash", "heavy", "unit_start"};
 
 namespace {
 
@@ -493,17 +493,31 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   const uint32_t node_limit = kNodeSlots / 2;
   uint32_t rk[K][kWarpCap / 32];
   uint8_t rl[kWarpCap / 32];
+  // work items = runs of consecutive buckets (whole level-0 subtrees) of about
+  // kUnitTarget events; an item above kWarpCap is split back into its buckets
+  uint32_t pend_lo = 0, pend_hi = 0, bl = 0, bh = 0;
   auto grab = [&](uint32_t &b, uint32_t &start, uint32_t &cnt) {
     while (true) {
-      b = 0;
-      if (lane == 0) b = atomicAdd(p.bucket_counter, 1u);
-      b = __shfl_sync(0xffffffffu, b, 0);
-      if (b >= p.n_buckets) { cnt = 0; return false; }
-      start = p.bucket_off[b];
-      cnt = p.bucket_off[b + 1] - start;
+      if (pend_lo < pend_hi) {
+        b = pend_lo++;
+        bl = b;
+        bh = b + 1;
+      } else {
+        uint32_t u = 0;
+        if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= p.n_units) { cnt = 0; return false; }
+        bl = p.unit_start[u];
+        bh = p.unit_start[u + 1];
+        b = bl;
+      }
+      if (bh <= bl) continue;
+      start = p.bucket_off[bl];
+      cnt = p.bucket_off[bh] - start;
       if (cnt == 0) continue;
       if (cnt > (uint32_t)kWarpCap) {
-        if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = b;
+        if (bh - bl > 1) { pend_lo = bl; pend_hi = bh; continue; }
+        if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = bl;
         continue;
       }
 #pragma unroll
@@ -522,7 +536,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   uint32_t b, start, cnt;
   bool have = grab(b, start, cnt);
   while (have) {
-    const uint32_t cur_b = b, cur_cnt = cnt;
+    const uint32_t cur_bl = bl, cur_bh = bh, cur_cnt = cnt;
     BucketKeys<K> bk;
 #pragma unroll
     for (int k = 0; k < K; ++k) bk.k[k] = w.key[k];
@@ -625,8 +639,9 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     ovf = __any_sync(0xffffffffu, ovf);
     __syncwarp();
     if (ovf) {
-      // too many distinct prefixes for the warp tables: hand the bucket to the CTA path
-      if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = cur_b;
+      // too many distinct prefixes for the warp tables: hand the buckets to the CTA path
+      for (uint32_t x = cur_bl + lane; x < cur_bh; x += 32)
+        if (p.bucket_off[x + 1] > p.bucket_off[x]) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = x;
     } else {
       // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B)
       for (uint32_t i = lane; i < nleaf; i += 32) {
@@ -676,6 +691,17 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), bb = i % 6;
     if (v && f < nf && l >= 1 && l <= K) atomicAdd(&p.acc->hist[f][l][bb], (unsigned long long)v);
   }
+}
+
+// ----------------------------------------------- work units for bucket_warp
+// unit u = buckets [unit_start[u], unit_start[u+1]): the buckets whose first event
+// lies in [u * kUnitTarget, (u + 1) * kUnitTarget)
+__global__ void unit_start_kernel(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units) {
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  const uint32_t lo = c == 0 ? 0u : off[c - 1] / kUnitTarget + 1u;
+  const uint32_t hi = c == nb ? n_units : off[c] / kUnitTarget;
+  for (uint32_t u = lo; u <= hi && u <= n_units; ++u) ustart[u] = c;
 }
 
 // ----------------------------------------------- global tables
@@ -1281,6 +1307,10 @@ cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t gr
     default: cudaFuncSetAttribute(bucket_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
   }
+}
+
+cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L) {
+  LTL4C_LAUNCH(kKUnitStart, unit_start_kernel<<<(nb + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units));
 }
 
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {

@@ -14,6 +14,7 @@ constexpr int kCap = 2048;           // events per bucket chunk held in shared m
 constexpr int kBucketThreads = 256;
 constexpr int kWarpCap = 512;        // events per warp-processed bucket
 constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
+constexpr int kUnitTarget = 384;     // events per bucket_warp work unit (consecutive buckets)
 constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
@@ -90,7 +91,9 @@ struct BucketParams {
   const unsigned long long *list_len;   // number of entries in list
   uint32_t *oversize_list;              // fast path: buckets larger than kCap
   uint32_t *medium_list;                // warp path: buckets larger than kWarpCap
-  uint32_t *bucket_counter;             // warp path: dynamic bucket scheduler
+  uint32_t *bucket_counter;             // warp path: dynamic unit scheduler
+  const uint32_t *unit_start;           // warp path: [n_units + 1] first bucket of each unit
+  uint32_t n_units;
   const DevProg *prog;
   DevAcc *acc;
   DevTables tab;
@@ -121,6 +124,7 @@ enum KernelId {
   kKFinalize,
   kKRehash,
   kKHeavy,
+  kKUnitStart,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -130,6 +134,7 @@ cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 size_t bucket_warp_smem(int K, int nf, int warps);
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);

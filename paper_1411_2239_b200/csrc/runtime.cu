@@ -162,7 +162,7 @@ struct ltl4c_state {
   DevBuf<unsigned long long> d_nvalid;
   DevBuf<uint32_t> bufkey[2][kMaxLevels];
   DevBuf<uint8_t> buflet[2];
-  DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, sched;
+  DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, sched, unit_start;
   int n_sms = 148, warp_ctas_per_sm = 1, warps_per_cta = 4;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
@@ -397,6 +397,7 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->bucket_off.ensure((size_t)pl->NB + 1));
   CU(st->oversize_list.ensure(pl->NB));
   CU(st->medium_list.ensure(pl->NB));
+  CU(st->unit_start.ensure(N / kUnitTarget + 4));
   return LTL4C_OK;
 }
 
@@ -412,6 +413,8 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.medium_list = st->medium_list.p;
   bp.bucket_counter = st->totals.p + kMaxPasses * 256 + 8;
   bp.warps_per_cta = st->warps_per_cta;
+  bp.unit_start = st->unit_start.p;
+  bp.n_units = (uint32_t)(pl.N / kUnitTarget + 2);
   bp.prog = st->d_prog.p;
   bp.acc = st->d_acc.p;
   bp.tab = st->tab.d;
@@ -466,6 +469,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     if (!online) {
       // warp per bucket; buckets above kWarpCap events go to the CTA kernel,
       // above kCap to the heavy path (after the first result copy)
+      CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
       CU(launch_bucket_warp(bp, K, (int)prog->n_formulas,
                             (uint32_t)std::min<uint64_t>(plan.NB, (uint64_t)st->n_sms * st->warp_ctas_per_sm), L));
       BucketParams mp = bp;
@@ -932,6 +936,7 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->bucket_off.release();
   st->oversize_list.release();
   st->medium_list.release();
+  st->unit_start.release();
   st->sched.release();
   for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
   st->hlet.release();
