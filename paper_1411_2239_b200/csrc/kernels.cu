@@ -643,25 +643,13 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       for (uint32_t x = cur_bl + lane; x < cur_bh; x += 32)
         if (p.bucket_off[x + 1] > p.bucket_off[x]) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = x;
     } else {
-      // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B);
-      // increments are aggregated across the warp (few distinct counters)
-      for (uint32_t i0 = 0; i0 < nleaf; i0 += 32) {
-        const uint32_t i = i0 + lane;
-        const bool act = i < nleaf;
-        const int q = act ? w.lstate[w.llist[i]] : 0;
-        const int ns = (K > 1 && act) ? (int)w.lnode[K - 1][i] : 0;
+      // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B)
+      for (uint32_t i = lane; i < nleaf; i += 32) {
+        const int q = w.lstate[w.llist[i]];
         for (int f = 0; f < nf; ++f) {
           const int v = slab[f * kMaxStates + q];
-          const uint32_t key = act ? (uint32_t)(ns * 8 + v) : 0xFFFFFFFFu;
-          const uint32_t peers = __match_any_sync(0xffffffffu, key);
-          if (act && (peers & lanemask_lt()) == 0) {
-            const uint32_t c = __popc(peers);
-            if (K > 1) atomicAdd(&w.nhist[K - 1][(ns * nf + f) * 3 + (v >> 1)], c << (16 * (v & 1)));
-          }
-          for (int vv = 0; vv < 6; ++vv) {
-            const uint32_t c = __popc(__ballot_sync(0xffffffffu, act && v == vv));
-            if (lane == 0 && c) w.acc[(f * (kMaxLevels + 1) + K) * 6 + vv] += c;
-          }
+          atomicAdd(&w.acc[(f * (kMaxLevels + 1) + K) * 6 + v], 1u);
+          if (K > 1) atomicAdd(&w.nhist[K - 1][(w.lnode[K - 1][i] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
         }
       }
       __syncwarp();
