@@ -56,7 +56,6 @@ struct Smem {
   uint8_t *ov;                // [kMaxFormulas][kCap] item verdicts (old, global path)
   uint8_t *nv;                // [kMaxFormulas][kCap] node verdicts
   uint8_t *nov;               // [kMaxFormulas][kCap] node old verdicts (global path)
-  uint32_t *sortbuf;          // [kCap]
   unsigned long long *lmap;   // [kCap] heavy path: composed map per leaf
   uint8_t *delta;             // [kMaxStates * 256]
   unsigned long long *map;    // [256]
@@ -74,7 +73,7 @@ __host__ __device__ inline size_t smem_bytes(int K, int nf, int mode) {
   const size_t fv = align16((size_t)nf * kCap);
   return (mode == 2 ? align16(8 * kCap) : 0) + align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
          align16(2 * 2 * kCap) + align16(2 * kCap) + 2 * align16(4 * (kCap + 1)) + align16(2 * kCap) +
-         align16(kCap) + (global ? 4 : 2) * fv + align16(4 * kCap) + align16(kMaxStates * 256) +
+         align16(kCap) + (global ? 4 : 2) * fv + align16(kMaxStates * 256) +
          align16(8 * 256) + align16(kMaxFormulas * kMaxStates) +
          align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6) + align16(4 * 64);
 }
@@ -99,7 +98,6 @@ __device__ Smem carve(uint8_t *base, int K, int nf, int mode) {
   s.nv = take((size_t)nf * kCap);
   s.ov = global ? take((size_t)nf * kCap) : nullptr;
   s.nov = global ? take((size_t)nf * kCap) : nullptr;
-  s.sortbuf = (uint32_t *)take(4 * kCap);
   s.delta = take(kMaxStates * 256);
   s.map = (unsigned long long *)take(8 * 256);
   s.lab = take(kMaxFormulas * kMaxStates);
@@ -170,42 +168,22 @@ __device__ void group_by_class(const Smem &s, int n, int C) {
   __syncthreads();
 }
 
-// Make every class segment of s.perm ascending (trace order, reading A15).
+// Make every SHORT class segment (<= 32 events) of s.perm ascending (trace
+// order, reading A15) by insertion sort.  Long classes are never sorted: their
+// transition maps are composed in position order by long_class_map().
 __device__ void order_segments(const Smem &s, int n, int C) {
+  (void)n;
   const int tid = threadIdx.x, nt = blockDim.x;
-  if (tid == 0) s.misc[40] = 0;
-  __syncthreads();
   for (int c = tid; c < C; c += nt) {
     const int a = s.scan[c], b = s.scan[c + 1];
-    if (b - a > 32) { s.misc[40] = 1; continue; }
-    for (int i = a + 1; i < b; ++i) {  // insertion sort
+    if (b - a > 32) continue;
+    for (int i = a + 1; i < b; ++i) {
       const uint16_t x = s.perm[i];
       int j = i - 1;
       while (j >= a && s.perm[j] > x) { s.perm[j + 1] = s.perm[j]; --j; }
       s.perm[j + 1] = x;
     }
   }
-  __syncthreads();
-  if (!s.misc[40]) return;
-  // long segments present: bitonic sort of (class << 16 | item) over the chunk
-  int P = 1;
-  while (P < n) P <<= 1;
-  for (int i = tid; i < P; i += nt) s.sortbuf[i] = i < n ? ((uint32_t)s.cls[i] << 16) | (uint32_t)i : 0xFFFFFFFFu;
-  __syncthreads();
-  for (int k = 2; k <= P; k <<= 1) {
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = tid; i < P; i += nt) {
-        const int ix = i ^ j;
-        if (ix > i) {
-          const uint32_t x = s.sortbuf[i], y = s.sortbuf[ix];
-          const bool up = (i & k) == 0;
-          if ((x > y) == up) { s.sortbuf[i] = y; s.sortbuf[ix] = x; }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int i = tid; i < n; i += nt) s.perm[i] = (uint16_t)(s.sortbuf[i] & 0xFFFF);
   __syncthreads();
 }
 
@@ -217,6 +195,22 @@ __device__ __forceinline__ unsigned long long map_apply(unsigned long long g, un
     r |= ((g >> (4 * fq)) & 15ull) << (4 * q);
   }
   return r;
+}
+
+// One warp: the ordered composition of the transition maps of class c's events
+// (events of the chunk are in trace order; lane l takes positions
+// [l * P, (l + 1) * P), then the 32 lane maps are composed in lane order).
+// Valid in every lane.
+__device__ unsigned long long long_class_map(const Smem &s, int n, int c, int nq, unsigned long long ident) {
+  const int lane = threadIdx.x & 31;
+  const int per = (n + 31) / 32;
+  const int lo = min(n, lane * per), hi = min(n, lo + per);
+  unsigned long long m = ident;
+  for (int i = lo; i < hi; ++i)
+    if (s.cls[i] == c) m = map_apply(s.map[s.let[i]], m, nq);
+  unsigned long long total = ident;
+  for (int l = 0; l < 32; ++l) total = map_apply(__shfl_sync(0xffffffffu, m, l), total, nq);
+  return total;
 }
 
 // Step every leaf class over its (ordered) segment from start state st0[c]
@@ -231,23 +225,13 @@ __device__ void step_leaves(const Smem &s, int C, int nq, int na_letters) {
     for (int i = a; i < b; ++i) q = s.delta[q * na_letters + s.let[s.perm[i]]];
     s.state[c] = (uint8_t)q;
   }
-  // long slices: one warp per leaf, each lane composes the transition maps of a
-  // contiguous piece, then the 32 maps are composed in order (associativity).
+  // long slices: one warp per leaf composes the leaf's transition maps in trace
+  // order (associativity), then applies the result to the start state
   unsigned long long ident = 0;
   for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
   for (int c = wid; c < C; c += nw) {
-    const int a = s.scan[c], b = s.scan[c + 1];
-    const int len = b - a;
-    if (len <= 32) continue;
-    const int per = (len + 31) / 32;
-    const int lo = a + min(len, lane * per), hi = a + min(len, (lane + 1) * per);
-    unsigned long long m = ident;
-    for (int i = lo; i < hi; ++i) m = map_apply(s.map[s.let[s.perm[i]]], m, nq);
-    unsigned long long total = ident;
-    for (int l = 0; l < 32; ++l) {
-      const unsigned long long ml = __shfl_sync(0xffffffffu, m, l);
-      total = map_apply(ml, total, nq);
-    }
+    if (s.scan[c + 1] - s.scan[c] <= 32) continue;
+    const unsigned long long total = long_class_map(s, s.misc[60], c, nq, ident);
     if (lane == 0) s.state[c] = (uint8_t)((total >> (4 * s.state[c])) & 15ull);
     __syncwarp();
   }
@@ -277,6 +261,7 @@ __device__ void flush_acc(const Smem &s, DevAcc *acc, int nf, int nl) {
 
 template <int K>
 __device__ int load_chunk(const Smem &s, const BucketParams &p, uint32_t start, int cnt) {
+  if (threadIdx.x == 0) s.misc[60] = (uint32_t)cnt;
   for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
 #pragma unroll
     for (int i = 0; i < K; ++i) s.key[i][e] = p.key[i][start + e];
@@ -989,14 +974,8 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
       s.lmap[c] = m;
     }
     for (int c = wid; c < C; c += nw) {
-      const int a = s.scan[c], e = s.scan[c + 1], len = e - a;
-      if (len <= 32) continue;
-      const int per = (len + 31) / 32;
-      const int lo = a + min(len, lane * per), hi = a + min(len, (lane + 1) * per);
-      unsigned long long m = ident;
-      for (int x = lo; x < hi; ++x) m = map_apply(s.map[s.let[s.perm[x]]], m, nq);
-      unsigned long long total = ident;
-      for (int l = 0; l < 32; ++l) total = map_apply(__shfl_sync(0xffffffffu, m, l), total, nq);
+      if (s.scan[c + 1] - s.scan[c] <= 32) continue;
+      const unsigned long long total = long_class_map(s, n, c, nq, ident);
       if (lane == 0) s.lmap[c] = total;
       __syncwarp();
     }
