@@ -137,7 +137,8 @@ __device__ int dedup(const Smem &s, int n, int m) {
     const int r = s.item_rep[i];
     uint32_t slot = hash_prefix<K>(s, r, m) & (TS - 1);
     while (true) {
-      const unsigned short old = atomicCAS(&s.htab[slot], (unsigned short)0xFFFF, (unsigned short)i);
+      unsigned short old = ((volatile uint16_t *)s.htab)[slot];
+      if (old == 0xFFFF) old = atomicCAS(&s.htab[slot], (unsigned short)0xFFFF, (unsigned short)i);
       if (old == 0xFFFF) { s.owner[i] = (uint16_t)i; break; }
       if (same_prefix<K>(s, s.item_rep[old], r, m)) { s.owner[i] = old; break; }
       slot = (slot + 1) & (TS - 1);
@@ -161,7 +162,17 @@ __device__ void group_by_class(const Smem &s, int n, int C) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int c = tid; c <= C; c += nt) s.scan[c] = 0;
   __syncthreads();
-  for (int i = tid; i < n; i += nt) s.owner[i] = (uint16_t)atomicAdd(&s.scan[s.cls[i]], 1u);
+  for (int i0 = 0; i0 < n; i0 += nt) {  // warp-aggregated: one atomic per (warp, class)
+    const int i = i0 + tid;
+    const bool act = i < n;
+    const uint32_t c = act ? s.cls[i] : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, c);
+    const int lead = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (act && (tid & 31) == lead) base = atomicAdd(&s.scan[c], (uint32_t)__popc(peers));
+    base = __shfl_sync(0xffffffffu, base, lead);
+    if (act) s.owner[i] = (uint16_t)(base + __popc(peers & lanemask_lt()));
+  }
   __syncthreads();
   block_exclusive_scan(s.scan, C + 1, s.misc);  // scan[C] = n
   for (int i = tid; i < n; i += nt) s.perm[s.scan[s.cls[i]] + s.owner[i]] = (uint16_t)i;
@@ -979,13 +990,19 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
       if (lane == 0) s.lmap[c] = total;
       __syncwarp();
     }
+    if (tid == 0) {  // one allocation of partial slots per segment
+      const unsigned long long pb = atomicAdd(h.n_part, (unsigned long long)C);
+      s.misc[52] = (uint32_t)pb;
+      s.misc[53] = (uint32_t)(pb >> 32);
+    }
     __syncthreads();
+    const unsigned long long pbase = (unsigned long long)s.misc[52] | ((unsigned long long)s.misc[53] << 32);
     for (int c = tid; c < C; c += nt) {
       uint32_t k[kMaxLevels] = {0, 0, 0};
       for (int x = 0; x < K; ++x) k[x] = s.key[x][s.rep[c]];
       int ins;
       const unsigned long long slot = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &h.acc->table_overflow);
-      if (ins < 0) continue;
+      if (ins < 0) { h.part[pbase + c] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u); continue; }
       uint32_t dense;
       if (ins == 1) {
         dense = (uint32_t)atomicAdd(h.n_leaves, 1ull);
@@ -996,9 +1013,8 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
         dense = *(volatile uint32_t *)&T.leaf_aux[slot];
       }
       atomicAdd(&h.leaf_npart[dense], 1u);
-      const unsigned long long pi = atomicAdd(h.n_part, 1ull);
       const unsigned long long m = s.lmap[c];
-      h.part[pi] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
+      h.part[pbase + c] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
     }
   }
 }
@@ -1041,6 +1057,7 @@ __global__ void heavy_group_kernel(HeavyParams h) {
   for (unsigned long long p = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; p < n;
        p += (unsigned long long)gridDim.x * blockDim.x) {
     const uint4 r = h.part[p];
+    if (r.x == 0xFFFFFFFFu) continue;
     const uint32_t pos = h.leaf_off[r.x] + atomicAdd(&h.leaf_fill[r.x], 1u);
     h.lists[pos] = make_uint4(r.y, r.z, r.w, 0u);
   }
@@ -1075,6 +1092,43 @@ __device__ void heavy_leaf_done(const HeavyParams &h, uint32_t dense, int q, int
   }
 }
 
+// warp-cooperative variant (all 32 lanes call it; `act` lanes carry a leaf):
+// increments of the same node-histogram counter are aggregated across the warp
+template <int K>
+__device__ void heavy_leaf_done_warp(const HeavyParams &h, bool act, uint32_t dense, int q, int *acc) {
+  const DevProg *prog = h.prog;
+  const DevTables &T = h.tab;
+  const int nf = prog->nf;
+  const int lane = threadIdx.x & 31;
+  unsigned long long nslot = 0;
+  bool ok = act;
+  if (K > 1 && act) {
+    const uint4 ks = T.leaf_slot[h.leaf_slot_of[dense]];
+    const uint32_t k[3] = {ks.y, ks.z, ks.w};
+    int ins;
+    nslot = table_find_insert(T.node_slot[K - 1], T.node_cap[K - 1], T.epoch, k, K - 1, &ins, &h.acc->table_overflow);
+    if (ins == 1) {
+      for (int x = 0; x < kMaxFormulas * 6; ++x) T.node_hist[K - 1][nslot * kMaxFormulas * 6 + x] = 0;
+      const uint32_t d = (uint32_t)atomicAdd(&h.n_nodes[K - 1], 1ull);
+      T.node_aux[K - 1][nslot] = d;
+      h.node_list[K - 1][d] = (uint32_t)nslot;
+      table_publish(T.node_slot[K - 1], nslot, T.epoch);
+    }
+    ok = ins >= 0;
+  }
+  for (int f = 0; f < nf; ++f) {
+    const int v = act ? prog->lab[f][q] : 0;
+    if (act) atomicAdd(&acc[acc_idx(f, K, v)], 1);
+    if (K > 1) {
+      const unsigned long long key = ok ? (nslot * 8ull + (unsigned long long)v) : ~0ull;
+      const uint32_t peers = __match_any_sync(0xffffffffu, key);
+      if (ok && (peers & lanemask_lt()) == 0)
+        atomicAdd(&T.node_hist[K - 1][nslot * kMaxFormulas * 6 + f * 6 + v], (uint32_t)__popc(peers));
+    }
+  }
+  (void)lane;
+}
+
 // H4: leaves with <= 32 partials (thread per leaf); longer ones are listed
 template <int K>
 __global__ void __launch_bounds__(256) heavy_short_kernel(HeavyParams h) {
@@ -1084,28 +1138,33 @@ __global__ void __launch_bounds__(256) heavy_short_kernel(HeavyParams h) {
   const DevProg *prog = h.prog;
   const int nq = prog->nq;
   const unsigned long long n = *h.n_leaves;
-  for (unsigned long long d = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; d < n;
-       d += (unsigned long long)gridDim.x * blockDim.x) {
-    const uint32_t off = h.leaf_off[d], len = h.leaf_npart[d];
-    if (len > 32) {
-      h.long_list[atomicAdd(&h.ctr[2], 1u)] = (uint32_t)d;
-      continue;
-    }
-    // insertion sort of the leaf's partials by segment item, then ordered composition
-    uint4 *l = h.lists + off;
-    for (uint32_t a = 1; a < len; ++a) {
-      const uint4 x = l[a];
-      int bb = (int)a - 1;
-      while (bb >= 0 && l[bb].x > x.x) { l[bb + 1] = l[bb]; --bb; }
-      l[bb + 1] = x;
-    }
+  const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+  for (unsigned long long d0 = (unsigned long long)blockIdx.x * blockDim.x; d0 < n; d0 += stride) {
+    const unsigned long long d = d0 + threadIdx.x;  // warp-uniform trip count
+    bool act = d < n;
     int q = prog->q0;
-    for (uint32_t a = 0; a < len; ++a) {
-      const unsigned long long m = (unsigned long long)l[a].y | ((unsigned long long)l[a].z << 32);
-      q = (int)((m >> (4 * q)) & 15ull);
+    if (act) {
+      const uint32_t off = h.leaf_off[d], len = h.leaf_npart[d];
+      if (len > 32) {
+        h.long_list[atomicAdd(&h.ctr[2], 1u)] = (uint32_t)d;
+        act = false;
+      } else {
+        // insertion sort of the leaf's partials by segment item, then ordered composition
+        uint4 *l = h.lists + off;
+        for (uint32_t a = 1; a < len; ++a) {
+          const uint4 x = l[a];
+          int bb = (int)a - 1;
+          while (bb >= 0 && l[bb].x > x.x) { l[bb + 1] = l[bb]; --bb; }
+          l[bb + 1] = x;
+        }
+        for (uint32_t a = 0; a < len; ++a) {
+          const unsigned long long m = (unsigned long long)l[a].y | ((unsigned long long)l[a].z << 32);
+          q = (int)((m >> (4 * q)) & 15ull);
+        }
+      }
     }
     (void)nq;
-    heavy_leaf_done<K>(h, (uint32_t)d, q, acc);
+    heavy_leaf_done_warp<K>(h, act, (uint32_t)(act ? d : 0), q, acc);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
