@@ -384,7 +384,9 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   pl->N = N;
   if (N == 0) return LTL4C_OK;
   const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
-  pl->B = std::min(kMaxPasses * kMaxDigitBits, std::max(1, ceil_log2(target)));
+  static const int max_bits = std::getenv("LTL4C_MAX_BITS") ? std::atoi(std::getenv("LTL4C_MAX_BITS"))
+                                                             : kMaxPasses * kMaxDigitBits;
+  pl->B = std::min(std::min(kMaxPasses * kMaxDigitBits, max_bits), std::max(1, ceil_log2(target)));
   pl->P = (pl->B + kMaxDigitBits - 1) / kMaxDigitBits;
   pl->NB = 1u << pl->B;
   pl->n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
