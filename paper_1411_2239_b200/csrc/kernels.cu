@@ -1019,21 +1019,26 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
   }
 }
 
-// H2: exclusive scan of leaf_npart[0 .. n_leaves) -> leaf_off (3 kernels)
+// H2: exclusive scan of leaf_npart[0 .. n_leaves) -> leaf_off (3 kernels; the
+// grids are persistent and loop over the device-side count)
 __global__ void __launch_bounds__(1024) heavy_scan_blocks(HeavyParams h) {
   __shared__ uint32_t buf[1024];
   __shared__ uint32_t wt[32];
   const unsigned long long n = *h.n_leaves;
-  const unsigned long long i = (unsigned long long)blockIdx.x * 1024 + threadIdx.x;
-  buf[threadIdx.x] = i < n ? h.leaf_npart[i] : 0u;
-  __syncthreads();
-  const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
-  if (i < n) h.leaf_off[i] = buf[threadIdx.x];
-  if (threadIdx.x == 0) h.scan_tmp[blockIdx.x] = tot;
+  for (unsigned long long blk = blockIdx.x; blk * 1024 < n; blk += gridDim.x) {
+    const unsigned long long i = blk * 1024 + threadIdx.x;
+    buf[threadIdx.x] = i < n ? h.leaf_npart[i] : 0u;
+    __syncthreads();
+    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
+    if (i < n) h.leaf_off[i] = buf[threadIdx.x];
+    if (threadIdx.x == 0) h.scan_tmp[blk] = tot;
+    __syncthreads();
+  }
 }
-__global__ void __launch_bounds__(1024) heavy_scan_sums(HeavyParams h, uint32_t nblk) {
+__global__ void __launch_bounds__(1024) heavy_scan_sums(HeavyParams h) {
   __shared__ uint32_t buf[1024];
   __shared__ uint32_t wt[32];
+  const uint32_t nblk = (uint32_t)((*h.n_leaves + 1023) / 1024);
   uint32_t carry = 0;
   for (uint32_t o = 0; o < nblk; o += 1024) {
     const uint32_t i = o + threadIdx.x;
@@ -1047,8 +1052,9 @@ __global__ void __launch_bounds__(1024) heavy_scan_sums(HeavyParams h, uint32_t 
 }
 __global__ void __launch_bounds__(1024) heavy_scan_add(HeavyParams h) {
   const unsigned long long n = *h.n_leaves;
-  const unsigned long long i = (unsigned long long)blockIdx.x * 1024 + threadIdx.x;
-  if (i < n) h.leaf_off[i] += h.scan_tmp[blockIdx.x];
+  for (unsigned long long i = (unsigned long long)blockIdx.x * 1024 + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * 1024)
+    h.leaf_off[i] += h.scan_tmp[i / 1024];
 }
 
 // H3: partials grouped by leaf (order inside a group restored in H4)
@@ -1394,10 +1400,9 @@ static cudaError_t heavy_all(const HeavyParams &h, int nf, int n_sms, const Laun
   const size_t sm = smem_bytes(K, nf, 2);
   cudaFuncSetAttribute(heavy_seg_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   heavy_seg_kernel<K><<<2 * n_sms, kBucketThreads, sm, L.stream>>>(h);
-  const uint32_t nblk = (uint32_t)((h.cap_leaves + 1023) / 1024);
-  heavy_scan_blocks<<<nblk ? nblk : 1, 1024, 0, L.stream>>>(h);
-  heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h, nblk ? nblk : 1);
-  heavy_scan_add<<<nblk ? nblk : 1, 1024, 0, L.stream>>>(h);
+  heavy_scan_blocks<<<2 * n_sms, 1024, 0, L.stream>>>(h);
+  heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h);
+  heavy_scan_add<<<2 * n_sms, 1024, 0, L.stream>>>(h);
   heavy_group_kernel<<<4 * n_sms, 256, 0, L.stream>>>(h);
   heavy_short_kernel<K><<<4 * n_sms, 256, 0, L.stream>>>(h);
   heavy_long_kernel<K><<<n_sms, 1024, 0, L.stream>>>(h);
