@@ -92,13 +92,9 @@ __global__ void __launch_bounds__(1024) part_scan_kernel(PartPlan pl, int pass) 
 
 template <int K>
 struct SweepSmem {
-  uint32_t kin[K][kTileEv];
   uint32_t kout[K][kTileEv];
-  uint8_t lin[kTileEv];
   uint8_t lout[kTileEv];
-  uint8_t dig[kTileEv];
   uint8_t dout[kTileEv];
-  uint16_t rank[kTileEv];
   uint16_t wcnt[kPWarps][256];
   uint32_t loc[256];     // tile-local exclusive offset of each digit
   uint32_t tcnt[256];    // tile count of each digit
@@ -108,8 +104,13 @@ struct SweepSmem {
   uint32_t ntile;        // bound events in this tile
 };
 
+// One tile of 4096 events: warp w loads its contiguous 256 events into
+// registers (8 coalesced rounds of 32), ranks them stably by digit in trace
+// order (match masks of all rounds first, then the per-warp digit counters),
+// scatters them into shared memory in digit order and the tile is written out
+// digit run by digit run (coalesced).
 template <int K>
-__global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl, int pass) {
+__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -121,35 +122,25 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
   const unsigned long long n = first ? pl.n : *pl.nvalid;
   const uint32_t dmask = (1u << pl.width[pass]) - 1u;
   const int lo = pl.lo[pass];
+  const uint32_t tile = blockIdx.x;
+  const unsigned long long wbase = (unsigned long long)tile * kTileEv + (unsigned long long)wid * (kTileEv / kPWarps);
+  // loads first (memory-level parallelism)
+  uint32_t rk[kRounds][K];
+  uint8_t rl[kRounds];
+#pragma unroll
+  for (int r = 0; r < kRounds; ++r) {
+    const unsigned long long j = wbase + r * 32 + lane;
+    const bool in = j < n;
+#pragma unroll
+    for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
+    rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
+  }
   if (tid < 256) {
     s.pbase[tid] = pl.digit_hist[pass * 256 + tid];
     s.loc[tid] = 0;
   }
   for (int i = tid; i < kPWarps * 256; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
   __syncthreads();
-  const uint32_t tile = blockIdx.x;
-  const unsigned long long base = (unsigned long long)tile * kTileEv;
-  // stage the tile: every load of this thread first (memory-level parallelism),
-  // then the shared-memory stores
-  {
-    uint32_t rk[kRounds][K];
-    uint8_t rl[kRounds];
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
-      const bool in = j < n;
-#pragma unroll
-      for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
-      rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
-    }
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const int i = r * kPartThreads + tid;
-#pragma unroll
-      for (int k = 0; k < K; ++k) s.kin[k][i] = rk[r][k];
-      s.lin[i] = rl[r];
-    }
-  }
   // pass base offsets: exclusive scan of the digit totals (first 256 threads)
   if (tid < 256) {
     uint32_t x = s.pbase[tid];
@@ -168,41 +159,30 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
     for (int w = 0; w < wid; ++w) add += s.wt[w];
     s.pbase[tid] += add;
   }
-  // stable rank: warp w owns events [w * 256, (w + 1) * 256) in rounds of 32.
-  // Digits and match masks of all rounds first (independent, so they pipeline),
-  // then the per-warp digit counters in round order.
-  {
-    uint32_t dg[kRounds], pm[kRounds];
-    bool vd[kRounds];
+  // stable rank within the warp's range
+  uint32_t dg[kRounds], pm[kRounds], rank[kRounds];
+  bool vd[kRounds];
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
-      bool valid = true;
+  for (int r = 0; r < kRounds; ++r) {
+    bool valid = true;
 #pragma unroll
-      for (int k = 0; k < K; ++k) valid &= s.kin[k][e] != kAbsent;
-      vd[r] = valid;
-      dg[r] = valid ? (salted_bucket(s.kin[0][e], pl.bits, pl.salt) >> lo) & dmask : 0u;
-    }
+    for (int k = 0; k < K; ++k) valid &= rk[r][k] != kAbsent;
+    vd[r] = valid;
+    dg[r] = valid ? (salted_bucket(rk[r][0], pl.bits, pl.salt) >> lo) & dmask : 0u;
+  }
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
-      pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
-    }
+  for (int r = 0; r < kRounds; ++r) {
+    const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
+    pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
+  }
 #pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const int e = wid * (kTileEv / kPWarps) + r * 32 + lane;
-      uint32_t old = 0;
-      if (vd[r]) {
-        old = s.wcnt[wid][dg[r]];
-        s.rank[e] = (uint16_t)(old + __popc(pm[r] & lanemask_lt()));
-        s.dig[e] = (uint8_t)dg[r];
-      } else {
-        s.rank[e] = 0xFFFF;
-      }
-      __syncwarp();
-      if (vd[r] && (pm[r] & lanemask_lt()) == 0) s.wcnt[wid][dg[r]] = (uint16_t)(old + __popc(pm[r]));
-      __syncwarp();
-    }
+  for (int r = 0; r < kRounds; ++r) {
+    uint32_t old = 0;
+    if (vd[r]) old = s.wcnt[wid][dg[r]];
+    rank[r] = old + __popc(pm[r] & lanemask_lt());
+    __syncwarp();
+    if (vd[r] && (pm[r] & lanemask_lt()) == 0) s.wcnt[wid][dg[r]] = (uint16_t)(old + __popc(pm[r]));
+    __syncwarp();
   }
   __syncthreads();
   if (tid < 256) {  // per digit: exclusive over warps, tile total
@@ -235,15 +215,15 @@ __global__ void __launch_bounds__(kPartThreads) part_scatter_kernel(PartPlan pl,
     s.gbase[tid] = s.pbase[tid] + (tid < (1 << pl.width[pass]) ? pl.counts[(size_t)tid * pl.n_tiles + tile] : 0u);
   }
   __syncthreads();
-  // local scatter into digit order
-  for (int e = tid; e < kTileEv; e += kPartThreads) {
-    const uint32_t rk = s.rank[e];
-    if (rk == 0xFFFF) continue;
-    const uint32_t d = s.dig[e];
-    const uint32_t lp = s.loc[d] + s.wcnt[e / (kTileEv / kPWarps)][d] + rk;
+  // local scatter into digit order (from registers)
 #pragma unroll
-    for (int k = 0; k < K; ++k) s.kout[k][lp] = s.kin[k][e];
-    s.lout[lp] = s.lin[e];
+  for (int r = 0; r < kRounds; ++r) {
+    if (!vd[r]) continue;
+    const uint32_t d = dg[r];
+    const uint32_t lp = s.loc[d] + s.wcnt[wid][d] + rank[r];
+#pragma unroll
+    for (int k = 0; k < K; ++k) s.kout[k][lp] = rk[r][k];
+    s.lout[lp] = rl[r];
     s.dout[lp] = (uint8_t)d;
   }
   __syncthreads();
