@@ -256,3 +256,42 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env_, capture_output=True, text=True, timeout=300,
                        cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_C5_formula_batch_offline(env):
+    """K = 3, F = 3 offline: warp, CTA and heavy bucket paths with 3-level tables."""
+    ltl4c, torch, dev = env
+    for n, users, hosts in [(200_000, 3000, 64), (400_000, 500, 4)]:
+        tr = tracegen.c5_trace(seed=2, n=n, users=users, hosts=hosts, span_events=n // 4)
+        prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+        st = prog.state(0)
+        k, l = _dev(torch, dev, tr.keys, tr.letters)
+        got = st.verify(k, l)
+        for f, text in enumerate(tracegen.C5_FORMULAS):
+            p = oracle.Property(text)
+            want = oracle.run_offline(text, tr.keys, _project(tr.letters, prog.atoms, p.atoms))
+            _assert_same(got[f], want, (n, f))
+
+
+def test_giant_single_slice(env):
+    """One value vector with 9M events: > 4096 segments, so the heavy path composes
+    the leaf's partial maps in several shared-memory windows."""
+    ltl4c, torch, dev = env
+    n = 9_000_000
+    rng = np.random.default_rng(77)
+    keys = [np.full(n, 12345, np.uint32)]
+    keys[0][rng.random(n) < 0.001] = 999   # a second, light key in the same stream
+    letters = rng.choice(np.array([0, 1, 2, 3], np.uint8), size=n, p=[0.4, 0.3, 0.2, 0.1])
+    for text in (tracegen.SOCKET, tracegen.FILES):
+        _assert_same(_gpu_offline(env, text, keys, letters)[0], oracle.run_offline(text, keys, letters), text)
+
+
+def test_online_host_buffers(env):
+    ltl4c, torch, dev = env
+    tr = tracegen.login_trace(seed=12, n=120_000, users=800, rid_events=3, p_unauth=0.1)
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    cuts = [0, 30_000, 30_001, 120_000]
+    for lo, hi in zip(cuts[:-1], cuts[1:]):
+        got = st.verify_host([x[lo:hi] for x in tr.keys], tr.letters[lo:hi], first_index=lo)[0]
+        want = oracle.run_offline(tr.formula, [x[:hi] for x in tr.keys], tr.letters[:hi])
+        _assert_same(got, want, hi)
