@@ -464,6 +464,28 @@ __device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const Bucke
   }
 }
 
+// find-or-insert of the full value vector kv of event e in the warp leaf table
+// (keys in registers; the caller appends new slots to the leaf list).
+template <int K>
+__device__ __forceinline__ int leaf_probe(uint32_t *tag, const BucketKeys<K> &bk, const uint32_t (&kv)[K], int e,
+                                          uint32_t hsh, bool *isnew) {
+  constexpr int shift = 32 - __builtin_ctz((unsigned)kLeafSlots);
+  uint32_t h = hsh >> shift;
+  volatile uint32_t *vt = tag;
+  while (true) {
+    uint32_t t = vt[h];
+    if (t == 0) {
+      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
+      if (t == 0) { *isnew = true; return (int)h; }
+    }
+    bool eq = true;
+#pragma unroll
+    for (int i = 0; i < K; ++i) eq &= bk.get(i, (int)t - 1) == kv[i];
+    if (eq) { *isnew = false; return (int)h; }
+    h = (h + 1) & (uint32_t)(kLeafSlots - 1);
+  }
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -554,18 +576,32 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     // otherwise the window is replayed as kIlp sub-rounds of 32 in which lanes
     // sharing a slot are grouped with __match_any_sync and their leader applies
     // the letters in lane order (so every slice u^D is stepped in trace order).
+    uint32_t nleaf = 0;
     for (uint32_t base = 0; base < cur_cnt; base += 32 * kIlp) {
       int slot[kIlp];
+      bool fresh[kIlp];
 #pragma unroll
       for (int r = 0; r < kIlp; ++r) {
         const int e = (int)(base + 32 * r + lane);
         slot[r] = -1;
+        fresh[r] = false;
         if (e < (int)cur_cnt) {
-          const uint32_t hsh = bk.hash(e, K);
-          bool isnew;
-          slot[r] = warp_probe<K>(w.ltag, kLeafSlots, bk, e, K, hsh, &isnew, &w.cnt[0], 0xFFFFFFFFu, w.llist);
-          if (isnew) w.lstate[slot[r]] = (uint8_t)q0;
+          uint32_t kv[K];
+          uint32_t hh = 0;
+#pragma unroll
+          for (int i = 0; i < K; ++i) {
+            kv[i] = bk.get(i, e);
+            hh += kv[i] * (0x9E3779B1u + 0x7F4A7C16u * i);
+          }
+          slot[r] = leaf_probe<K>(w.ltag, bk, kv, e, fmix32(hh), &fresh[r]);
+          if (fresh[r]) w.lstate[slot[r]] = (uint8_t)q0;
         }
+      }
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r) {  // append new leaves (warp-uniform count)
+        const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
+        if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
+        nleaf += __popc(nm);
       }
 #pragma unroll
       for (int r = 0; r < kIlp; ++r)
@@ -602,7 +638,6 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       }
       __syncwarp();
     }
-    const uint32_t nleaf = w.cnt[0];
     // a5 (i): the ancestors of every leaf at depths 1 .. K-1 (P)
     bool ovf = false;
     if (K > 1) {
@@ -640,12 +675,28 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         if (p.bucket_off[x + 1] > p.bucket_off[x]) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = x;
     } else {
       // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B)
+      // per-lane leaf-verdict counts, one byte per value {0, 2, 3, 5} (<= 16 leaves
+      // per lane and unit), reduced over the warp once per unit
+      uint32_t pc[kMaxFormulas] = {0, 0, 0, 0};
       for (uint32_t i = lane; i < nleaf; i += 32) {
         const int q = w.lstate[w.llist[i]];
-        for (int f = 0; f < nf; ++f) {
-          const int v = slab[f * kMaxStates + q];
-          atomicAdd(&w.acc[(f * (kMaxLevels + 1) + K) * 6 + v], 1u);
-          if (K > 1) atomicAdd(&w.nhist[K - 1][(w.lnode[K - 1][i] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+#pragma unroll
+        for (int f = 0; f < kMaxFormulas; ++f) {
+          if (f < nf) {
+            const int v = slab[f * kMaxStates + q];
+            pc[f] += 1u << (8 * ((v + 1) >> 1));
+            if (K > 1) atomicAdd(&w.nhist[K - 1][(w.lnode[K - 1][i] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+          }
+        }
+      }
+#pragma unroll
+      for (int f = 0; f < kMaxFormulas; ++f) {
+        if (f < nf) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t c = __reduce_add_sync(0xffffffffu, (pc[f] >> (8 * j)) & 0xFFu);
+            if (lane == 0) w.acc[(f * (kMaxLevels + 1) + K) * 6 + (j == 0 ? 0 : j + 1 + (j == 3))] += c;
+          }
         }
       }
       __syncwarp();

@@ -8,8 +8,9 @@ namespace ltl4c {
 
 constexpr int kTileEv = 4096;        // events per partition tile
 constexpr int kPartThreads = 512;    // 16 warps x 8 rounds x 32 lanes
-constexpr int kMaxDigitBits = 8;     // <= 256 digits per stable partition pass
-constexpr int kMaxPasses = 3;        // bucket bits <= 24
+constexpr int kMaxDigitBits = 9;     // <= 512 digits per stable partition pass
+constexpr int kMaxDigits = 1 << kMaxDigitBits;
+constexpr int kMaxPasses = 3;        // bucket bits <= 27
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
 constexpr int kWarpCap = 512;        // events per warp-processed bucket
@@ -30,8 +31,9 @@ struct PartPlan {
   int K, bits, passes;
   uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
-  uint32_t *digit_hist;                 // [kMaxPasses][256] digit totals (bound events)
-  uint32_t *counts;                     // [256][n_tiles] tile counts, scanned in place
+  uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
+  uint32_t *counts;                     // [kMaxDigits][n_tiles] tile counts, scanned in place
+  int rank_ballot;                      // stable rank by per-bit ballots instead of match.any
   unsigned long long *nvalid;           // bound events of this batch
   DevAcc *acc;
 };

@@ -30,10 +30,10 @@ constexpr int kRounds = kTileEv / kPartThreads;  // rounds of 32 events per warp
 // applies the epsilon filter; later passes read k0 of the previous pass.
 template <int K, bool kFirst>
 __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, int pass) {
-  __shared__ uint32_t h[256];
+  __shared__ uint32_t h[kMaxDigits];
   __shared__ uint32_t nv;
   const int tid = threadIdx.x, lane = tid & 31;
-  for (int i = tid; i < 256; i += kPartThreads) h[i] = 0;
+  for (int i = tid; i < kMaxDigits; i += kPartThreads) h[i] = 0;
   if (tid == 0) nv = 0;
   __syncthreads();
   const uint32_t *const *in_key = kFirst ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
@@ -87,28 +87,44 @@ __global__ void __launch_bounds__(1024) part_scan_kernel(PartPlan pl, int pass) 
     carry += tot;
     __syncthreads();
   }
-  if (threadIdx.x == 0) pl.digit_hist[pass * 256 + blockIdx.x] = carry;
+  if (threadIdx.x == 0) pl.digit_hist[pass * kMaxDigits + blockIdx.x] = carry;
 }
+
+static_assert(kPartThreads == kMaxDigits, "one partition thread per digit");
 
 template <int K>
 struct SweepSmem {
-  uint32_t kout[K][kTileEv];
+  uint32_t kout[K][kTileEv];        // the tile in digit order
+  uint32_t gout[kTileEv];           // global position of each of them
   uint8_t lout[kTileEv];
-  uint8_t dout[kTileEv];
-  uint16_t wcnt[kPWarps][256];
-  uint32_t loc[256];     // tile-local exclusive offset of each digit
-  uint32_t tcnt[256];    // tile count of each digit
-  uint32_t gbase[256];   // global position of the tile's digit run
-  uint32_t pbase[256];   // exclusive scan of the pass's digit totals
-  uint32_t wt[32];
-  uint32_t ntile;        // bound events in this tile
+  uint16_t wcnt[kPWarps][kMaxDigits];  // per-warp digit counts -> tile-local run starts
+  uint32_t gdelta[kMaxDigits];      // global run start - tile-local run start
+  uint32_t wt[kPWarps];
 };
+
+// exclusive scan over the block, one value per thread (kPartThreads = 16 warps)
+__device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint32_t inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wt[wid] = inc;
+  __syncthreads();
+  uint32_t add = 0;
+#pragma unroll
+  for (int w = 0; w < kPWarps; ++w) add += w < wid ? wt[w] : 0u;
+  __syncthreads();
+  return inc - x + add;
+}
 
 // One tile of 4096 events: warp w loads its contiguous 256 events into
 // registers (8 coalesced rounds of 32), ranks them stably by digit in trace
 // order (match masks of all rounds first, then the per-warp digit counters),
-// scatters them into shared memory in digit order and the tile is written out
-// digit run by digit run (coalesced).
+// scatters them into shared memory in digit order together with their global
+// position, and the tile is written out digit run by digit run (coalesced).
 template <int K>
 __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
@@ -120,7 +136,8 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
   uint32_t *const *out_key = pl.buf_key[pass & 1];
   uint8_t *out_let = pl.buf_let[pass & 1];
   const unsigned long long n = first ? pl.n : *pl.nvalid;
-  const uint32_t dmask = (1u << pl.width[pass]) - 1u;
+  const int width = pl.width[pass];
+  const uint32_t dmask = (1u << width) - 1u;
   const int lo = pl.lo[pass];
   const uint32_t tile = blockIdx.x;
   const unsigned long long wbase = (unsigned long long)tile * kTileEv + (unsigned long long)wid * (kTileEv / kPWarps);
@@ -135,32 +152,21 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
     for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
     rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
   }
-  if (tid < 256) {
-    s.pbase[tid] = pl.digit_hist[pass * 256 + tid];
-    s.loc[tid] = 0;
+  // digits 2t, 2t+1 belong to thread t < kMaxDigits / 2: global run start =
+  // pass base (scan of the digit totals) + the tile's offset within the digit
+  const bool dth = tid < kMaxDigits / 2;
+  const int d0 = 2 * tid, d1 = 2 * tid + 1;
+  uint32_t tot0 = 0, tot1 = 0, til0 = 0, til1 = 0;
+  if (dth) {
+    tot0 = pl.digit_hist[pass * kMaxDigits + d0];
+    tot1 = pl.digit_hist[pass * kMaxDigits + d1];
+    if (d0 <= (int)dmask) til0 = pl.counts[(size_t)d0 * pl.n_tiles + tile];
+    if (d1 <= (int)dmask) til1 = pl.counts[(size_t)d1 * pl.n_tiles + tile];
   }
-  for (int i = tid; i < kPWarps * 256; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
+  for (int i = tid; i < kPWarps * kMaxDigits; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
   __syncthreads();
-  // pass base offsets: exclusive scan of the digit totals (first 256 threads)
-  if (tid < 256) {
-    uint32_t x = s.pbase[tid];
-    uint32_t inc = x;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += y;
-    }
-    if (lane == 31) s.wt[wid] = inc;
-    s.pbase[tid] = inc - x;
-  }
-  __syncthreads();
-  if (tid < 256) {
-    uint32_t add = 0;
-    for (int w = 0; w < wid; ++w) add += s.wt[w];
-    s.pbase[tid] += add;
-  }
   // stable rank within the warp's range
-  uint32_t dg[kRounds], pm[kRounds], rank[kRounds];
+  uint32_t dg[kRounds], pm[kRounds];
   bool vd[kRounds];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
@@ -170,83 +176,113 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
     vd[r] = valid;
     dg[r] = valid ? (salted_bucket(rk[r][0], pl.bits, pl.salt) >> lo) & dmask : 0u;
   }
+  if (pl.rank_ballot) {
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
-    pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
+    for (int r = 0; r < kRounds; ++r) {
+      uint32_t m = __ballot_sync(0xffffffffu, vd[r]);
+#pragma unroll
+      for (int b = 0; b < kMaxDigitBits; ++b) {
+        if (b < width) {
+          const bool bit = (dg[r] >> b) & 1u;
+          const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+          m &= bit ? bal : ~bal;
+        }
+      }
+      pm[r] = vd[r] ? m : 0u;
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRounds; ++r) {
+      const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
+      pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
+    }
   }
+  // dr[r] = digit | rank << 16 (the rank within the tile is < 4096)
+  uint32_t dr[kRounds];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     uint32_t old = 0;
     if (vd[r]) old = s.wcnt[wid][dg[r]];
-    rank[r] = old + __popc(pm[r] & lanemask_lt());
+    dr[r] = dg[r] | (old + __popc(pm[r] & lanemask_lt())) << 16;
     __syncwarp();
     if (vd[r] && (pm[r] & lanemask_lt()) == 0) s.wcnt[wid][dg[r]] = (uint16_t)(old + __popc(pm[r]));
     __syncwarp();
   }
   __syncthreads();
-  if (tid < 256) {  // per digit: exclusive over warps, tile total
-    uint32_t run = 0;
-    for (int w = 0; w < kPWarps; ++w) {
-      const uint32_t c = s.wcnt[w][tid];
-      s.wcnt[w][tid] = (uint16_t)run;
-      run += c;
-    }
-    s.tcnt[tid] = run;
-    s.loc[tid] = run;
-  }
-  __syncthreads();
-  if (tid < 256) {  // tile-local exclusive digit offsets
-    uint32_t x = s.loc[tid], inc = x;
+  // digits 2t, 2t+1: exclusive over warps (two u16 halves per word, < 4096 each),
+  // tile totals, tile-local run starts
+  uint32_t *wc32 = reinterpret_cast<uint32_t *>(&s.wcnt[0][0]);
+  uint32_t wc[kPWarps];
+  uint32_t run = 0;
+  if (dth) {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
-      if (lane >= d) inc += y;
+    for (int w = 0; w < kPWarps; ++w) {
+      wc[w] = run;
+      run += wc32[w * (kMaxDigits / 2) + tid];
     }
-    if (lane == 31) s.wt[wid] = inc;
-    s.loc[tid] = inc - x;
   }
-  __syncthreads();
-  if (tid < 256) {
-    uint32_t add = 0;
-    for (int w = 0; w < wid; ++w) add += s.wt[w];
-    s.loc[tid] += add;
-    if (tid == 255) s.ntile = s.loc[255] + s.tcnt[255];
-    s.gbase[tid] = s.pbase[tid] + (tid < (1 << pl.width[pass]) ? pl.counts[(size_t)tid * pl.n_tiles + tile] : 0u);
+  const uint32_t c0 = run & 0xFFFFu, c1 = run >> 16;
+  const uint32_t loc0 = block_scan_512(c0 + c1, s.wt), loc1 = loc0 + c0;
+  const uint32_t pb0 = block_scan_512(tot0 + tot1, s.wt), pb1 = pb0 + tot0;
+  if (dth) {
+    const uint32_t lp = loc0 | loc1 << 16;
+#pragma unroll
+    for (int w = 0; w < kPWarps; ++w) wc32[w * (kMaxDigits / 2) + tid] = wc[w] + lp;
+    s.gdelta[d0] = pb0 + til0 - loc0;
+    s.gdelta[d1] = pb1 + til1 - loc1;
   }
   __syncthreads();
   // local scatter into digit order (from registers)
+  uint32_t ntile = 0;
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
+    ntile += __popc(__ballot_sync(0xffffffffu, vd[r]));
     if (!vd[r]) continue;
-    const uint32_t d = dg[r];
-    const uint32_t lp = s.loc[d] + s.wcnt[wid][d] + rank[r];
+    const uint32_t d = dr[r] & 0xFFFFu;
+    const uint32_t lp = s.wcnt[wid][d] + (dr[r] >> 16);
 #pragma unroll
     for (int k = 0; k < K; ++k) s.kout[k][lp] = rk[r][k];
     s.lout[lp] = rl[r];
-    s.dout[lp] = (uint8_t)d;
+    s.gout[lp] = lp + s.gdelta[d];
   }
+  if (lane == 0) s.wt[wid] = ntile;
   __syncthreads();
+  uint32_t total = 0;
+#pragma unroll
+  for (int w = 0; w < kPWarps; ++w) total += s.wt[w];
   // coalesced write-out, digit run by digit run
-  const uint32_t nt = s.ntile;
-  for (uint32_t i = tid; i < nt; i += kPartThreads) {
-    const uint32_t d = s.dout[i];
-    const uint32_t g = s.gbase[d] + (i - s.loc[d]);
+  for (uint32_t i = tid; i < total; i += kPartThreads) {
+    const uint32_t g = s.gout[i];
 #pragma unroll
     for (int k = 0; k < K; ++k) out_key[k][g] = s.kout[k][i];
     out_let[g] = s.lout[i];
   }
 }
 
-// off[c] = first position of bucket c in the final order, off[NB] = n.
+// off[c] = first position of bucket c in the final order, off[NB] = n.  Each
+// thread covers 4 consecutive positions (one 16-byte load).
 __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, int bits,
                                      uint32_t *off, uint32_t nb) {
   const unsigned long long n = *nvalid;
-  for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
-       i += (unsigned long long)gridDim.x * blockDim.x) {
-    const long long prev = i == 0 ? -1 : (long long)bucket_of(k0[i - 1], bits);
-    const long long cur = i == n ? (long long)nb : (long long)bucket_of(k0[i], bits);
-    for (long long c = prev + 1; c <= cur; ++c) off[c] = (uint32_t)i;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; 4 * t <= n;
+       t += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i0 = 4 * t;
+    long long b[4];
+    if (i0 + 4 <= n) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(k0 + i0));
+      b[0] = bucket_of(v.x, bits); b[1] = bucket_of(v.y, bits);
+      b[2] = bucket_of(v.z, bits); b[3] = bucket_of(v.w, bits);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = i0 + j < n ? (long long)bucket_of(k0[i0 + j], bits) : (long long)nb;
+    }
+    long long prev = i0 == 0 ? -1 : (long long)bucket_of(k0[i0 - 1], bits);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (i0 + j > n) break;
+      for (long long c = prev + 1; c <= b[j]; ++c) off[c] = (uint32_t)(i0 + j);
+      prev = b[j];
+    }
   }
 }
 
@@ -293,7 +329,8 @@ cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) 
 
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
   const uint32_t *k0 = p.buf_key[(p.passes - 1) & 1][0];
-  const unsigned grid = (unsigned)((p.n + 1 + 255) / 256 > 148 * 16 ? 148 * 16 : (p.n + 1 + 255) / 256);
+  const unsigned long long want = (p.n / 4 + 1 + 255) / 256;
+  const unsigned grid = (unsigned)(want > 148 * 16 ? 148 * 16 : want);
   LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(k0, p.nvalid, p.bits, off, n_buckets));
 }
 

@@ -377,13 +377,19 @@ struct Plan {
   uint32_t NB = 0, n_tiles = 0;
 };
 
+static int rank_ballot() {
+  static const int v = std::getenv("LTL4C_RANK_BALLOT") ? std::atoi(std::getenv("LTL4C_RANK_BALLOT")) : 1;
+  return v;
+}
+
 // Buffer sizes for a batch of N events (all allocation happens here, outside
 // any stream capture).
 ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   const int K = (int)st->prog->n_levels;
   pl->N = N;
   if (N == 0) return LTL4C_OK;
-  const uint64_t target = std::max<uint64_t>(2, (3 * N + kWarpCap - 1) / kWarpCap);
+  static const uint64_t mul = std::getenv("LTL4C_BUCKET_MUL") ? std::atoi(std::getenv("LTL4C_BUCKET_MUL")) : 6;
+  const uint64_t target = std::max<uint64_t>(2, (mul * N + kWarpCap - 1) / kWarpCap);
   static const int max_bits = std::getenv("LTL4C_MAX_BITS") ? std::atoi(std::getenv("LTL4C_MAX_BITS"))
                                                              : kMaxPasses * kMaxDigitBits;
   pl->B = std::min(std::min(kMaxPasses * kMaxDigitBits, max_bits), std::max(1, ceil_log2(target)));
@@ -394,8 +400,8 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
     for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
     CU(st->buflet[i].ensure(N));
   }
-  CU(st->counts.ensure((size_t)256 * pl->n_tiles));
-  CU(st->totals.ensure(kMaxPasses * 256 + 16));
+  CU(st->counts.ensure((size_t)kMaxDigits * pl->n_tiles));
+  CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
   CU(st->bucket_off.ensure((size_t)pl->NB + 1));
   CU(st->oversize_list.ensure(pl->NB));
   CU(st->medium_list.ensure(pl->NB));
@@ -413,7 +419,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.n_buckets = pl.NB;
   bp.oversize_list = st->oversize_list.p;
   bp.medium_list = st->medium_list.p;
-  bp.bucket_counter = st->totals.p + kMaxPasses * 256 + 8;
+  bp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 8;
   bp.warps_per_cta = st->warps_per_cta;
   bp.unit_start = st->unit_start.p;
   bp.n_units = (uint32_t)(pl.N / kUnitTarget + 2);
@@ -434,7 +440,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
   if (!online) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
   CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
   if (plan.N > 0) {
-    CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
+    CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
     PartPlan pl{};
     for (int l = 0; l < K; ++l) {
       pl.in_key[l] = keys[l];
@@ -449,6 +455,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.K = K;
     pl.bits = plan.B;
     pl.salt = kBucketSalt;
+    pl.rank_ballot = rank_ballot();
     pl.passes = plan.P;
     int lo = 0;
     for (int pass = 0; pass < plan.P; ++pass) {
@@ -502,10 +509,10 @@ ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_
   const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
   for (int l = 0; l < K; ++l) CU(st->bufkey[0][l].ensure(N));
   CU(st->buflet[0].ensure(N));
-  CU(st->counts.ensure((size_t)256 * n_tiles));
-  CU(st->totals.ensure(kMaxPasses * 256 + 16));
+  CU(st->counts.ensure((size_t)kMaxDigits * n_tiles));
+  CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
   CU(st->dc_cnt.ensure((size_t)G + (size_t)G * G));
-  CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * 256 + 16), s));
+  CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
   CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
   CU(cudaMemsetAsync(st->d_sacc.p, 0, sizeof(DevAcc), s));
   if (N > 0) {
@@ -524,6 +531,7 @@ ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_
     pl.bits = st->owner_bits;
     pl.passes = 1;
     pl.salt = kOwnerSalt;
+    pl.rank_ballot = rank_ballot();
     pl.lo[0] = 0;
     pl.width[0] = st->owner_bits;
     pl.digit_hist = st->totals.p;
