@@ -38,6 +38,7 @@ struct DevAcc {
   unsigned long long events_seen;
   unsigned long long events_bound;
   unsigned long long medium_buckets;
+  unsigned long long large_buckets;
   unsigned long long oversize_buckets;
   unsigned long long oversize_events;
   unsigned long long table_overflow;

@@ -352,232 +352,202 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
   flush_acc(s, p.acc, nf, nl);
 }
 
-// ----------------------------------------------- warp-per-bucket path (offline)
-// One warp owns one bucket of <= kWarpCap events; no block barriers.  Events are
-// consumed in rounds of 32 in trace order; lanes holding the same value vector
-// in a round are grouped with __match_any_sync and their leader applies the
-// letters in lane order (so every slice u^D is stepped in trace order).  Leaves
-// and tree nodes live in warp-private shared-memory hash tables whose slots
-// store the index of a representative event; keys are compared in place in the
-// (L1-resident) partitioned arrays.  The next bucket is prefetched into L1
-// while the current one is processed.
-constexpr int kIlp = 4;  // events per lane per window
+// ----------------------------------------------- warp-per-unit path (offline)
+// One warp owns one work unit (a run of consecutive buckets = whole level-0
+// subtrees, <= kWarpCap events); no block barriers.  The unit is staged into
+// warp-private shared memory with cp.async (16-byte chunks) while the NEXT
+// unit's byte ranges are prefetched into L2 by one bulk (TMA) prefetch per
+// array.  Events are consumed in windows of 32 x kIlp in trace order:
+//   a3  every lane find-or-inserts the value vectors of its kIlp events in the
+//       warp's leaf table (keys in registers, compared against the staged keys
+//       of the slot's representative event); a new leaf resolves its ancestors
+//       (depths 1 .. K-1, P) right away in the node tables;
+//   a4  a window whose touched slots are all new steps each of them once from
+//       q0; otherwise it is replayed as kIlp sub-rounds of 32 in which lanes
+//       sharing a slot are grouped (__match_any_sync) and their leader applies
+//       the letters in lane order -- every slice u^D is stepped in trace order;
+//   a5  leaf verdicts (Def. 5) -> per-node child histograms (B) with
+//       per-lane run-length aggregation, then Def. 6 level by level.
+constexpr int kIlp = 4;                 // events per lane per window
+constexpr int kWarpHdr = kMaxStates * 256 + kMaxFormulas * kMaxStates + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
 
-struct WarpSmem {
-  uint32_t *key[kMaxLevels];   // [kWarpCap] staged keys of the bucket
-  uint8_t *let;                // [kWarpCap]
-  uint32_t *ltag;              // [kLeafSlots]: 0 empty, else rep event + 1
-  uint8_t *lstate;             // [kLeafSlots]
-  uint16_t *lmark;             // [kLeafSlots]: last event of the round that probed the slot
-  uint16_t *llist;             // [kWarpCap]
-  uint16_t *lnode[kMaxLevels]; // [kWarpCap]: slot of each leaf's depth-l ancestor
-  uint32_t *ntag[kMaxLevels];  // level l in [1, K-1]: [kNodeSlots]
-  uint32_t *nhist[kMaxLevels]; // [kNodeSlots][nf][3]: two u16 counters per word
-  uint16_t *nlist[kMaxLevels]; // [kNodeSlots]
-  uint16_t *npar[kMaxLevels];  // [kNodeSlots]: parent slot (depth l - 1)
-  uint32_t *cnt;               // [4]: leaves, nodes per level
-  uint32_t *acc;               // [kMaxFormulas][kMaxLevels + 1][6]
+template <int K, int NF, int CAP>
+struct alignas(16) WarpTab {
+  static constexpr int NL = K > 1 ? K - 1 : 1;        // inner levels 1 .. K-1 (index l - 1)
+  static constexpr int NS = K > 1 ? kNodeSlots : 1;
+  static constexpr int LS = 2 * CAP;                  // leaf slots (load <= 1/2)
+  uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
+  uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
+  uint16_t ltag[LS];                    // 0 empty, else rep event + 1
+  uint16_t lnode[K > 1 ? LS : 1];       // depth-(K-1) ancestor slot of the leaf
+  uint8_t lstate[LS];
+  uint16_t llist[CAP];                  // leaf slots in creation order
+  uint16_t ntag[NL][NS];
+  uint32_t nhist[NL][NS][NF * 3];       // two u16 counters per word: h[2x] | h[2x+1] << 16
+  uint16_t nlist[NL][NS];
+  uint16_t npar[NL][NS];                // parent slot (depth l - 1), l >= 2
+  uint32_t ncnt[4];                     // claimed node slots per level
 };
 
-__host__ __device__ inline size_t warp_smem_bytes(int K, int nf) {
-  size_t b = align16(4 * kWarpCap) * K + align16(kWarpCap) + align16(4 * kLeafSlots) + align16(kLeafSlots) +
-             align16(2 * kLeafSlots) + align16(2 * kWarpCap);
-  b += (size_t)(K - 1) * (align16(2 * kWarpCap) + align16(4 * kNodeSlots) + align16((size_t)4 * kNodeSlots * nf * 3) +
-                          2 * align16(2 * kNodeSlots));
-  b += align16(16) + align16(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
-  return b;
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
-
-__host__ __device__ inline size_t warp_cta_smem_bytes(int K, int nf, int warps) {
-  return align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) + (size_t)warps * warp_smem_bytes(K, nf);
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
 }
-
-__device__ WarpSmem carve_warp(uint8_t *p, int K, int nf) {
-  WarpSmem w;
-  auto take = [&](size_t bytes) { uint8_t *r = p; p += align16(bytes); return r; };
-  for (int i = 0; i < kMaxLevels; ++i) w.key[i] = i < K ? (uint32_t *)take(4 * kWarpCap) : nullptr;
-  w.let = take(kWarpCap);
-  w.ltag = (uint32_t *)take(4 * kLeafSlots);
-  w.lstate = take(kLeafSlots);
-  w.lmark = (uint16_t *)take(2 * kLeafSlots);
-  w.llist = (uint16_t *)take(2 * kWarpCap);
-  for (int l = 0; l < kMaxLevels; ++l) {
-    w.lnode[l] = nullptr; w.ntag[l] = nullptr; w.nhist[l] = nullptr; w.nlist[l] = nullptr; w.npar[l] = nullptr;
-  }
-  for (int l = 1; l < K; ++l) {
-    w.lnode[l] = (uint16_t *)take(2 * kWarpCap);
-    w.ntag[l] = (uint32_t *)take(4 * kNodeSlots);
-    w.nhist[l] = (uint32_t *)take((size_t)4 * kNodeSlots * nf * 3);
-    w.nlist[l] = (uint16_t *)take(2 * kNodeSlots);
-    w.npar[l] = (uint16_t *)take(2 * kNodeSlots);
-  }
-  w.cnt = (uint32_t *)take(16);
-  w.acc = (uint32_t *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
-  return w;
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte granules)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
+  const uintptr_t a = (uintptr_t)p & ~uintptr_t(15);
+  const uint32_t n = (uint32_t)((((uintptr_t)p + bytes + 15) & ~uintptr_t(15)) - a);
+  if (n) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
 }
 
 template <int K>
-struct BucketKeys {
-  const uint32_t *k[K];
-  __device__ __forceinline__ uint32_t get(int i, int e) const { return k[i][e]; }
-  // hash of the m-key prefix (table index = top bits): one multiply per key
-  // word, then a murmur finaliser
-  __device__ __forceinline__ uint32_t hash(int e, int m) const {
-    uint32_t h = 0;
+__device__ __forceinline__ uint32_t key_hash(const uint32_t (&kv)[K], int m) {
+  uint32_t h = 0;
 #pragma unroll
-    for (int i = 0; i < K; ++i)
-      if (i < m) h += get(i, e) * (0x9E3779B1u + 0x7F4A7C16u * i);
-    return fmix32(h);
-  }
-  __device__ __forceinline__ bool same(int a, int b, int m) const {
-    bool eq = true;
-#pragma unroll
-    for (int i = 0; i < K; ++i)
-      if (i < m) eq &= get(i, a) == get(i, b);
-    return eq;
-  }
-};
+  for (int i = 0; i < K; ++i)
+    if (i < m) h += kv[i] * (0x9E3779B1u + 0x7F4A7C16u * i);
+  return fmix32(h);
+}
 
-// find-or-insert of the m-key prefix of event e; slots store rep event + 1.
-// Returns the slot (-1 when `limit` claims are exceeded); *isnew when this call
-// created it.  Lock-free: a claimed slot's keys are those of its rep event.
+// find-or-insert of the m-key prefix of kv (event e) in a node table; returns the
+// slot, -1 when `limit` claims are exceeded (overflow -> CTA path).
 template <int K>
-__device__ __forceinline__ int warp_probe(uint32_t *tag, int nslots, const BucketKeys<K> &bk, int e, int m,
-                                          uint32_t hsh, bool *isnew, uint32_t *claims, uint32_t limit,
+__device__ __forceinline__ int node_probe(uint16_t *tag, const uint32_t *const (&kb)[K], const uint32_t (&kv)[K],
+                                          int e, int m, bool *isnew, uint32_t *claims, uint32_t limit,
                                           uint16_t *list) {
-  const int shift = 32 - __popc((uint32_t)nslots - 1u);
-  uint32_t h = hsh >> shift;
-  volatile uint32_t *vt = tag;
+  constexpr int shift = 32 - __builtin_ctz((unsigned)kNodeSlots);
+  uint32_t h = key_hash<K>(kv, m) >> shift;
+  volatile uint16_t *vt = tag;
   while (true) {
     uint32_t t = vt[h];
     if (t == 0) {
       if (*(volatile uint32_t *)claims >= limit) return -1;
-      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
+      t = atomicCAS(&tag[h], (unsigned short)0, (unsigned short)(e + 1));
       if (t == 0) {
         *isnew = true;
         list[atomicAdd(claims, 1u)] = (uint16_t)h;
         return (int)h;
       }
     }
-    if (bk.same((int)t - 1, e, m)) { *isnew = false; return (int)h; }
-    h = (h + 1) & (uint32_t)(nslots - 1);
-  }
-}
-
-// find-or-insert of the full value vector kv of event e in the warp leaf table
-// (keys in registers; the caller appends new slots to the leaf list).
-template <int K>
-__device__ __forceinline__ int leaf_probe(uint32_t *tag, const BucketKeys<K> &bk, const uint32_t (&kv)[K], int e,
-                                          uint32_t hsh, bool *isnew) {
-  constexpr int shift = 32 - __builtin_ctz((unsigned)kLeafSlots);
-  uint32_t h = hsh >> shift;
-  volatile uint32_t *vt = tag;
-  while (true) {
-    uint32_t t = vt[h];
-    if (t == 0) {
-      t = atomicCAS(&tag[h], 0u, (uint32_t)e + 1u);
-      if (t == 0) { *isnew = true; return (int)h; }
-    }
     bool eq = true;
 #pragma unroll
-    for (int i = 0; i < K; ++i) eq &= bk.get(i, (int)t - 1) == kv[i];
+    for (int i = 0; i < K; ++i)
+      if (i < m) eq &= kb[i][t - 1] == kv[i];
     if (eq) { *isnew = false; return (int)h; }
-    h = (h + 1) & (uint32_t)(kLeafSlots - 1);
+    h = (h + 1) & (uint32_t)(kNodeSlots - 1);
   }
 }
 
-template <int K>
+template <int K, int NF, int CAP>
 __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
+  using Tab = WarpTab<K, NF, CAP>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
-  const int nf = prog->nf, nq = prog->nq, A = 1 << prog->na;
+  const int nq = prog->nq, A = 1 << prog->na;
   uint8_t *sdelta = smem_raw;
-  uint8_t *slab = smem_raw + align16(kMaxStates * 256);
+  uint8_t *slab = smem_raw + kMaxStates * 256;
+  uint32_t *sacc = reinterpret_cast<uint32_t *>(smem_raw + kMaxStates * 256 + kMaxFormulas * kMaxStates);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tab &w = reinterpret_cast<Tab *>(smem_raw + kWarpHdr)[wid];
   for (int i = threadIdx.x; i < nq * A; i += blockDim.x) sdelta[i] = prog->delta[i / A][i % A];
   for (int i = threadIdx.x; i < kMaxFormulas * kMaxStates; i += blockDim.x)
     slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const WarpSmem w = carve_warp(smem_raw + align16(kMaxStates * 256) + align16(kMaxFormulas * kMaxStates) +
-                                    (size_t)wid * warp_smem_bytes(K, nf), K, nf);
-  for (int i = lane; i < kLeafSlots; i += 32) w.ltag[i] = 0;
-  for (int l = 1; l < K; ++l) {
-    for (int i = lane; i < kNodeSlots; i += 32) w.ntag[l][i] = 0;
-    for (int i = lane; i < kNodeSlots * nf * 3; i += 32) w.nhist[l][i] = 0;
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) sacc[i] = 0;
+  for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+  if (K > 1) {
+    for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
+    for (int i = lane; i < Tab::NL * Tab::NS * NF * 3; i += 32) (&w.nhist[0][0][0])[i] = 0;
   }
-  for (int i = lane; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += 32) w.acc[i] = 0;
-  if (lane < 4) w.cnt[lane] = 0;
+  if (lane < 4) w.ncnt[lane] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
   const uint32_t node_limit = kNodeSlots / 2;
-  uint32_t rk[K][kWarpCap / 32];
-  uint8_t rl[kWarpCap / 32];
-  // work items = runs of consecutive buckets (whole level-0 subtrees) of about
-  // kUnitTarget events; an item above kWarpCap is split back into its buckets
-  uint32_t pend_lo = 0, pend_hi = 0, bl = 0, bh = 0;
-  auto grab = [&](uint32_t &b, uint32_t &start, uint32_t &cnt) {
-    while (true) {
-      if (pend_lo < pend_hi) {
-        b = pend_lo++;
-        bl = b;
-        bh = b + 1;
-      } else {
-        uint32_t u = 0;
-        if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
-        u = __shfl_sync(0xffffffffu, u, 0);
-        if (u >= p.n_units) { cnt = 0; return false; }
-        bl = p.unit_start[u];
-        bh = p.unit_start[u + 1];
-        b = bl;
-      }
-      if (bh <= bl) continue;
-      start = p.bucket_off[bl];
-      cnt = p.bucket_off[bh] - start;
-      if (cnt == 0) continue;
-      if (cnt > (uint32_t)kWarpCap) {
-        if (bh - bl > 1) { pend_lo = bl; pend_hi = bh; continue; }
-        if (lane == 0) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = bl;
-        continue;
-      }
+  uint32_t lc[NF][4];                   // per-lane leaf verdict counts (v = 0, 2, 3, 5)
 #pragma unroll
-      for (int j = 0; j < kWarpCap / 32; ++j) {
-        if ((uint32_t)j * 32 >= cnt) break;
-        const uint32_t i = j * 32 + lane;
-        if (i < cnt) {
+  for (int f = 0; f < NF; ++f)
 #pragma unroll
-          for (int k = 0; k < K; ++k) rk[k][j] = p.key[k][start + i];
-          rl[j] = p.let[start + i];
+    for (int j = 0; j < 4; ++j) lc[f][j] = 0;
+
+  // work: units [unit_start[u], unit_start[u+1]) (or the buckets of p.list)
+  // taken dynamically one ahead; a unit above CAP events is split back into its
+  // buckets; a bucket above CAP (or overflowing the node tables) is spilled to
+  // the next path's list
+  const bool listed = p.list != nullptr;
+  const uint32_t n_items = listed ? (uint32_t)*p.list_len : p.n_units;
+  auto grab = [&]() {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
+    return __shfl_sync(0xffffffffu, u, 0);
+  };
+  auto item = [&](uint32_t u, uint32_t &lo, uint32_t &hi) {
+    if (listed) { lo = p.list[u]; hi = lo + 1; }
+    else { lo = p.unit_start[u]; hi = p.unit_start[u + 1]; }
+  };
+  uint32_t cu = grab();
+  uint32_t cbl = 0, cbh = 0;
+  if (cu < n_items) item(cu, cbl, cbh);
+  uint32_t nu = grab();
+  uint32_t pend_lo = 0, pend_hi = 0;
+  while (true) {
+    uint32_t bl, bh;
+    if (pend_lo < pend_hi) {
+      bl = pend_lo++;
+      bh = bl + 1;
+    } else {
+      if (cu >= n_items) break;
+      bl = cbl;
+      bh = cbh;
+      // advance the pipeline: resolve the next unit, prefetch its bytes into L2
+      cu = nu;
+      if (cu < n_items) {
+        item(cu, cbl, cbh);
+        nu = grab();
+        if (lane <= K && cbh > cbl) {
+          const uint32_t s0 = p.bucket_off[cbl], s1 = p.bucket_off[cbh];
+          if (s1 - s0 <= (uint32_t)CAP) {
+            if (lane < K) bulk_prefetch_l2(p.key[lane] + s0, 4 * (s1 - s0));
+            else bulk_prefetch_l2(p.let + s0, s1 - s0);
+          }
         }
       }
-      return true;
+      if (bh <= bl) continue;
     }
-  };
-  uint32_t b, start, cnt;
-  bool have = grab(b, start, cnt);
-  while (have) {
-    const uint32_t cur_bl = bl, cur_bh = bh, cur_cnt = cnt;
-    BucketKeys<K> bk;
-#pragma unroll
-    for (int k = 0; k < K; ++k) bk.k[k] = w.key[k];
-#pragma unroll
-    for (int j = 0; j < kWarpCap / 32; ++j) {
-      if ((uint32_t)j * 32 >= cur_cnt) break;
-      const uint32_t i = j * 32 + lane;
-      if (i < cur_cnt) {
-#pragma unroll
-        for (int k = 0; k < K; ++k) w.key[k][i] = rk[k][j];
-        w.let[i] = rl[j];
-      }
+    const uint32_t start = p.bucket_off[bl];
+    const uint32_t cnt = p.bucket_off[bh] - start;
+    if (cnt == 0) continue;
+    if (cnt > (uint32_t)CAP) {
+      if (bh - bl > 1) { pend_lo = bl; pend_hi = bh; continue; }
+      if (lane == 0) p.spill_list[atomicAdd(p.spill_len, 1ull)] = bl;
+      continue;
     }
+    // stage the unit (cp.async, 16-byte chunks from 16-byte aligned addresses)
+    const uint32_t koff = start & 3u, loff = start & 15u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t *g = p.key[k] + (start - koff);
+      for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
+    }
+    {
+      const uint8_t *g = p.let + (start - loff);
+      for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
+    }
+    cp_async_wait_all();
     __syncwarp();
-    have = grab(b, start, cnt);  // prefetch of the next bucket overlaps the work below
-    // a3 + a4: windows of 32 x kIlp events in trace order.  Every lane probes
-    // kIlp events (independent, for memory-level parallelism); new slots start at
-    // q0.  If no vector repeats inside the window each slot is stepped once;
-    // otherwise the window is replayed as kIlp sub-rounds of 32 in which lanes
-    // sharing a slot are grouped with __match_any_sync and their leader applies
-    // the letters in lane order (so every slice u^D is stepped in trace order).
+    const uint32_t *kb[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
+    const uint8_t *lb = &w.let[loff];
+    // a3 + a4 over windows of 32 x kIlp events
     uint32_t nleaf = 0;
-    for (uint32_t base = 0; base < cur_cnt; base += 32 * kIlp) {
+    bool ovf = false;
+    int cslot = -1;                     // per-lane cache: deepest ancestor of the last new leaf
+    uint32_t ck[K > 1 ? K - 1 : 1];
+#pragma unroll
+    for (int i = 0; i < (K > 1 ? K - 1 : 1); ++i) ck[i] = 0;
+    for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
       int slot[kIlp];
       bool fresh[kIlp];
 #pragma unroll
@@ -585,16 +555,47 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         const int e = (int)(base + 32 * r + lane);
         slot[r] = -1;
         fresh[r] = false;
-        if (e < (int)cur_cnt) {
+        if (e < (int)cnt) {
           uint32_t kv[K];
-          uint32_t hh = 0;
 #pragma unroll
-          for (int i = 0; i < K; ++i) {
-            kv[i] = bk.get(i, e);
-            hh += kv[i] * (0x9E3779B1u + 0x7F4A7C16u * i);
+          for (int i = 0; i < K; ++i) kv[i] = kb[i][e];
+          constexpr int shift = 32 - __builtin_ctz((unsigned)Tab::LS);
+          uint32_t h = key_hash<K>(kv, K) >> shift;
+          volatile uint16_t *vt = w.ltag;
+          while (true) {
+            uint32_t t = vt[h];
+            if (t == 0) {
+              t = atomicCAS(&w.ltag[h], (unsigned short)0, (unsigned short)(e + 1));
+              if (t == 0) { fresh[r] = true; break; }
+            }
+            bool eq = true;
+#pragma unroll
+            for (int i = 0; i < K; ++i) eq &= kb[i][t - 1] == kv[i];
+            if (eq) break;
+            h = (h + 1) & (uint32_t)(Tab::LS - 1);
           }
-          slot[r] = leaf_probe<K>(w.ltag, bk, kv, e, fmix32(hh), &fresh[r]);
-          if (fresh[r]) w.lstate[slot[r]] = (uint8_t)q0;
+          slot[r] = (int)h;
+          if (K > 1 && fresh[r] && !ovf) {
+            // ancestors of the new leaf (depths 1 .. K-1), cached per lane
+            bool hit = cslot >= 0;
+#pragma unroll
+            for (int i = 0; i < K - 1; ++i) hit &= ck[i] == kv[i];
+            if (!hit) {
+              int parent = -1;
+              for (int l = 1; l < K; ++l) {
+                bool isnew = false;
+                const int ns = node_probe<K>(w.ntag[l - 1], kb, kv, e, l, &isnew, &w.ncnt[l], node_limit,
+                                             w.nlist[l - 1]);
+                if (ns < 0) { ovf = true; break; }
+                if (isnew && l > 1) w.npar[l - 1][ns] = (uint16_t)parent;
+                parent = ns;
+              }
+              cslot = ovf ? -1 : parent;
+#pragma unroll
+              for (int i = 0; i < K - 1; ++i) ck[i] = kv[i];
+            }
+            if (!ovf) w.lnode[h] = (uint16_t)cslot;
+          }
         }
       }
 #pragma unroll
@@ -603,19 +604,19 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
         if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
         nleaf += __popc(nm);
       }
+      bool old = false;
 #pragma unroll
-      for (int r = 0; r < kIlp; ++r)
-        if (slot[r] >= 0) w.lmark[slot[r]] = (uint16_t)(base + 32 * r + lane);
-      __syncwarp();
-      bool dup = false;
-#pragma unroll
-      for (int r = 0; r < kIlp; ++r)
-        if (slot[r] >= 0) dup |= w.lmark[slot[r]] != (uint16_t)(base + 32 * r + lane);
-      if (!__any_sync(0xffffffffu, dup)) {
+      for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
+      if (!__any_sync(0xffffffffu, old)) {
+        // every touched slot is new and touched once: one step from q0
 #pragma unroll
         for (int r = 0; r < kIlp; ++r)
-          if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[w.lstate[slot[r]] * A + w.let[base + 32 * r + lane]];
+          if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[q0 * A + lb[base + 32 * r + lane]];
       } else {
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r)
+          if (fresh[r]) w.lstate[slot[r]] = (uint8_t)q0;
+        __syncwarp();
 #pragma unroll
         for (int r = 0; r < kIlp; ++r) {
           const bool act = slot[r] >= 0;
@@ -628,7 +629,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
               while (m) {
                 const int i = __ffs(m) - 1;
                 m &= m - 1;
-                q = sdelta[q * A + w.let[base + 32 * r + i]];
+                q = sdelta[q * A + lb[base + 32 * r + i]];
               }
               w.lstate[slot[r]] = (uint8_t)q;
             }
@@ -638,105 +639,106 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
       }
       __syncwarp();
     }
-    // a5 (i): the ancestors of every leaf at depths 1 .. K-1 (P)
-    bool ovf = false;
-    if (K > 1) {
-      // per-lane cache of the last ancestor per depth (leaves of a bucket share few)
-      int cslot[kMaxLevels] = {-1, -1, -1};
-      uint32_t ck0 = 0, ck1 = 0;
-      for (uint32_t i = lane; i < nleaf && !ovf; i += 32) {
-        const int rep = (int)w.ltag[w.llist[i]] - 1;
-        const uint32_t k0 = bk.get(0, rep), k1 = K > 2 ? bk.get(1, rep) : 0u;
-        int parent = -1;
-        for (int l = 1; l < K; ++l) {
-          int ns;
-          if (cslot[l] >= 0 && k0 == ck0 && (l < 2 || k1 == ck1)) {
-            ns = cslot[l];
-          } else {
-            bool isnew;
-            ns = warp_probe<K>(w.ntag[l], kNodeSlots, bk, rep, l, bk.hash(rep, l), &isnew, &w.cnt[l], node_limit,
-                               w.nlist[l]);
-            if (ns < 0) { ovf = true; break; }
-            if (isnew && l > 1) w.npar[l][ns] = (uint16_t)parent;
-          }
-          w.lnode[l][i] = (uint16_t)ns;
-          cslot[l] = ns;
-          parent = ns;
-        }
-        ck0 = k0;
-        ck1 = k1;
-      }
-    }
     ovf = __any_sync(0xffffffffu, ovf);
-    __syncwarp();
     if (ovf) {
-      // too many distinct prefixes for the warp tables: hand the buckets to the CTA path
-      for (uint32_t x = cur_bl + lane; x < cur_bh; x += 32)
-        if (p.bucket_off[x + 1] > p.bucket_off[x]) p.medium_list[atomicAdd(&p.acc->medium_buckets, 1ull)] = x;
+      // too many distinct prefixes for the warp tables: hand the buckets on
+      for (uint32_t x = bl + lane; x < bh; x += 32)
+        if (p.bucket_off[x + 1] > p.bucket_off[x]) p.spill_list[atomicAdd(p.spill_len, 1ull)] = x;
     } else {
-      // a5 (ii): leaf verdicts (Def. 5) and depth-(K-1) child histograms (B)
-      // per-lane leaf-verdict counts, one byte per value {0, 2, 3, 5} (<= 16 leaves
-      // per lane and unit), reduced over the warp once per unit
-      uint32_t pc[kMaxFormulas] = {0, 0, 0, 0};
-      for (uint32_t i = lane; i < nleaf; i += 32) {
-        const int q = w.lstate[w.llist[i]];
+      // a5 (i): leaf verdicts; lane takes a contiguous run of the leaf list so
+      // its child counts are aggregated per ancestor before one atomic flush
+      const uint32_t per = (nleaf + 31) >> 5;
+      const uint32_t i0 = min(nleaf, lane * per), i1 = min(nleaf, i0 + per);
+      int cur = -1;
+      uint32_t hv[NF][3];
 #pragma unroll
-        for (int f = 0; f < kMaxFormulas; ++f) {
-          if (f < nf) {
-            const int v = slab[f * kMaxStates + q];
-            pc[f] += 1u << (8 * ((v + 1) >> 1));
-            if (K > 1) atomicAdd(&w.nhist[K - 1][(w.lnode[K - 1][i] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+      for (int f = 0; f < NF; ++f) hv[f][0] = hv[f][1] = hv[f][2] = 0;
+      for (uint32_t i = i0; i < i1; ++i) {
+        const int s = w.llist[i];
+        const int q = w.lstate[s];
+        if (K > 1) {
+          const int nd = w.lnode[s];
+          if (nd != cur) {
+            if (cur >= 0) {
+#pragma unroll
+              for (int f = 0; f < NF; ++f)
+#pragma unroll
+                for (int x = 0; x < 3; ++x)
+                  if (hv[f][x]) { atomicAdd(&w.nhist[K - 2][cur][f * 3 + x], hv[f][x]); hv[f][x] = 0; }
+            }
+            cur = nd;
+          }
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          const int v = slab[f * kMaxStates + q];
+          const int j = (v + 1) >> 1;   // 0 -> 0, 2 -> 1, 3 -> 2, 5 -> 3
+          lc[f][0] += j == 0; lc[f][1] += j == 1; lc[f][2] += j == 2; lc[f][3] += j == 3;
+          if (K > 1) {
+            const uint32_t inc = 1u << (16 * (v & 1));
+            hv[f][0] += (v >> 1) == 0 ? inc : 0u;
+            hv[f][1] += (v >> 1) == 1 ? inc : 0u;
+            hv[f][2] += (v >> 1) == 2 ? inc : 0u;
           }
         }
       }
+      if (K > 1 && cur >= 0) {
 #pragma unroll
-      for (int f = 0; f < kMaxFormulas; ++f) {
-        if (f < nf) {
+        for (int f = 0; f < NF; ++f)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const uint32_t c = __reduce_add_sync(0xffffffffu, (pc[f] >> (8 * j)) & 0xFFu);
-            if (lane == 0) w.acc[(f * (kMaxLevels + 1) + K) * 6 + (j == 0 ? 0 : j + 1 + (j == 3))] += c;
-          }
-        }
+          for (int x = 0; x < 3; ++x)
+            if (hv[f][x]) atomicAdd(&w.nhist[K - 2][cur][f * 3 + x], hv[f][x]);
       }
       __syncwarp();
-      // a5 (iii): node verdicts by Def. 6, depth K-1 .. 1
+      // a5 (ii): node verdicts by Def. 6, depth K-1 .. 1
       for (int l = K - 1; l >= 1; --l) {
-        const uint32_t nn = w.cnt[l];
+        const uint32_t nn = w.ncnt[l];
         for (uint32_t i = lane; i < nn; i += 32) {
-          const int slot = w.nlist[l][i];
-          for (int f = 0; f < nf; ++f) {
-            const uint32_t *hw = &w.nhist[l][(slot * nf + f) * 3];
+          const int s = w.nlist[l - 1][i];
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            const uint32_t *hw = w.nhist[l - 1][s] + f * 3;
             uint32_t h[6];
 #pragma unroll
             for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
             const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
-            atomicAdd(&w.acc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
-            if (l > 1) atomicAdd(&w.nhist[l - 1][(w.npar[l][slot] * nf + f) * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+            atomicAdd(&sacc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
+            if (l > 1) atomicAdd(&w.nhist[l - 2][w.npar[l - 1][s]][f * 3 + (v >> 1)], 1u << (16 * (v & 1)));
           }
         }
         __syncwarp();
       }
     }
-    // clear the tables touched by this bucket (claims beyond the list on overflow
-    // are still listed: every claim appends)
+    // clear the slots this unit claimed
     for (uint32_t i = lane; i < nleaf; i += 32) w.ltag[w.llist[i]] = 0;
-    for (int l = 1; l < K; ++l) {
-      const uint32_t nn = min(w.cnt[l], (uint32_t)kNodeSlots);
-      for (uint32_t i = lane; i < nn; i += 32) {
-        const int slot = w.nlist[l][i];
-        w.ntag[l][slot] = 0;
-        for (int x = 0; x < nf * 3; ++x) w.nhist[l][slot * nf * 3 + x] = 0;
+    if (K > 1) {
+      for (int l = 1; l < K; ++l) {
+        const uint32_t nn = min(w.ncnt[l], (uint32_t)Tab::NS);
+        for (uint32_t i = lane; i < nn; i += 32) {
+          const int s = w.nlist[l - 1][i];
+          w.ntag[l - 1][s] = 0;
+#pragma unroll
+          for (int x = 0; x < NF * 3; ++x) w.nhist[l - 1][s][x] = 0;
+        }
       }
     }
     __syncwarp();
-    if (lane < 4) w.cnt[lane] = 0;
+    if (lane < 4) w.ncnt[lane] = 0;
     __syncwarp();
   }
-  for (int i = lane; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += 32) {
-    const uint32_t v = w.acc[i];
+  // leaf-level counts: warp reduce, CTA accumulate, one global flush per CTA
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t c = __reduce_add_sync(0xffffffffu, lc[f][j]);
+      if (lane == 0 && c) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + (j == 0 ? 0 : j + 1 + (j == 3))], c);
+    }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const uint32_t v = sacc[i];
     const int f = i / ((kMaxLevels + 1) * 6), l = (i / 6) % (kMaxLevels + 1), bb = i % 6;
-    if (v && f < nf && l >= 1 && l <= K) atomicAdd(&p.acc->hist[f][l][bb], (unsigned long long)v);
+    if (v && f < NF && l >= 1 && l <= K) atomicAdd(&p.acc->hist[f][l][bb], (unsigned long long)v);
   }
 }
 
@@ -1413,20 +1415,62 @@ cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart
   LTL4C_LAUNCH(kKUnitStart, unit_start_kernel<<<(n_units + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units));
 }
 
-cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
-  const int warps = p.warps_per_cta;
-  const size_t sm = warp_cta_smem_bytes(K, nf, warps);
-  switch (K) {
-    case 1: cudaFuncSetAttribute(bucket_warp_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<1><<<grid, 32 * warps, sm, L.stream>>>(p));
-    case 2: cudaFuncSetAttribute(bucket_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<2><<<grid, 32 * warps, sm, L.stream>>>(p));
-    default: cudaFuncSetAttribute(bucket_warp_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<3><<<grid, 32 * warps, sm, L.stream>>>(p));
+template <int K, int NF, int CAP>
+static size_t warp_smem(int warps) { return kWarpHdr + (size_t)warps * sizeof(WarpTab<K, NF, CAP>); }
+
+template <int K, int NF>
+static cudaError_t warp_launch(const BucketParams &p, uint32_t grid, const Launcher &L) {
+  if (p.list) {  // medium buckets: the same kernel with 4x the capacity
+    const size_t sm = warp_smem<K, NF, kWarpCapBig>(p.warps_per_cta);
+    cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCapBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<K, NF, kWarpCapBig><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
   }
+  const size_t sm = warp_smem<K, NF, kWarpCap>(p.warps_per_cta);
+  cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<K, NF, kWarpCap><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
 }
 
-size_t bucket_warp_smem(int K, int nf, int warps) { return warp_cta_smem_bytes(K, nf, warps); }
+// (warps per CTA, resident CTAs per SM) with the most resident warps (registers
+// and shared memory both counted by the occupancy calculator)
+template <int K, int NF, int CAP>
+static cudaError_t warp_config_cap(int *warps, int *ctas) {
+  int best = 0;
+  for (int w = 1; w <= 8; ++w) {
+    const size_t sm = warp_smem<K, NF, CAP>(w);
+    if (sm > 227 * 1024) break;
+    cudaError_t e = cudaFuncSetAttribute(bucket_warp_kernel<K, NF, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, bucket_warp_kernel<K, NF, CAP>, 32 * w, sm);
+    if (e != cudaSuccess) return e;
+    if (n * w >= best && n > 0) { best = n * w; *warps = w; *ctas = n; }
+  }
+  return best ? cudaSuccess : cudaErrorInvalidConfiguration;
+}
+
+template <int K, int NF>
+static cudaError_t warp_config(int *cfg) {
+  cudaError_t e = warp_config_cap<K, NF, kWarpCap>(&cfg[0], &cfg[1]);
+  return e != cudaSuccess ? e : warp_config_cap<K, NF, kWarpCapBig>(&cfg[2], &cfg[3]);
+}
+
+#define LTL4C_KNF(K, NF, FN, ...)                                        \
+  switch ((K) * 10 + (NF)) {                                               \
+    case 11: return FN<1, 1>(__VA_ARGS__); case 12: return FN<1, 2>(__VA_ARGS__); \
+    case 13: return FN<1, 3>(__VA_ARGS__); case 14: return FN<1, 4>(__VA_ARGS__); \
+    case 21: return FN<2, 1>(__VA_ARGS__); case 22: return FN<2, 2>(__VA_ARGS__); \
+    case 23: return FN<2, 3>(__VA_ARGS__); case 24: return FN<2, 4>(__VA_ARGS__); \
+    case 31: return FN<3, 1>(__VA_ARGS__); case 32: return FN<3, 2>(__VA_ARGS__); \
+    case 33: return FN<3, 3>(__VA_ARGS__); default: return FN<3, 4>(__VA_ARGS__); \
+  }
+
+cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
+  LTL4C_KNF(K, nf, warp_launch, p, grid, L);
+}
+
+cudaError_t bucket_warp_config(int K, int nf, int *cfg) {
+  LTL4C_KNF(K, nf, warp_config, cfg);
+}
 
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, 1);

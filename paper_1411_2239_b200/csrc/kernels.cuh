@@ -13,9 +13,9 @@ constexpr int kMaxDigits = 1 << kMaxDigitBits;
 constexpr int kMaxPasses = 3;        // bucket bits <= 27
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
-constexpr int kWarpCap = 512;        // events per warp-processed bucket
-constexpr int kLeafSlots = 1024;     // warp leaf table (load <= 1/2)
-constexpr int kUnitTarget = 384;     // events per bucket_warp work unit (consecutive buckets)
+constexpr int kWarpCap = 256;        // events per warp-processed unit
+constexpr int kWarpCapBig = 1024;    // events per warp-processed medium bucket
+constexpr int kUnitTarget = 192;     // events per bucket_warp work unit (consecutive buckets)
 constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
@@ -93,6 +93,8 @@ struct BucketParams {
   const unsigned long long *list_len;   // number of entries in list
   uint32_t *oversize_list;              // fast path: buckets larger than kCap
   uint32_t *medium_list;                // warp path: buckets larger than kWarpCap
+  uint32_t *spill_list;                 // warp paths: buckets that do not fit go here
+  unsigned long long *spill_len;
   uint32_t *bucket_counter;             // warp path: dynamic unit scheduler
   const uint32_t *unit_start;           // warp path: [n_units + 1] first bucket of each unit
   uint32_t n_units;
@@ -138,7 +140,9 @@ cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_bu
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
-size_t bucket_warp_smem(int K, int nf, int warps);
+// {warps per CTA, CTAs per SM} of the unit kernel (cfg[0..1]) and of the
+// medium-bucket kernel (cfg[2..3])
+cudaError_t bucket_warp_config(int K, int nf, int *cfg);
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L);
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,

@@ -162,8 +162,9 @@ struct ltl4c_state {
   DevBuf<unsigned long long> d_nvalid;
   DevBuf<uint32_t> bufkey[2][kMaxLevels];
   DevBuf<uint8_t> buflet[2];
-  DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, sched, unit_start;
-  int n_sms = 148, warp_ctas_per_sm = 1, warps_per_cta = 4;
+  DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, large_list, sched, unit_start;
+  int n_sms = 148;
+  int warp_cfg[4] = {4, 1, 1, 1};  // {warps/CTA, CTAs/SM} of the unit and the medium warp kernels
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
@@ -397,14 +398,15 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   pl->NB = 1u << pl->B;
   pl->n_tiles = (uint32_t)((N + kTileEv - 1) / kTileEv);
   for (int i = 0; i < 2; ++i) {
-    for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N));
-    CU(st->buflet[i].ensure(N));
+    for (int l = 0; l < K; ++l) CU(st->bufkey[i][l].ensure(N + 16));
+    CU(st->buflet[i].ensure(N + 16));
   }
   CU(st->counts.ensure((size_t)kMaxDigits * pl->n_tiles));
   CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
   CU(st->bucket_off.ensure((size_t)pl->NB + 1));
   CU(st->oversize_list.ensure(pl->NB));
   CU(st->medium_list.ensure(pl->NB));
+  CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
   return LTL4C_OK;
 }
@@ -420,7 +422,9 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.oversize_list = st->oversize_list.p;
   bp.medium_list = st->medium_list.p;
   bp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 8;
-  bp.warps_per_cta = st->warps_per_cta;
+  bp.warps_per_cta = st->warp_cfg[0];
+  bp.spill_list = st->medium_list.p;
+  bp.spill_len = &st->d_acc.p->medium_buckets;
   bp.unit_start = st->unit_start.p;
   bp.n_units = (uint32_t)(pl.N / kUnitTarget + 2);
   bp.prog = st->d_prog.p;
@@ -476,15 +480,23 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
-      // warp per bucket; buckets above kWarpCap events go to the CTA kernel,
-      // above kCap to the heavy path (after the first result copy)
+      // a warp per unit (<= kWarpCap events); buckets above that go to the same
+      // kernel with kWarpCapBig, above that to the CTA kernel, and above kCap to
+      // the heavy path (after the first result copy)
       CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
-      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas,
-                            (uint32_t)std::min<uint64_t>(plan.NB, (uint64_t)st->n_sms * st->warp_ctas_per_sm), L));
+      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, (uint32_t)(st->n_sms * st->warp_cfg[1]), L));
       BucketParams mp = bp;
       mp.list = st->medium_list.p;
       mp.list_len = &st->d_acc.p->medium_buckets;
-      CU(launch_bucket_fast(mp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
+      mp.spill_list = st->large_list.p;
+      mp.spill_len = &st->d_acc.p->large_buckets;
+      mp.bucket_counter = bp.bucket_counter + 1;
+      mp.warps_per_cta = st->warp_cfg[2];
+      CU(launch_bucket_warp(mp, K, (int)prog->n_formulas, (uint32_t)(st->n_sms * st->warp_cfg[3]), L));
+      BucketParams fp = bp;
+      fp.list = st->large_list.p;
+      fp.list_len = &st->d_acc.p->large_buckets;
+      CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
     } else {
       CU(launch_bucket_global(bp, K, (int)prog->n_formulas, plan.NB, L));
     }
@@ -507,8 +519,8 @@ ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_
   Nccl *nc = nccl();
   if (!nc) return fail(LTL4C_E_NCCL, "NCCL library not found");
   const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
-  for (int l = 0; l < K; ++l) CU(st->bufkey[0][l].ensure(N));
-  CU(st->buflet[0].ensure(N));
+  for (int l = 0; l < K; ++l) CU(st->bufkey[0][l].ensure(N + 16));
+  CU(st->buflet[0].ensure(N + 16));
   CU(st->counts.ensure((size_t)kMaxDigits * n_tiles));
   CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
   CU(st->dc_cnt.ensure((size_t)G + (size_t)G * G));
@@ -835,22 +847,16 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
     const int K = (int)prog->n_levels;
     for (int i = 0; i < 2; ++i) {
       for (int l = 0; l < K; ++l)
-        if (st->bufkey[i][l].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
-      if (st->buflet[i].ensure(capacity_hint)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
+        if (st->bufkey[i][l].ensure(capacity_hint + 16)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
+      if (st->buflet[i].ensure(capacity_hint + 16)) return cleanup(fail(LTL4C_E_OOM, "buffer allocation failed"));
     }
   }
   st->n_sms = dp.multiProcessorCount;
   {
-    // warp-per-bucket kernel: the (warps per CTA, CTAs per SM) pair that keeps
-    // the most warps resident for this program's (K, F) shared-memory plan
-    const int K = (int)prog->n_levels, F = (int)prog->n_formulas;
-    int best = 0;
-    for (int w = 1; w <= 8; ++w) {
-      const size_t sm = bucket_warp_smem(K, F, w);
-      if (sm > 200 * 1024) break;
-      const int ctas = (int)std::min<size_t>(16, (size_t)dp.sharedMemPerMultiprocessor / (sm + 1024));
-      if (ctas * w > best) { best = ctas * w; st->warps_per_cta = w; st->warp_ctas_per_sm = ctas; }
-    }
+    // warp-per-unit kernel: the (warps per CTA, CTAs per SM) pair that keeps the
+    // most warps resident for this program's (K, F) shared-memory plan
+    cudaError_t e = bucket_warp_config((int)prog->n_levels, (int)prog->n_formulas, st->warp_cfg);
+    if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
   }
   cudaSetDevice(prev);
   *out = st;
@@ -946,6 +952,7 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->bucket_off.release();
   st->oversize_list.release();
   st->medium_list.release();
+  st->large_list.release();
   st->unit_start.release();
   st->sched.release();
   for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
