@@ -354,10 +354,11 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 
 // ----------------------------------------------- warp-per-unit path (offline)
 // One warp owns one work unit (a run of consecutive buckets = whole level-0
-// subtrees, <= kWarpCap events); no block barriers.  The unit is staged into
-// warp-private shared memory with cp.async (16-byte chunks) while the NEXT
-// unit's byte ranges are prefetched into L2 by one bulk (TMA) prefetch per
-// array.  Events are consumed in windows of 32 x kIlp in trace order:
+// subtrees, <= CAP events); no block barriers.  The unit is staged into
+// warp-private shared memory with cp.async (16-byte chunks); the NEXT unit is
+// resolved one step ahead and its byte ranges are prefetched into L2 with one
+// bulk (TMA) prefetch per array.  Events are consumed in windows of 32 x kIlp
+// in trace order:
 //   a3  every lane find-or-inserts the value vectors of its kIlp events in the
 //       warp's leaf table (keys in registers, compared against the staged keys
 //       of the slot's representative event); a new leaf resolves its ancestors
@@ -368,6 +369,8 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 //       the letters in lane order -- every slice u^D is stepped in trace order;
 //   a5  leaf verdicts (Def. 5) -> per-node child histograms (B) with
 //       per-lane run-length aggregation, then Def. 6 level by level.
+// Table slots carry a per-unit epoch (tag = epoch << 16 | rep event + 1), so no
+// table is cleared between units.
 constexpr int kIlp = 4;                 // events per lane per window
 constexpr int kWarpHdr = kMaxStates * 256 + kMaxFormulas * kMaxStates + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
 
@@ -378,11 +381,11 @@ struct alignas(16) WarpTab {
   static constexpr int LS = 2 * CAP;                  // leaf slots (load <= 1/2)
   uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
   uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
-  uint16_t ltag[LS];                    // 0 empty, else rep event + 1
+  uint32_t ltag[LS];                    // epoch << 16 | rep event + 1 (other epochs = empty)
   uint16_t lnode[K > 1 ? LS : 1];       // depth-(K-1) ancestor slot of the leaf
   uint8_t lstate[LS];
   uint16_t llist[CAP];                  // leaf slots in creation order
-  uint16_t ntag[NL][NS];
+  uint32_t ntag[NL][NS];                // as ltag
   uint32_t nhist[NL][NS][NF * 3];       // two u16 counters per word: h[2x] | h[2x+1] << 16
   uint16_t nlist[NL][NS];
   uint16_t npar[NL][NS];                // parent slot (depth l - 1), l >= 2
@@ -412,30 +415,35 @@ __device__ __forceinline__ uint32_t key_hash(const uint32_t (&kv)[K], int m) {
   return fmix32(h);
 }
 
-// find-or-insert of the m-key prefix of kv (event e) in a node table; returns the
-// slot, -1 when `limit` claims are exceeded (overflow -> CTA path).
-template <int K>
-__device__ __forceinline__ int node_probe(uint16_t *tag, const uint32_t *const (&kb)[K], const uint32_t (&kv)[K],
-                                          int e, int m, bool *isnew, uint32_t *claims, uint32_t limit,
-                                          uint16_t *list) {
+// find-or-insert of the m-key prefix of kv (event e) in a node table of the
+// current epoch; returns the slot, -1 when `limit` claims are exceeded
+// (overflow -> the next path).  A new slot's histogram words are zeroed.
+template <int K, int NF>
+__device__ __forceinline__ int node_probe(uint32_t *tag, uint32_t (*hist)[NF * 3], const uint32_t *const (&kb)[K],
+                                          const uint32_t (&kv)[K], int e, int m, uint32_t ep, bool *isnew,
+                                          uint32_t *claims, uint32_t limit, uint16_t *list) {
   constexpr int shift = 32 - __builtin_ctz((unsigned)kNodeSlots);
   uint32_t h = key_hash<K>(kv, m) >> shift;
-  volatile uint16_t *vt = tag;
+  volatile uint32_t *vt = tag;
   while (true) {
     uint32_t t = vt[h];
-    if (t == 0) {
+    if ((t >> 16) != ep) {
       if (*(volatile uint32_t *)claims >= limit) return -1;
-      t = atomicCAS(&tag[h], (unsigned short)0, (unsigned short)(e + 1));
-      if (t == 0) {
+      const uint32_t o = atomicCAS(&tag[h], t, ep << 16 | (uint32_t)(e + 1));
+      if (o == t) {
         *isnew = true;
+#pragma unroll
+        for (int x = 0; x < NF * 3; ++x) hist[h][x] = 0;
         list[atomicAdd(claims, 1u)] = (uint16_t)h;
         return (int)h;
       }
+      t = o;
     }
+    const int rep = (int)(t & 0xFFFFu) - 1;
     bool eq = true;
 #pragma unroll
     for (int i = 0; i < K; ++i)
-      if (i < m) eq &= kb[i][t - 1] == kv[i];
+      if (i < m) eq &= kb[i][rep] == kv[i];
     if (eq) { *isnew = false; return (int)h; }
     h = (h + 1) & (uint32_t)(kNodeSlots - 1);
   }
@@ -457,283 +465,284 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) sacc[i] = 0;
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
-  if (K > 1) {
-    for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
-    for (int i = lane; i < Tab::NL * Tab::NS * NF * 3; i += 32) (&w.nhist[0][0][0])[i] = 0;
-  }
-  if (lane < 4) w.ncnt[lane] = 0;
+  for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
   const uint32_t node_limit = kNodeSlots / 2;
-  uint32_t lc[NF][4];                   // per-lane leaf verdict counts (v = 0, 2, 3, 5)
+  // per-lane leaf verdict counts, 16-bit fields j = 0..3 for v = 0, 2, 3, 5
+  unsigned long long lcp[NF];
 #pragma unroll
-  for (int f = 0; f < NF; ++f)
+  for (int f = 0; f < NF; ++f) lcp[f] = 0;
+  uint32_t since = 0;                   // leaves counted into lcp since its last flush (warp-uniform)
+  auto flush_lcp = [&]() {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) lc[f][j] = 0;
+    for (int f = 0; f < NF; ++f) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t c = __reduce_add_sync(0xffffffffu, (uint32_t)(lcp[f] >> (16 * j)) & 0xFFFFu);
+        if (lane == 0 && c) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + (j == 0 ? 0 : j + 1 + (j == 3))], c);
+      }
+      lcp[f] = 0;
+    }
+  };
 
-  // work: units [unit_start[u], unit_start[u+1]) (or the buckets of p.list)
-  // taken dynamically one ahead; a unit above CAP events is split back into its
-  // buckets; a bucket above CAP (or overflowing the node tables) is spilled to
-  // the next path's list
+  // work: units [unit_start[u], unit_start[u+1]) (or the buckets of p.list),
+  // taken dynamically; unit u+1 is resolved and prefetched while u is processed.
+  // A unit above CAP events is split back into its buckets; a bucket above CAP
+  // (or overflowing the node tables) is spilled to the next path's list.
   const bool listed = p.list != nullptr;
   const uint32_t n_items = listed ? (uint32_t)*p.list_len : p.n_units;
-  auto grab = [&]() {
-    uint32_t u = 0;
-    if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
-    return __shfl_sync(0xffffffffu, u, 0);
-  };
   auto item = [&](uint32_t u, uint32_t &lo, uint32_t &hi) {
     if (listed) { lo = p.list[u]; hi = lo + 1; }
     else { lo = p.unit_start[u]; hi = p.unit_start[u + 1]; }
   };
-  uint32_t cu = grab();
-  uint32_t cbl = 0, cbh = 0;
-  if (cu < n_items) item(cu, cbl, cbh);
-  uint32_t nu = grab();
-  uint32_t pend_lo = 0, pend_hi = 0;
-  while (true) {
-    uint32_t bl, bh;
-    if (pend_lo < pend_hi) {
-      bl = pend_lo++;
-      bh = bl + 1;
-    } else {
-      if (cu >= n_items) break;
-      bl = cbl;
-      bh = cbh;
-      // advance the pipeline: resolve the next unit, prefetch its bytes into L2
-      cu = nu;
-      if (cu < n_items) {
-        item(cu, cbl, cbh);
-        nu = grab();
-        if (lane <= K && cbh > cbl) {
-          const uint32_t s0 = p.bucket_off[cbl], s1 = p.bucket_off[cbh];
-          if (s1 - s0 <= (uint32_t)CAP) {
-            if (lane < K) bulk_prefetch_l2(p.key[lane] + s0, 4 * (s1 - s0));
-            else bulk_prefetch_l2(p.let + s0, s1 - s0);
-          }
-        }
+  uint32_t nraw = 0;
+  if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+  uint32_t cu = __shfl_sync(0xffffffffu, nraw, 0);
+  uint32_t cbl = 0, cbh = 0, cs0 = 0, cs1 = 0;
+  if (cu < n_items) {
+    item(cu, cbl, cbh);
+    cs0 = p.bucket_off[cbl];
+    cs1 = p.bucket_off[cbh];
+  }
+  if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+  uint32_t ep = 0;
+  while (cu < n_items) {
+    const uint32_t nu = __shfl_sync(0xffffffffu, nraw, 0);
+    uint32_t nbl = 0, nbh = 0, ns0 = 0, ns1 = 0;
+    if (nu < n_items) item(nu, nbl, nbh);
+    if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+    bool nres = false;
+    auto resolve_next = [&]() {   // next unit's event range + L2 prefetch of its bytes
+      if (nres) return;
+      nres = true;
+      if (nu >= n_items) return;
+      ns0 = p.bucket_off[nbl];
+      ns1 = p.bucket_off[nbh];
+      if (lane <= K && ns1 > ns0 && ns1 - ns0 <= (uint32_t)CAP) {
+        if (lane < K) bulk_prefetch_l2(p.key[lane] + ns0, 4 * (ns1 - ns0));
+        else bulk_prefetch_l2(p.let + ns0, ns1 - ns0);
       }
-      if (bh <= bl) continue;
-    }
-    const uint32_t start = p.bucket_off[bl];
-    const uint32_t cnt = p.bucket_off[bh] - start;
-    if (cnt == 0) continue;
-    if (cnt > (uint32_t)CAP) {
-      if (bh - bl > 1) { pend_lo = bl; pend_hi = bh; continue; }
-      if (lane == 0) p.spill_list[atomicAdd(p.spill_len, 1ull)] = bl;
-      continue;
-    }
-    // stage the unit (cp.async, 16-byte chunks from 16-byte aligned addresses)
-    const uint32_t koff = start & 3u, loff = start & 15u;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t *g = p.key[k] + (start - koff);
-      for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
-    }
-    {
-      const uint8_t *g = p.let + (start - loff);
-      for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
-    }
-    cp_async_wait_all();
-    __syncwarp();
-    const uint32_t *kb[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
-    const uint8_t *lb = &w.let[loff];
-    // a3 + a4 over windows of 32 x kIlp events
-    uint32_t nleaf = 0;
-    bool ovf = false;
-    int cslot = -1;                     // per-lane cache: deepest ancestor of the last new leaf
-    uint32_t ck[K > 1 ? K - 1 : 1];
-#pragma unroll
-    for (int i = 0; i < (K > 1 ? K - 1 : 1); ++i) ck[i] = 0;
-    for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
-      int slot[kIlp];
-      bool fresh[kIlp];
-#pragma unroll
-      for (int r = 0; r < kIlp; ++r) {
-        const int e = (int)(base + 32 * r + lane);
-        slot[r] = -1;
-        fresh[r] = false;
-        if (e < (int)cnt) {
-          uint32_t kv[K];
-#pragma unroll
-          for (int i = 0; i < K; ++i) kv[i] = kb[i][e];
-          constexpr int shift = 32 - __builtin_ctz((unsigned)Tab::LS);
-          uint32_t h = key_hash<K>(kv, K) >> shift;
-          volatile uint16_t *vt = w.ltag;
-          while (true) {
-            uint32_t t = vt[h];
-            if (t == 0) {
-              t = atomicCAS(&w.ltag[h], (unsigned short)0, (unsigned short)(e + 1));
-              if (t == 0) { fresh[r] = true; break; }
-            }
-            bool eq = true;
-#pragma unroll
-            for (int i = 0; i < K; ++i) eq &= kb[i][t - 1] == kv[i];
-            if (eq) break;
-            h = (h + 1) & (uint32_t)(Tab::LS - 1);
-          }
-          slot[r] = (int)h;
-          if (K > 1 && fresh[r] && !ovf) {
-            // ancestors of the new leaf (depths 1 .. K-1), cached per lane
-            bool hit = cslot >= 0;
-#pragma unroll
-            for (int i = 0; i < K - 1; ++i) hit &= ck[i] == kv[i];
-            if (!hit) {
-              int parent = -1;
-              for (int l = 1; l < K; ++l) {
-                bool isnew = false;
-                const int ns = node_probe<K>(w.ntag[l - 1], kb, kv, e, l, &isnew, &w.ncnt[l], node_limit,
-                                             w.nlist[l - 1]);
-                if (ns < 0) { ovf = true; break; }
-                if (isnew && l > 1) w.npar[l - 1][ns] = (uint16_t)parent;
-                parent = ns;
-              }
-              cslot = ovf ? -1 : parent;
-#pragma unroll
-              for (int i = 0; i < K - 1; ++i) ck[i] = kv[i];
-            }
-            if (!ovf) w.lnode[h] = (uint16_t)cslot;
-          }
-        }
-      }
-#pragma unroll
-      for (int r = 0; r < kIlp; ++r) {  // append new leaves (warp-uniform count)
-        const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
-        if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
-        nleaf += __popc(nm);
-      }
-      bool old = false;
-#pragma unroll
-      for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
-      if (!__any_sync(0xffffffffu, old)) {
-        // every touched slot is new and touched once: one step from q0
-#pragma unroll
-        for (int r = 0; r < kIlp; ++r)
-          if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[q0 * A + lb[base + 32 * r + lane]];
+    };
+    const bool split = cs1 - cs0 > (uint32_t)CAP && cbh - cbl > 1;
+    for (uint32_t b = cbl;;) {
+      uint32_t bl, bh, start, cnt;
+      if (!split) {
+        bl = cbl; bh = cbh; start = cs0; cnt = cs1 - cs0;
       } else {
+        if (b >= cbh) break;
+        bl = b; bh = b + 1;
+        start = p.bucket_off[b];
+        cnt = p.bucket_off[b + 1] - start;
+        ++b;
+      }
+      if (cnt > (uint32_t)CAP) {
+        if (lane == 0) p.spill_list[atomicAdd(p.spill_len, 1ull)] = bl;
+      } else if (cnt > 0) {
+        // a new epoch: every slot of the previous unit reads as empty
+        if (++ep == 0x10000u) {
+          for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+          for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
+          ep = 1;
+        }
+        if (lane < 4) w.ncnt[lane] = 0;
+        // stage the unit (cp.async, 16-byte chunks from 16-byte aligned addresses)
+        const uint32_t koff = start & 3u, loff = start & 15u;
 #pragma unroll
-        for (int r = 0; r < kIlp; ++r)
-          if (fresh[r]) w.lstate[slot[r]] = (uint8_t)q0;
+        for (int k = 0; k < K; ++k) {
+          const uint32_t *g = p.key[k] + (start - koff);
+          for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
+        }
+        {
+          const uint8_t *g = p.let + (start - loff);
+          for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
+        }
+        cp_async_wait_all();
         __syncwarp();
+        const uint32_t *kb[K];
 #pragma unroll
-        for (int r = 0; r < kIlp; ++r) {
-          const bool act = slot[r] >= 0;
-          const uint32_t am = __ballot_sync(0xffffffffu, act);
-          if (act) {
-            const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
-            if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
-              uint32_t q = w.lstate[slot[r]];
-              uint32_t m = peers;
-              while (m) {
-                const int i = __ffs(m) - 1;
-                m &= m - 1;
-                q = sdelta[q * A + lb[base + 32 * r + i]];
+        for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
+        const uint8_t *lb = &w.let[loff];
+        // a3 + a4 over windows of 32 x kIlp events
+        uint32_t nleaf = 0;
+        bool ovf = false;
+        int cslot = -1;                 // per-lane cache: deepest ancestor of the last new leaf
+        uint32_t ck[K > 1 ? K - 1 : 1];
+#pragma unroll
+        for (int i = 0; i < (K > 1 ? K - 1 : 1); ++i) ck[i] = 0;
+        for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
+          int slot[kIlp];
+          bool fresh[kIlp];
+#pragma unroll
+          for (int r = 0; r < kIlp; ++r) {
+            const int e = (int)(base + 32 * r + lane);
+            slot[r] = -1;
+            fresh[r] = false;
+            if (e < (int)cnt) {
+              uint32_t kv[K];
+#pragma unroll
+              for (int i = 0; i < K; ++i) kv[i] = kb[i][e];
+              constexpr int shift = 32 - __builtin_ctz((unsigned)Tab::LS);
+              uint32_t h = key_hash<K>(kv, K) >> shift;
+              volatile uint32_t *vt = w.ltag;
+              while (true) {
+                uint32_t t = vt[h];
+                if ((t >> 16) != ep) {
+                  const uint32_t o = atomicCAS(&w.ltag[h], t, ep << 16 | (uint32_t)(e + 1));
+                  if (o == t) { fresh[r] = true; break; }
+                  t = o;
+                }
+                const int rep = (int)(t & 0xFFFFu) - 1;
+                bool eq = true;
+#pragma unroll
+                for (int i = 0; i < K; ++i) eq &= kb[i][rep] == kv[i];
+                if (eq) break;
+                h = (h + 1) & (uint32_t)(Tab::LS - 1);
               }
-              w.lstate[slot[r]] = (uint8_t)q;
+              slot[r] = (int)h;
+              if (K > 1 && fresh[r] && !ovf) {
+                // ancestors of the new leaf (depths 1 .. K-1), cached per lane
+                bool hit = cslot >= 0;
+#pragma unroll
+                for (int i = 0; i < K - 1; ++i) hit &= ck[i] == kv[i];
+                if (!hit) {
+                  int parent = -1;
+                  for (int l = 1; l < K; ++l) {
+                    bool isnew = false;
+                    const int ns = node_probe<K, NF>(w.ntag[l - 1], w.nhist[l - 1], kb, kv, e, l, ep, &isnew,
+                                                     &w.ncnt[l], node_limit, w.nlist[l - 1]);
+                    if (ns < 0) { ovf = true; break; }
+                    if (isnew && l > 1) w.npar[l - 1][ns] = (uint16_t)parent;
+                    parent = ns;
+                  }
+                  cslot = ovf ? -1 : parent;
+#pragma unroll
+                  for (int i = 0; i < K - 1; ++i) ck[i] = kv[i];
+                }
+                if (!ovf) w.lnode[h] = (uint16_t)cslot;
+              }
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < kIlp; ++r) {  // append new leaves (warp-uniform count)
+            const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
+            if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
+            nleaf += __popc(nm);
+          }
+          bool old = false;
+#pragma unroll
+          for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
+          if (!__any_sync(0xffffffffu, old)) {
+            // every touched slot is new and touched once: one step from q0
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r)
+              if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[q0 * A + lb[base + 32 * r + lane]];
+          } else {
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r)
+              if (fresh[r]) w.lstate[slot[r]] = (uint8_t)q0;
+            __syncwarp();
+#pragma unroll
+            for (int r = 0; r < kIlp; ++r) {
+              if (base + 32 * r >= cnt) break;
+              const bool act = slot[r] >= 0;
+              const uint32_t am = __ballot_sync(0xffffffffu, act);
+              if (act) {
+                const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
+                if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
+                  uint32_t q = w.lstate[slot[r]];
+                  uint32_t m = peers;
+                  while (m) {
+                    const int i = __ffs(m) - 1;
+                    m &= m - 1;
+                    q = sdelta[q * A + lb[base + 32 * r + i]];
+                  }
+                  w.lstate[slot[r]] = (uint8_t)q;
+                }
+              }
+              __syncwarp();
             }
           }
           __syncwarp();
         }
-      }
-      __syncwarp();
-    }
-    ovf = __any_sync(0xffffffffu, ovf);
-    if (ovf) {
-      // too many distinct prefixes for the warp tables: hand the buckets on
-      for (uint32_t x = bl + lane; x < bh; x += 32)
-        if (p.bucket_off[x + 1] > p.bucket_off[x]) p.spill_list[atomicAdd(p.spill_len, 1ull)] = x;
-    } else {
-      // a5 (i): leaf verdicts; lane takes a contiguous run of the leaf list so
-      // its child counts are aggregated per ancestor before one atomic flush
-      const uint32_t per = (nleaf + 31) >> 5;
-      const uint32_t i0 = min(nleaf, lane * per), i1 = min(nleaf, i0 + per);
-      int cur = -1;
-      uint32_t hv[NF][3];
+        resolve_next();
+        ovf = __any_sync(0xffffffffu, ovf);
+        if (ovf) {
+          // too many distinct prefixes for the warp tables: hand the buckets on
+          for (uint32_t x = bl + lane; x < bh; x += 32)
+            if (p.bucket_off[x + 1] > p.bucket_off[x]) p.spill_list[atomicAdd(p.spill_len, 1ull)] = x;
+        } else {
+          // a5 (i): leaf verdicts; lane takes a contiguous run of the leaf list so
+          // its child counts are aggregated per ancestor before one atomic flush
+          const uint32_t per = (nleaf + 31) >> 5;
+          const uint32_t i0 = min(nleaf, lane * per), i1 = min(nleaf, i0 + per);
+          int cur = -1;
+          unsigned long long hv[NF];
 #pragma unroll
-      for (int f = 0; f < NF; ++f) hv[f][0] = hv[f][1] = hv[f][2] = 0;
-      for (uint32_t i = i0; i < i1; ++i) {
-        const int s = w.llist[i];
-        const int q = w.lstate[s];
-        if (K > 1) {
-          const int nd = w.lnode[s];
-          if (nd != cur) {
-            if (cur >= 0) {
+          for (int f = 0; f < NF; ++f) hv[f] = 0;
+          auto flush_hv = [&]() {
 #pragma unroll
-              for (int f = 0; f < NF; ++f)
-#pragma unroll
-                for (int x = 0; x < 3; ++x)
-                  if (hv[f][x]) { atomicAdd(&w.nhist[K - 2][cur][f * 3 + x], hv[f][x]); hv[f][x] = 0; }
+            for (int f = 0; f < NF; ++f) {
+              if (hv[f]) {
+                uint32_t *hw = w.nhist[K > 1 ? K - 2 : 0][cur] + f * 3;
+                const uint32_t f0 = (uint32_t)hv[f] & 0xFFFFu, f1 = (uint32_t)(hv[f] >> 16) & 0xFFFFu;
+                const uint32_t f2 = (uint32_t)(hv[f] >> 32) & 0xFFFFu, f3 = (uint32_t)(hv[f] >> 48);
+                if (f0) atomicAdd(&hw[0], f0);
+                if (f1 | f2) atomicAdd(&hw[1], f1 | f2 << 16);
+                if (f3) atomicAdd(&hw[2], f3 << 16);
+                lcp[f] += hv[f];
+                hv[f] = 0;
+              }
             }
-            cur = nd;
+          };
+          for (uint32_t i = i0; i < i1; ++i) {
+            const int s = w.llist[i];
+            const int q = w.lstate[s];
+            if (K > 1) {
+              const int nd = w.lnode[s];
+              if (nd != cur) {
+                if (cur >= 0) flush_hv();
+                cur = nd;
+              }
+            }
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              const int v = slab[f * kMaxStates + q];
+              const unsigned long long inc = 1ull << (16 * ((v + 1) >> 1));  // v = 0, 2, 3, 5 -> field 0..3
+              if (K > 1) hv[f] += inc; else lcp[f] += inc;
+            }
           }
-        }
+          if (K > 1 && cur >= 0) flush_hv();
+          since += per;
+          if (since > 60000u) { flush_lcp(); since = 0; }
+          __syncwarp();
+          // a5 (ii): node verdicts by Def. 6, depth K-1 .. 1
+          for (int l = K - 1; l >= 1; --l) {
+            const uint32_t nn = w.ncnt[l];
+            for (uint32_t i = lane; i < nn; i += 32) {
+              const int s = w.nlist[l - 1][i];
 #pragma unroll
-        for (int f = 0; f < NF; ++f) {
-          const int v = slab[f * kMaxStates + q];
-          const int j = (v + 1) >> 1;   // 0 -> 0, 2 -> 1, 3 -> 2, 5 -> 3
-          lc[f][0] += j == 0; lc[f][1] += j == 1; lc[f][2] += j == 2; lc[f][3] += j == 3;
-          if (K > 1) {
-            const uint32_t inc = 1u << (16 * (v & 1));
-            hv[f][0] += (v >> 1) == 0 ? inc : 0u;
-            hv[f][1] += (v >> 1) == 1 ? inc : 0u;
-            hv[f][2] += (v >> 1) == 2 ? inc : 0u;
-          }
-        }
-      }
-      if (K > 1 && cur >= 0) {
+              for (int f = 0; f < NF; ++f) {
+                const uint32_t *hw = w.nhist[l - 1][s] + f * 3;
+                uint32_t h[6];
 #pragma unroll
-        for (int f = 0; f < NF; ++f)
-#pragma unroll
-          for (int x = 0; x < 3; ++x)
-            if (hv[f][x]) atomicAdd(&w.nhist[K - 2][cur][f * 3 + x], hv[f][x]);
-      }
-      __syncwarp();
-      // a5 (ii): node verdicts by Def. 6, depth K-1 .. 1
-      for (int l = K - 1; l >= 1; --l) {
-        const uint32_t nn = w.ncnt[l];
-        for (uint32_t i = lane; i < nn; i += 32) {
-          const int s = w.nlist[l - 1][i];
-#pragma unroll
-          for (int f = 0; f < NF; ++f) {
-            const uint32_t *hw = w.nhist[l - 1][s] + f * 3;
-            uint32_t h[6];
-#pragma unroll
-            for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
-            const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
-            atomicAdd(&sacc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
-            if (l > 1) atomicAdd(&w.nhist[l - 2][w.npar[l - 1][s]][f * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+                for (int x = 0; x < 6; ++x) h[x] = (hw[x >> 1] >> (16 * (x & 1))) & 0xFFFFu;
+                const int v = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
+                atomicAdd(&sacc[(f * (kMaxLevels + 1) + l) * 6 + v], 1u);
+                if (l > 1) atomicAdd(&w.nhist[l - 2][w.npar[l - 1][s]][f * 3 + (v >> 1)], 1u << (16 * (v & 1)));
+              }
+            }
+            __syncwarp();
           }
         }
         __syncwarp();
       }
+      if (!split) break;
     }
-    // clear the slots this unit claimed
-    for (uint32_t i = lane; i < nleaf; i += 32) w.ltag[w.llist[i]] = 0;
-    if (K > 1) {
-      for (int l = 1; l < K; ++l) {
-        const uint32_t nn = min(w.ncnt[l], (uint32_t)Tab::NS);
-        for (uint32_t i = lane; i < nn; i += 32) {
-          const int s = w.nlist[l - 1][i];
-          w.ntag[l - 1][s] = 0;
-#pragma unroll
-          for (int x = 0; x < NF * 3; ++x) w.nhist[l - 1][s][x] = 0;
-        }
-      }
-    }
-    __syncwarp();
-    if (lane < 4) w.ncnt[lane] = 0;
-    __syncwarp();
+    resolve_next();
+    cu = nu; cbl = nbl; cbh = nbh; cs0 = ns0; cs1 = ns1;
   }
-  // leaf-level counts: warp reduce, CTA accumulate, one global flush per CTA
-#pragma unroll
-  for (int f = 0; f < NF; ++f)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const uint32_t c = __reduce_add_sync(0xffffffffu, lc[f][j]);
-      if (lane == 0 && c) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + (j == 0 ? 0 : j + 1 + (j == 3))], c);
-    }
+  flush_lcp();
   __syncthreads();
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
     const uint32_t v = sacc[i];
