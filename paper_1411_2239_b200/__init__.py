@@ -22,6 +22,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libltl4c.so")
+if os.environ.get("LTL4C_LIB_VARIANT"):  # in-tree tuning variants (scripts/build_variant.sh)
+    LIB_PATH = os.path.join(_HERE, f"libltl4c_{os.environ['LTL4C_LIB_VARIANT']}.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "ltl4c.h")
 
 MAX_LEVELS = 3

@@ -371,14 +371,20 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 //       per-lane run-length aggregation, then Def. 6 level by level.
 // Table slots carry a per-unit epoch (tag = epoch << 16 | rep event + 1), so no
 // table is cleared between units.
-constexpr int kIlp = 4;                 // events per lane per window
+#ifndef LTL4C_ILP
+#define LTL4C_ILP 4
+#endif
+#ifndef LTL4C_LS_MUL
+#define LTL4C_LS_MUL 2
+#endif
+constexpr int kIlp = LTL4C_ILP;         // events per lane per window
 constexpr int kWarpHdr = kMaxStates * 256 + kMaxFormulas * kMaxStates + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
 
 template <int K, int NF, int CAP>
 struct alignas(16) WarpTab {
   static constexpr int NL = K > 1 ? K - 1 : 1;        // inner levels 1 .. K-1 (index l - 1)
   static constexpr int NS = K > 1 ? kNodeSlots : 1;
-  static constexpr int LS = 2 * CAP;                  // leaf slots (load <= 1/2)
+  static constexpr int LS = LTL4C_LS_MUL * CAP;       // leaf slots (load <= 1/2)
   uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
   uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
   uint32_t ltag[LS];                    // epoch << 16 | rep event + 1 (other epochs = empty)

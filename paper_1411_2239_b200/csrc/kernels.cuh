@@ -13,9 +13,15 @@ constexpr int kMaxDigits = 1 << kMaxDigitBits;
 constexpr int kMaxPasses = 3;        // bucket bits <= 27
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
-constexpr int kWarpCap = 256;        // events per warp-processed unit
-constexpr int kWarpCapBig = 1024;    // events per warp-processed medium bucket
-constexpr int kUnitTarget = 192;     // events per bucket_warp work unit (consecutive buckets)
+#ifndef LTL4C_WARP_CAP
+#define LTL4C_WARP_CAP 256
+#endif
+#ifndef LTL4C_UNIT_TARGET
+#define LTL4C_UNIT_TARGET 192
+#endif
+constexpr int kWarpCap = LTL4C_WARP_CAP;        // events per warp-processed unit
+constexpr int kWarpCapBig = 1024;               // events per warp-processed medium bucket
+constexpr int kUnitTarget = LTL4C_UNIT_TARGET;  // events per bucket_warp work unit (consecutive buckets)
 constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)

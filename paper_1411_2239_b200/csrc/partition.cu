@@ -102,7 +102,9 @@ struct SweepSmem {
   uint32_t wt[kPWarps];
 };
 
-// exclusive scan over the block, one value per thread (kPartThreads = 16 warps)
+// exclusive scan over the block, one value per thread (kPartThreads = 16 warps):
+// warp scans by shuffles, then the 16 warp totals are scanned by shuffles in
+// every warp (one broadcast load each)
 __device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   uint32_t inc = x;
@@ -113,9 +115,13 @@ __device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
   }
   if (lane == 31) wt[wid] = inc;
   __syncthreads();
-  uint32_t add = 0;
+  uint32_t t = wt[lane & (kPWarps - 1)];
 #pragma unroll
-  for (int w = 0; w < kPWarps; ++w) add += w < wid ? wt[w] : 0u;
+  for (int d = 1; d < kPWarps; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+    if ((lane & (kPWarps - 1)) >= d) t += y;
+  }
+  const uint32_t add = wid ? __shfl_sync(0xffffffffu, t, wid - 1) : 0u;
   __syncthreads();
   return inc - x + add;
 }
@@ -163,7 +169,9 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
     if (d0 <= (int)dmask) til0 = pl.counts[(size_t)d0 * pl.n_tiles + tile];
     if (d1 <= (int)dmask) til1 = pl.counts[(size_t)d1 * pl.n_tiles + tile];
   }
-  for (int i = tid; i < kPWarps * kMaxDigits; i += kPartThreads) (&s.wcnt[0][0])[i] = 0;
+  static_assert(sizeof(s.wcnt) % (16 * kPartThreads) == 0, "wcnt zeroing by 16-byte stores");
+#pragma unroll
+  for (int i = tid; i < (int)(sizeof(s.wcnt) / 16); i += kPartThreads) reinterpret_cast<uint4 *>(&s.wcnt[0][0])[i] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   // stable rank within the warp's range
   uint32_t dg[kRounds], pm[kRounds];
