@@ -759,18 +759,16 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
 
 // ----------------------------------------------- work units for bucket_warp
 // unit u = buckets [unit_start[u], unit_start[u+1]): the buckets whose first event
-// lies in [u * kUnitTarget, (u + 1) * kUnitTarget)
+// lies in [u * kUnitTarget, (u + 1) * kUnitTarget).  Thread per bucket c: the
+// units whose boundary u * kUnitTarget lies in (off[c-1], off[c]] start at c
+// (c = nb, the end: every remaining unit).
 __global__ void unit_start_kernel(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units) {
-  const uint32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-  if (u > n_units) return;
-  // lower bound: first bucket c with off[c] >= u * kUnitTarget (off is ascending)
-  const unsigned long long x = (unsigned long long)u * kUnitTarget;
-  uint32_t lo = 0, hi = nb;
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if ((unsigned long long)off[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  ustart[u] = lo;
+  const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c > nb) return;
+  if (c == 0) { ustart[0] = 0; return; }
+  const uint32_t u0 = off[c - 1] / kUnitTarget + 1;
+  const uint32_t u1 = c == nb ? n_units : min(n_units, off[c] / kUnitTarget);
+  for (uint32_t u = u0; u <= u1; ++u) ustart[u] = c;
 }
 
 // ----------------------------------------------- global tables
@@ -1427,7 +1425,7 @@ cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t gr
 }
 
 cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L) {
-  LTL4C_LAUNCH(kKUnitStart, unit_start_kernel<<<(n_units + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units));
+  LTL4C_LAUNCH(kKUnitStart, unit_start_kernel<<<(nb + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units));
 }
 
 template <int K, int NF, int CAP>

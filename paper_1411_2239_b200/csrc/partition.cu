@@ -72,19 +72,48 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
   }
 }
 
-// exclusive scan of counts[d][0..n_tiles) in place (one CTA per digit), totals[d]
-__global__ void __launch_bounds__(1024) part_scan_kernel(PartPlan pl, int pass) {
-  __shared__ uint32_t buf[1024];
-  __shared__ uint32_t wt[32];
+// exclusive scan of counts[d][0..n_tiles) in place (one CTA per digit), totals[d]:
+// thread t owns a contiguous run of the row (all its loads issued at once), one
+// block scan of the run sums
+constexpr int kScanThreads = 256;
+constexpr int kScanPer = 16;  // rows up to 4096 tiles in one sweep (16.7M events)
+__global__ void __launch_bounds__(kScanThreads) part_scan_kernel(PartPlan pl, int pass) {
+  __shared__ uint32_t wt[kScanThreads / 32];
   uint32_t *row = pl.counts + (size_t)blockIdx.x * pl.n_tiles;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint32_t carry = 0;
-  for (uint32_t off = 0; off < pl.n_tiles; off += 1024) {
-    const uint32_t i = off + threadIdx.x;
-    buf[threadIdx.x] = i < pl.n_tiles ? row[i] : 0;
+  for (uint32_t off = 0; off < pl.n_tiles; off += kScanThreads * kScanPer) {
+    const uint32_t per = min((uint32_t)kScanPer, (pl.n_tiles - off + kScanThreads - 1) / kScanThreads);
+    const uint32_t lo = off + tid * per;
+    uint32_t v[kScanPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+      v[i] = ((uint32_t)i < per && lo + i < pl.n_tiles) ? row[lo + i] : 0u;
+      sum += v[i];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    if (lane == 31) wt[wid] = inc;
     __syncthreads();
-    const uint32_t tot = block_exclusive_scan(buf, 1024, wt);
-    if (i < pl.n_tiles) row[i] = buf[threadIdx.x] + carry;
-    carry += tot;
+    uint32_t t = lane < kScanThreads / 32 ? wt[lane] : 0u;
+#pragma unroll
+    for (int d = 1; d < kScanThreads / 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += y;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, t, kScanThreads / 32 - 1);
+    uint32_t run = carry + inc - sum + (wid ? __shfl_sync(0xffffffffu, t, wid - 1) : 0u);
+#pragma unroll
+    for (int i = 0; i < kScanPer; ++i) {
+      if ((uint32_t)i < per && lo + i < pl.n_tiles) row[lo + i] = run;
+      run += v[i];
+    }
+    carry += total;
     __syncthreads();
   }
   if (threadIdx.x == 0) pl.digit_hist[pass * kMaxDigits + blockIdx.x] = carry;
@@ -268,28 +297,33 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 }
 
 // off[c] = first position of bucket c in the final order, off[NB] = n.  Each
-// thread covers 4 consecutive positions (one 16-byte load).
+// thread covers 16 consecutive positions (four 16-byte loads issued together).
+constexpr int kBoundsPer = 16;
 __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, int bits,
                                      uint32_t *off, uint32_t nb) {
   const unsigned long long n = *nvalid;
-  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; 4 * t <= n;
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; kBoundsPer * t <= n;
        t += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long i0 = 4 * t;
-    long long b[4];
-    if (i0 + 4 <= n) {
-      const uint4 v = __ldg(reinterpret_cast<const uint4 *>(k0 + i0));
-      b[0] = bucket_of(v.x, bits); b[1] = bucket_of(v.y, bits);
-      b[2] = bucket_of(v.z, bits); b[3] = bucket_of(v.w, bits);
+    const unsigned long long i0 = kBoundsPer * t;
+    uint32_t kv[kBoundsPer];
+    if (i0 + kBoundsPer <= n) {
+#pragma unroll
+      for (int q = 0; q < kBoundsPer / 4; ++q) {
+        const uint4 v = __ldg(reinterpret_cast<const uint4 *>(k0 + i0) + q);
+        kv[4 * q] = v.x; kv[4 * q + 1] = v.y; kv[4 * q + 2] = v.z; kv[4 * q + 3] = v.w;
+      }
     } else {
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = i0 + j < n ? (long long)bucket_of(k0[i0 + j], bits) : (long long)nb;
+      for (int j = 0; j < kBoundsPer; ++j) kv[j] = i0 + j < n ? k0[i0 + j] : 0u;
     }
-    long long prev = i0 == 0 ? -1 : (long long)bucket_of(k0[i0 - 1], bits);
+    const uint32_t kp = i0 == 0 ? 0u : k0[i0 - 1];
+    long long prev = i0 == 0 ? -1 : (long long)bucket_of(kp, bits);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < kBoundsPer; ++j) {
       if (i0 + j > n) break;
-      for (long long c = prev + 1; c <= b[j]; ++c) off[c] = (uint32_t)(i0 + j);
-      prev = b[j];
+      const long long b = i0 + j < n ? (long long)bucket_of(kv[j], bits) : (long long)nb;
+      for (long long c = prev + 1; c <= b; ++c) off[c] = (uint32_t)(i0 + j);
+      prev = b;
     }
   }
 }
@@ -317,7 +351,7 @@ cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
 }
 
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {
-  LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width[pass], 1024, 0, L.stream>>>(p, pass));
+  LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width[pass], kScanThreads, 0, L.stream>>>(p, pass));
 }
 
 template <int K>
@@ -337,7 +371,7 @@ cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) 
 
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
   const uint32_t *k0 = p.buf_key[(p.passes - 1) & 1][0];
-  const unsigned long long want = (p.n / 4 + 1 + 255) / 256;
+  const unsigned long long want = (p.n / kBoundsPer + 1 + 255) / 256;
   const unsigned grid = (unsigned)(want > 148 * 16 ? 148 * 16 : want);
   LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(k0, p.nvalid, p.bits, off, n_buckets));
 }
