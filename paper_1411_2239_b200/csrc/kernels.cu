@@ -378,17 +378,23 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 #define LTL4C_LS_MUL 2
 #endif
 constexpr int kIlp = LTL4C_ILP;         // events per lane per window
-constexpr int kWarpHdr = kMaxStates * 256 + kMaxFormulas * kMaxStates + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
+// CTA header: sacc [kMaxFormulas][kMaxLevels + 1][6] u32, lab [kMaxFormulas][kMaxStates],
+// then delta [nq][2^na] (sized by the program: warp_hdr_bytes)
+constexpr int kWarpHdrFixed = 4 * kMaxFormulas * (kMaxLevels + 1) * 6 + kMaxFormulas * kMaxStates;
+__host__ __device__ inline uint32_t warp_hdr_bytes(uint32_t nq, uint32_t na) {
+  return (uint32_t)align16(kWarpHdrFixed + (size_t)nq * (1u << na));
+}
 
 template <int K, int NF, int CAP>
 struct alignas(16) WarpTab {
   static constexpr int NL = K > 1 ? K - 1 : 1;        // inner levels 1 .. K-1 (index l - 1)
-  static constexpr int NS = K > 1 ? kNodeSlots : 1;
+  static constexpr int NSL = CAP / 4;                 // node slots per inner level (claims <= NSL / 2)
+  static constexpr int NS = K > 1 ? NSL : 1;
   static constexpr int LS = LTL4C_LS_MUL * CAP;       // leaf slots (load <= 1/2)
   uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
   uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
   uint32_t ltag[LS];                    // epoch << 16 | rep event + 1 (other epochs = empty)
-  uint16_t lnode[K > 1 ? LS : 1];       // depth-(K-1) ancestor slot of the leaf
+  uint8_t lnode[K > 1 ? LS : 1];        // depth-(K-1) ancestor slot of the leaf
   uint8_t lstate[LS];
   uint16_t llist[CAP];                  // leaf slots in creation order
   uint32_t ntag[NL][NS];                // as ltag
@@ -424,11 +430,11 @@ __device__ __forceinline__ uint32_t key_hash(const uint32_t (&kv)[K], int m) {
 // find-or-insert of the m-key prefix of kv (event e) in a node table of the
 // current epoch; returns the slot, -1 when `limit` claims are exceeded
 // (overflow -> the next path).  A new slot's histogram words are zeroed.
-template <int K, int NF>
+template <int K, int NF, int NSL>
 __device__ __forceinline__ int node_probe(uint32_t *tag, uint32_t (*hist)[NF * 3], const uint32_t *const (&kb)[K],
                                           const uint32_t (&kv)[K], int e, int m, uint32_t ep, bool *isnew,
                                           uint32_t *claims, uint32_t limit, uint16_t *list) {
-  constexpr int shift = 32 - __builtin_ctz((unsigned)kNodeSlots);
+  constexpr int shift = 32 - __builtin_ctz((unsigned)NSL);
   uint32_t h = key_hash<K>(kv, m) >> shift;
   volatile uint32_t *vt = tag;
   while (true) {
@@ -451,7 +457,7 @@ __device__ __forceinline__ int node_probe(uint32_t *tag, uint32_t (*hist)[NF * 3
     for (int i = 0; i < K; ++i)
       if (i < m) eq &= kb[i][rep] == kv[i];
     if (eq) { *isnew = false; return (int)h; }
-    h = (h + 1) & (uint32_t)(kNodeSlots - 1);
+    h = (h + 1) & (uint32_t)(NSL - 1);
   }
 }
 
@@ -461,11 +467,11 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
   const int nq = prog->nq, A = 1 << prog->na;
-  uint8_t *sdelta = smem_raw;
-  uint8_t *slab = smem_raw + kMaxStates * 256;
-  uint32_t *sacc = reinterpret_cast<uint32_t *>(smem_raw + kMaxStates * 256 + kMaxFormulas * kMaxStates);
+  uint32_t *sacc = reinterpret_cast<uint32_t *>(smem_raw);
+  uint8_t *slab = smem_raw + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
+  uint8_t *sdelta = slab + kMaxFormulas * kMaxStates;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Tab &w = reinterpret_cast<Tab *>(smem_raw + kWarpHdr)[wid];
+  Tab &w = reinterpret_cast<Tab *>(smem_raw + warp_hdr_bytes(nq, prog->na))[wid];
   for (int i = threadIdx.x; i < nq * A; i += blockDim.x) sdelta[i] = prog->delta[i / A][i % A];
   for (int i = threadIdx.x; i < kMaxFormulas * kMaxStates; i += blockDim.x)
     slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
@@ -474,7 +480,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
-  const uint32_t node_limit = kNodeSlots / 2;
+  const uint32_t node_limit = Tab::NSL / 2;
   // per-lane leaf verdict counts, 16-bit fields j = 0..3 for v = 0, 2, 3, 5
   unsigned long long lcp[NF];
 #pragma unroll
@@ -615,7 +621,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
                   int parent = -1;
                   for (int l = 1; l < K; ++l) {
                     bool isnew = false;
-                    const int ns = node_probe<K, NF>(w.ntag[l - 1], w.nhist[l - 1], kb, kv, e, l, ep, &isnew,
+                    const int ns = node_probe<K, NF, Tab::NSL>(w.ntag[l - 1], w.nhist[l - 1], kb, kv, e, l, ep, &isnew,
                                                      &w.ncnt[l], node_limit, w.nlist[l - 1]);
                     if (ns < 0) { ovf = true; break; }
                     if (isnew && l > 1) w.npar[l - 1][ns] = (uint16_t)parent;
@@ -625,7 +631,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
 #pragma unroll
                   for (int i = 0; i < K - 1; ++i) ck[i] = kv[i];
                 }
-                if (!ovf) w.lnode[h] = (uint16_t)cslot;
+                if (!ovf) w.lnode[h] = (uint8_t)cslot;
               }
             }
           }
@@ -1429,16 +1435,16 @@ cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart
 }
 
 template <int K, int NF, int CAP>
-static size_t warp_smem(int warps) { return kWarpHdr + (size_t)warps * sizeof(WarpTab<K, NF, CAP>); }
+static size_t warp_smem(int warps, uint32_t hdr) { return hdr + (size_t)warps * sizeof(WarpTab<K, NF, CAP>); }
 
 template <int K, int NF>
 static cudaError_t warp_launch(const BucketParams &p, uint32_t grid, const Launcher &L) {
   if (p.list) {  // medium buckets: the same kernel with 4x the capacity
-    const size_t sm = warp_smem<K, NF, kWarpCapBig>(p.warps_per_cta);
+    const size_t sm = warp_smem<K, NF, kWarpCapBig>(p.warps_per_cta, p.warp_hdr);
     cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCapBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<K, NF, kWarpCapBig><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
   }
-  const size_t sm = warp_smem<K, NF, kWarpCap>(p.warps_per_cta);
+  const size_t sm = warp_smem<K, NF, kWarpCap>(p.warps_per_cta, p.warp_hdr);
   cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<K, NF, kWarpCap><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
 }
@@ -1446,10 +1452,10 @@ static cudaError_t warp_launch(const BucketParams &p, uint32_t grid, const Launc
 // (warps per CTA, resident CTAs per SM) with the most resident warps (registers
 // and shared memory both counted by the occupancy calculator)
 template <int K, int NF, int CAP>
-static cudaError_t warp_config_cap(int *warps, int *ctas) {
+static cudaError_t warp_config_cap(uint32_t hdr, int *warps, int *ctas) {
   int best = 0;
   for (int w = 1; w <= 8; ++w) {
-    const size_t sm = warp_smem<K, NF, CAP>(w);
+    const size_t sm = warp_smem<K, NF, CAP>(w, hdr);
     if (sm > 227 * 1024) break;
     cudaError_t e = cudaFuncSetAttribute(bucket_warp_kernel<K, NF, CAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
@@ -1462,9 +1468,9 @@ static cudaError_t warp_config_cap(int *warps, int *ctas) {
 }
 
 template <int K, int NF>
-static cudaError_t warp_config(int *cfg) {
-  cudaError_t e = warp_config_cap<K, NF, kWarpCap>(&cfg[0], &cfg[1]);
-  return e != cudaSuccess ? e : warp_config_cap<K, NF, kWarpCapBig>(&cfg[2], &cfg[3]);
+static cudaError_t warp_config(uint32_t hdr, int *cfg) {
+  cudaError_t e = warp_config_cap<K, NF, kWarpCap>(hdr, &cfg[0], &cfg[1]);
+  return e != cudaSuccess ? e : warp_config_cap<K, NF, kWarpCapBig>(hdr, &cfg[2], &cfg[3]);
 }
 
 #define LTL4C_KNF(K, NF, FN, ...)                                        \
@@ -1481,9 +1487,11 @@ cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t gr
   LTL4C_KNF(K, nf, warp_launch, p, grid, L);
 }
 
-cudaError_t bucket_warp_config(int K, int nf, int *cfg) {
-  LTL4C_KNF(K, nf, warp_config, cfg);
+cudaError_t bucket_warp_config(int K, int nf, int nq, int na, int *cfg) {
+  LTL4C_KNF(K, nf, warp_config, warp_hdr_bytes((uint32_t)nq, (uint32_t)na), cfg);
 }
+
+uint32_t bucket_warp_hdr(int nq, int na) { return warp_hdr_bytes((uint32_t)nq, (uint32_t)na); }
 
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, 1);

@@ -20,9 +20,11 @@ constexpr int kBucketThreads = 256;
 #define LTL4C_UNIT_TARGET 192
 #endif
 constexpr int kWarpCap = LTL4C_WARP_CAP;        // events per warp-processed unit
-constexpr int kWarpCapBig = 1024;               // events per warp-processed medium bucket
+#ifndef LTL4C_WARP_CAP_BIG
+#define LTL4C_WARP_CAP_BIG 1024
+#endif
+constexpr int kWarpCapBig = LTL4C_WARP_CAP_BIG;  // events per warp-processed medium bucket
 constexpr int kUnitTarget = LTL4C_UNIT_TARGET;  // events per bucket_warp work unit (consecutive buckets)
-constexpr int kNodeSlots = 128;      // warp node table per inner level (overflow -> CTA path)
 
 // The stable LSD partition of a batch by bucket = top `bits` bits of hash(k0)
 // (a1 + a2).  Per pass p (digit bits [lo[p], lo[p] + width[p])): count per
@@ -94,6 +96,7 @@ struct BucketParams {
   const uint8_t *let;
   const uint32_t *bucket_off;           // [n_buckets + 1]
   int warps_per_cta;
+  uint32_t warp_hdr;                    // warp kernels: CTA header bytes (bucket_warp_hdr)
   uint32_t n_buckets;
   const uint32_t *list;                 // if set: CTA i processes bucket list[i]
   const unsigned long long *list_len;   // number of entries in list
@@ -148,7 +151,8 @@ cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 // {warps per CTA, CTAs per SM} of the unit kernel (cfg[0..1]) and of the
 // medium-bucket kernel (cfg[2..3])
-cudaError_t bucket_warp_config(int K, int nf, int *cfg);
+cudaError_t bucket_warp_config(int K, int nf, int nq, int na, int *cfg);
+uint32_t bucket_warp_hdr(int nq, int na);  // CTA header bytes of the warp kernels
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L);
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,

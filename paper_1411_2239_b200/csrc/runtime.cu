@@ -423,6 +423,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.medium_list = st->medium_list.p;
   bp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 8;
   bp.warps_per_cta = st->warp_cfg[0];
+  bp.warp_hdr = bucket_warp_hdr((int)st->prog->n_states, (int)st->prog->n_atoms);
   bp.spill_list = st->medium_list.p;
   bp.spill_len = &st->d_acc.p->medium_buckets;
   bp.unit_start = st->unit_start.p;
@@ -855,7 +856,8 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   {
     // warp-per-unit kernel: the (warps per CTA, CTAs per SM) pair that keeps the
     // most warps resident for this program's (K, F) shared-memory plan
-    cudaError_t e = bucket_warp_config((int)prog->n_levels, (int)prog->n_formulas, st->warp_cfg);
+    cudaError_t e = bucket_warp_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states,
+                                       (int)prog->n_atoms, st->warp_cfg);
     if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
   }
   cudaSetDevice(prev);
