@@ -35,7 +35,8 @@ namespace ltl4c {
 
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast", "bucket_global",
-                                                "finalize", "rehash", "heavy", "unit_start"};
+                                                "finalize", "rehash", "heavy", "unit_start",
+                                                "bucket_warp_big"};
 
 namespace {
 
@@ -1442,7 +1443,7 @@ static cudaError_t warp_launch(const BucketParams &p, uint32_t grid, const Launc
   if (p.list) {  // medium buckets: the same kernel with 4x the capacity
     const size_t sm = warp_smem<K, NF, kWarpCapBig>(p.warps_per_cta, p.warp_hdr);
     cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCapBig>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    LTL4C_LAUNCH(kKBucketWarp, bucket_warp_kernel<K, NF, kWarpCapBig><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
+    LTL4C_LAUNCH(kKBucketWarpBig, bucket_warp_kernel<K, NF, kWarpCapBig><<<grid, 32 * p.warps_per_cta, sm, L.stream>>>(p));
   }
   const size_t sm = warp_smem<K, NF, kWarpCap>(p.warps_per_cta, p.warp_hdr);
   cudaFuncSetAttribute(bucket_warp_kernel<K, NF, kWarpCap>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

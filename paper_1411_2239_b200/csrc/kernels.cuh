@@ -138,6 +138,7 @@ enum KernelId {
   kKRehash,
   kKHeavy,
   kKUnitStart,
+  kKBucketWarpBig,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
