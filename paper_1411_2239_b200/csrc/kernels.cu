@@ -386,12 +386,14 @@ __host__ __device__ inline uint32_t warp_hdr_bytes(uint32_t nq, uint32_t na) {
   return (uint32_t)align16(kWarpHdrFixed + (size_t)nq * (1u << na));
 }
 
+__host__ __device__ constexpr int pow2ceil(int x) { return x <= 1 ? 1 : 2 * pow2ceil((x + 1) / 2); }
+
 template <int K, int NF, int CAP>
 struct alignas(16) WarpTab {
   static constexpr int NL = K > 1 ? K - 1 : 1;        // inner levels 1 .. K-1 (index l - 1)
-  static constexpr int NSL = CAP / 4;                 // node slots per inner level (claims <= NSL / 2)
+  static constexpr int NSL = pow2ceil(CAP / 4);       // node slots per inner level (claims <= NSL / 2)
   static constexpr int NS = K > 1 ? NSL : 1;
-  static constexpr int LS = LTL4C_LS_MUL * CAP;       // leaf slots (load <= 1/2)
+  static constexpr int LS = pow2ceil(LTL4C_LS_MUL * CAP);  // leaf slots (load <= 1/2)
   uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
   uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
   uint32_t ltag[LS];                    // epoch << 16 | rep event + 1 (other epochs = empty)
