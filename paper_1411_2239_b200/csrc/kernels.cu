@@ -36,7 +36,7 @@ namespace ltl4c {
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast", "bucket_global",
                                                 "finalize", "rehash", "heavy", "unit_start",
-                                                "bucket_warp_big"};
+                                                "bucket_warp_big", "online_leaf", "online_nodes"};
 
 namespace {
 
@@ -958,6 +958,339 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketPar
   flush_acc(s, p.acc, nf, nl);
 }
 
+// ----------------------------------------------- online path (carried state)
+// Online mode (§3.3): the submonitor set 𝔻 and every node of
+// the quantifier tree persist across batches in global tables.  A batch is
+// partitioned by the DEEPEST key (all events of a leaf share it, so a leaf's
+// events land in one bucket, in trace order, and buckets stay balanced even
+// when level-0 keys are few), then:
+//   online_leaf   warp per unit (or per <= CAP-event chunk of a larger bucket, in
+//                 order): leaves deduplicated in shared memory; a leaf seen for
+//                 the first time in the chunk is found-or-inserted in the global
+//                 leaf table (new leaves start at q0, existing ones resume --
+//                 "merged"); its events are stepped in trace order;
+//                 the state is written back; a verdict change old -> new moves
+//                 one child of its depth-(K-1) node (h[old]--, h[new]++) and
+//                 marks that node touched;
+//   online_nodes  depth K-1 .. 1: every touched node re-evaluates Def. 6 from
+//                 its histogram; a change moves one child of its parent.
+// The per-level histograms (acc) receive the same signed deltas; the root rule
+// is applied to the depth-1 histogram by finalize.
+constexpr uint8_t kNewLeaf = 0xFF;
+
+template <int K>
+struct alignas(16) OnlineTab {
+  static constexpr int CAP = kWarpCap;
+  static constexpr int LS = 2 * CAP;
+  uint32_t key[K][CAP + 4];             // staged keys; event i at [i + (start & 3)]
+  uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
+  uint32_t ltag[LS];                    // epoch << 16 | rep event + 1
+  uint32_t lg[LS];                      // global leaf slot
+  uint8_t lstate[LS];
+  uint8_t linit[LS];                    // state at chunk start, kNewLeaf for a leaf created now
+  uint16_t llist[CAP];
+};
+
+// node of depth l (keys k[0..l-1]) in the carried tables; a new node starts with
+// an empty histogram and no verdict
+__device__ __forceinline__ unsigned long long online_node(const OnlineParams &p, int l, const uint32_t *k,
+                                                          bool *ok) {
+  const DevTables &T = p.b.tab;
+  int ins;
+  const unsigned long long s = table_find_insert(T.node_slot[l], T.node_cap[l], T.epoch, k, l, &ins,
+                                                 &p.b.acc->table_overflow);
+  if (ins == 1) {
+    for (int x = 0; x < kMaxFormulas * 6; ++x) T.node_hist[l][s * kMaxFormulas * 6 + x] = 0;
+    T.node_verdict[l][s] = 0xFFFFFFFFu;
+    table_publish(T.node_slot[l], s, T.epoch);
+    atomicAdd(&p.b.acc->nodes[l], 1ull);
+  }
+  *ok = ins >= 0;
+  return s;
+}
+
+__device__ __forceinline__ void online_touch(const OnlineParams &p, int l, unsigned long long s) {
+  if (atomicExch(&p.b.tab.node_aux[l][s], p.bid) != p.bid) p.tlist[l][atomicAdd(&p.tcnt[l], 1u)] = (uint32_t)s;
+}
+
+template <int K, int NF>
+__global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
+  using Tab = OnlineTab<K>;
+  constexpr int CAP = Tab::CAP;
+  const BucketParams &p = op.b;
+  const DevTables &T = p.tab;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const DevProg *prog = p.prog;
+  const int nq = prog->nq, A = 1 << prog->na;
+  int *sacc = reinterpret_cast<int *>(smem_raw);
+  uint8_t *slab = smem_raw + 4 * kMaxFormulas * (kMaxLevels + 1) * 6;
+  uint8_t *sdelta = slab + kMaxFormulas * kMaxStates;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tab &w = reinterpret_cast<Tab *>(smem_raw + warp_hdr_bytes(nq, prog->na))[wid];
+  for (int i = threadIdx.x; i < nq * A; i += blockDim.x) sdelta[i] = prog->delta[i / A][i % A];
+  for (int i = threadIdx.x; i < kMaxFormulas * kMaxStates; i += blockDim.x)
+    slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) sacc[i] = 0;
+  for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+  __syncthreads();
+  const uint32_t q0 = prog->q0;
+  uint32_t ep = 0;
+  while (true) {
+    uint32_t u = 0;
+    if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= p.n_units) break;
+    const uint32_t ubl = p.unit_start[u], ubh = p.unit_start[u + 1];
+    if (ubh <= ubl) continue;
+    const uint32_t us = p.bucket_off[ubl], ue = p.bucket_off[ubh];
+    // pieces: the whole unit, or each bucket in chunks of <= CAP events (in order)
+    const bool split = ue - us > (uint32_t)CAP;
+    uint32_t b = ubl, pos = us, bend = split ? us : ue;
+    while (true) {
+      uint32_t start, cnt;
+      if (!split) {
+        if (pos >= ue) break;
+        start = us;
+        cnt = ue - us;
+        pos = ue;
+      } else {
+        while (pos >= bend && b < ubh) { pos = p.bucket_off[b]; bend = p.bucket_off[b + 1]; ++b; }
+        if (pos >= bend) break;
+        start = pos;
+        cnt = min((uint32_t)CAP, bend - pos);
+        pos += cnt;
+      }
+      if (++ep == 0x10000u) {
+        for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+        ep = 1;
+      }
+      const uint32_t koff = start & 3u, loff = start & 15u;
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const uint32_t *g = p.key[k] + (start - koff);
+        for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
+      }
+      {
+        const uint8_t *g = p.let + (start - loff);
+        for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
+      }
+      cp_async_wait_all();
+      __syncwarp();
+      const uint32_t *kb[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
+      const uint8_t *lb = &w.let[loff];
+      uint32_t nleaf = 0;
+      for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
+        int slot[kIlp];
+        bool fresh[kIlp];
+        uint32_t qs[kIlp];
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r) {
+          const int e = (int)(base + 32 * r + lane);
+          slot[r] = -1;
+          fresh[r] = false;
+          qs[r] = 0;
+          if (e < (int)cnt) {
+            uint32_t kv[K];
+#pragma unroll
+            for (int i = 0; i < K; ++i) kv[i] = kb[i][e];
+            constexpr int shift = 32 - __builtin_ctz((unsigned)Tab::LS);
+            uint32_t h = key_hash<K>(kv, K) >> shift;
+            volatile uint32_t *vt = w.ltag;
+            while (true) {
+              uint32_t t = vt[h];
+              if ((t >> 16) != ep) {
+                const uint32_t o = atomicCAS(&w.ltag[h], t, ep << 16 | (uint32_t)(e + 1));
+                if (o == t) { fresh[r] = true; break; }
+                t = o;
+              }
+              const int rep = (int)(t & 0xFFFFu) - 1;
+              bool eq = true;
+#pragma unroll
+              for (int i = 0; i < K; ++i) eq &= kb[i][rep] == kv[i];
+              if (eq) break;
+              h = (h + 1) & (uint32_t)(Tab::LS - 1);
+            }
+            slot[r] = (int)h;
+            if (fresh[r]) {
+              // first sight in this chunk: the carried leaf (or a new one at q0)
+              uint32_t k3[kMaxLevels] = {kv[0], K > 1 ? kv[1 % K] : 0u, K > 2 ? kv[2 % K] : 0u};
+              int ins;
+              const unsigned long long g = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k3, K, &ins,
+                                                             &p.acc->table_overflow);
+              uint32_t q = q0;
+              if (ins == 1) {
+                T.leaf_state[g] = (uint8_t)q0;
+                table_publish(T.leaf_slot, g, T.epoch);
+                atomicAdd(&p.acc->leaves, 1ull);
+              } else if (ins == 0) {
+                q = T.leaf_state[g];
+              }
+              w.lg[h] = (uint32_t)g;
+              w.linit[h] = ins == 0 ? (uint8_t)q : kNewLeaf;
+              w.lstate[h] = (uint8_t)q;
+              qs[r] = q;
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r) {  // append new leaves (warp-uniform count)
+          const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
+          if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
+          nleaf += __popc(nm);
+        }
+        bool old = false;
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
+        if (!__any_sync(0xffffffffu, old)) {
+#pragma unroll
+          for (int r = 0; r < kIlp; ++r)
+            if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[qs[r] * A + lb[base + 32 * r + lane]];
+        } else {
+          __syncwarp();
+#pragma unroll
+          for (int r = 0; r < kIlp; ++r) {
+            if (base + 32 * r >= cnt) break;
+            const bool act = slot[r] >= 0;
+            const uint32_t am = __ballot_sync(0xffffffffu, act);
+            if (act) {
+              const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
+              if ((peers & lanemask_lt()) == 0) {
+                uint32_t q = w.lstate[slot[r]];
+                uint32_t m = peers;
+                while (m) {
+                  const int i = __ffs(m) - 1;
+                  m &= m - 1;
+                  q = sdelta[q * A + lb[base + 32 * r + i]];
+                }
+                w.lstate[slot[r]] = (uint8_t)q;
+              }
+            }
+            __syncwarp();
+          }
+        }
+        __syncwarp();
+      }
+      // write back, verdict deltas, parent histogram deltas (lane-contiguous runs:
+      // a lane's leaves mostly share a parent, looked up once)
+      const uint32_t per = (nleaf + 31) >> 5;
+      const uint32_t i0 = min(nleaf, lane * per), i1 = min(nleaf, i0 + per);
+      long long pslot = -1;
+      bool pok = false;
+      uint32_t pk[kMaxLevels] = {0, 0, 0};
+      for (uint32_t i = i0; i < i1; ++i) {
+        const int s = w.llist[i];
+        const uint32_t qn = w.lstate[s], qi = w.linit[s];
+        T.leaf_state[w.lg[s]] = (uint8_t)qn;
+        int vo[NF], vn[NF];
+        bool any = false;
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+          vn[f] = slab[f * kMaxStates + qn];
+          vo[f] = qi == kNewLeaf ? -1 : (int)slab[f * kMaxStates + qi];
+          if (vo[f] != vn[f]) {
+            any = true;
+            if (vo[f] >= 0) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + vo[f]], -1);
+            atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + vn[f]], 1);
+          }
+        }
+        if (K > 1 && any) {
+          const int rep = (int)(w.ltag[s] & 0xFFFFu) - 1;
+          uint32_t k[kMaxLevels] = {0, 0, 0};
+          bool same = pslot >= 0;
+#pragma unroll
+          for (int x = 0; x < K - 1; ++x) {
+            k[x] = kb[x][rep];
+            same &= k[x] == pk[x];
+          }
+          if (!same) {
+            pslot = (long long)online_node(op, K - 1, k, &pok);
+#pragma unroll
+            for (int x = 0; x < K - 1; ++x) pk[x] = k[x];
+            if (pok) online_touch(op, K - 1, (unsigned long long)pslot);
+          }
+          if (pok) {
+            uint32_t *hist = T.node_hist[K - 1] + (unsigned long long)pslot * kMaxFormulas * 6;
+#pragma unroll
+            for (int f = 0; f < NF; ++f) {
+              if (vo[f] != vn[f]) {
+                if (vo[f] >= 0) atomicAdd(&hist[f * 6 + vo[f]], 0xFFFFFFFFu);
+                atomicAdd(&hist[f * 6 + vn[f]], 1u);
+              }
+            }
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
+    const int v = sacc[i];
+    if (v) atomicAdd(&p.acc->hist[0][0][0] + i, (unsigned long long)(long long)v);
+  }
+}
+
+// depth-l touched nodes: Def. 6 from the carried histogram; a changed verdict moves
+// one child of the parent (depth l-1), or of the root's histogram for l = 1
+template <int NF>
+__global__ void __launch_bounds__(256) online_nodes_kernel(OnlineParams op, int l) {
+  __shared__ int sacc[kMaxFormulas * 6];
+  const BucketParams &p = op.b;
+  const DevTables &T = p.tab;
+  const DevProg *prog = p.prog;
+  for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x) sacc[i] = 0;
+  __syncthreads();
+  const uint32_t n = op.tcnt[l];
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint32_t s = op.tlist[l][i];
+    const uint32_t *hist = T.node_hist[l] + (unsigned long long)s * kMaxFormulas * 6;
+    const uint32_t packed = T.node_verdict[l][s];
+    uint32_t np = packed;
+    int vo[NF], vn[NF];
+    bool any = false;
+#pragma unroll
+    for (int f = 0; f < NF; ++f) {
+      uint32_t h[6];
+#pragma unroll
+      for (int v = 0; v < 6; ++v) h[v] = hist[f * 6 + v];
+      vn[f] = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l], prog->qden[f][l], h);
+      const uint32_t o = (packed >> (8 * f)) & 0xFFu;
+      vo[f] = o == 0xFFu ? -1 : (int)o;
+      if (vo[f] != vn[f]) {
+        any = true;
+        if (vo[f] >= 0) atomicAdd(&sacc[f * 6 + vo[f]], -1);
+        atomicAdd(&sacc[f * 6 + vn[f]], 1);
+        np = (np & ~(0xFFu << (8 * f))) | ((uint32_t)vn[f] << (8 * f));
+      }
+    }
+    if (!any) continue;
+    T.node_verdict[l][s] = np;
+    if (l >= 2) {
+      const uint4 ks = T.node_slot[l][s];
+      const uint32_t k[kMaxLevels] = {ks.y, ks.z, ks.w};
+      bool ok;
+      const unsigned long long ps = online_node(op, l - 1, k, &ok);
+      if (!ok) continue;
+      online_touch(op, l - 1, ps);
+      uint32_t *ph = T.node_hist[l - 1] + ps * kMaxFormulas * 6;
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+        if (vo[f] != vn[f]) {
+          if (vo[f] >= 0) atomicAdd(&ph[f * 6 + vo[f]], 0xFFFFFFFFu);
+          atomicAdd(&ph[f * 6 + vn[f]], 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x) {
+    const int v = sacc[i];
+    if (v) atomicAdd(&p.acc->hist[i / 6][l][i % 6], (unsigned long long)(long long)v);
+  }
+}
+
 // ----------------------------------------------- rehash (online tables grow)
 __global__ void rehash_kernel(DevTables from, DevTables to, int nl, int nf, unsigned long long *overflow) {
   const unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1505,6 +1838,45 @@ cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t 
       LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<2><<<grid, kBucketThreads, sm, L.stream>>>(p));
     default: cudaFuncSetAttribute(bucket_global_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
+  }
+}
+
+template <int K, int NF>
+static cudaError_t online_leaf_launch(const OnlineParams &p, uint32_t grid, const Launcher &L) {
+  const size_t sm = p.b.warp_hdr + (size_t)p.b.warps_per_cta * sizeof(OnlineTab<K>);
+  cudaFuncSetAttribute(online_leaf_kernel<K, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKOnlineLeaf, online_leaf_kernel<K, NF><<<grid, 32 * p.b.warps_per_cta, sm, L.stream>>>(p));
+}
+
+cudaError_t launch_online_leaf(const OnlineParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
+  LTL4C_KNF(K, nf, online_leaf_launch, p, grid, L);
+}
+
+template <int K, int NF>
+static cudaError_t online_config_t(uint32_t hdr, int *cfg) {
+  int best = 0;
+  for (int w = 1; w <= 8; ++w) {
+    const size_t sm = hdr + (size_t)w * sizeof(OnlineTab<K>);
+    cudaError_t e = cudaFuncSetAttribute(online_leaf_kernel<K, NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    int n = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, online_leaf_kernel<K, NF>, 32 * w, sm);
+    if (e != cudaSuccess) return e;
+    if (n * w >= best && n > 0) { best = n * w; cfg[0] = w; cfg[1] = n; }
+  }
+  return best ? cudaSuccess : cudaErrorInvalidConfiguration;
+}
+
+cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg) {
+  LTL4C_KNF(K, nf, online_config_t, warp_hdr_bytes((uint32_t)nq, (uint32_t)na), cfg);
+}
+
+cudaError_t launch_online_nodes(const OnlineParams &p, int nf, int l, uint32_t grid, const Launcher &L) {
+  switch (nf) {
+    case 1: LTL4C_LAUNCH(kKOnlineNodes, online_nodes_kernel<1><<<grid, 256, 0, L.stream>>>(p, l));
+    case 2: LTL4C_LAUNCH(kKOnlineNodes, online_nodes_kernel<2><<<grid, 256, 0, L.stream>>>(p, l));
+    case 3: LTL4C_LAUNCH(kKOnlineNodes, online_nodes_kernel<3><<<grid, 256, 0, L.stream>>>(p, l));
+    default: LTL4C_LAUNCH(kKOnlineNodes, online_nodes_kernel<4><<<grid, 256, 0, L.stream>>>(p, l));
   }
 }
 

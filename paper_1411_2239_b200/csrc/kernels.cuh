@@ -37,6 +37,8 @@ struct PartPlan {
   unsigned long long n;                 // events in the batch
   uint32_t n_tiles;                     // ceil(n / kTileEv)
   int K, bits, passes;
+  int hk;                               // key column hashed for the bucket (0; K-1 in online mode)
+  const uint32_t *hcol[2];              // that column in buf_key[0] / buf_key[1]
   uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
@@ -112,6 +114,14 @@ struct BucketParams {
   DevTables tab;
 };
 
+// Online mode: the bucket parameters plus the per-batch touched-node lists.
+struct OnlineParams {
+  BucketParams b;
+  uint32_t bid;                         // batch id (!= 0), the touch mark of this batch
+  uint32_t *tlist[kMaxLevels];          // touched node slots per depth (capacity node_cap)
+  uint32_t *tcnt;                       // [kMaxLevels] entries in tlist (zeroed per batch)
+};
+
 // Everything the host reads back after a verify (one D2H copy).
 struct DevOut {
   DevResult res[kMaxFormulas];
@@ -139,6 +149,8 @@ enum KernelId {
   kKHeavy,
   kKUnitStart,
   kKBucketWarpBig,
+  kKOnlineLeaf,
+  kKOnlineNodes,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -156,6 +168,9 @@ cudaError_t bucket_warp_config(int K, int nf, int nq, int na, int *cfg);
 uint32_t bucket_warp_hdr(int nq, int na);  // CTA header bytes of the warp kernels
 cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L);
+cudaError_t launch_online_leaf(const OnlineParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+cudaError_t launch_online_nodes(const OnlineParams &p, int nf, int l, uint32_t grid, const Launcher &L);
+cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {warps/CTA, CTAs/SM}
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);

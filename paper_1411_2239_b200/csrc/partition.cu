@@ -28,7 +28,7 @@ constexpr int kRounds = kTileEv / kPartThreads;  // rounds of 32 events per warp
 
 // Digit counts of one tile (counts[d][tile]).  Pass 0 reads the batch and
 // applies the epsilon filter; later passes read k0 of the previous pass.
-template <int K, bool kFirst>
+template <int K, bool kFirst, bool kDeep>
 __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, int pass) {
   __shared__ uint32_t h[kMaxDigits];
   __shared__ uint32_t nv;
@@ -41,16 +41,25 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
   const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv;
   const uint32_t dmask = (1u << pl.width[pass]) - 1u;
   const int lo = pl.lo[pass];
-  uint32_t k0[kRounds];
+  uint32_t k0[kRounds];  // the hash key (column 0, or K-1 if kDeep; pass 0 also checks every guard key)
   bool ok[kRounds];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {  // all loads first (memory-level parallelism)
     const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
     ok[r] = j < n;
-    k0[r] = ok[r] ? in_key[0][j] : 0u;
-    if (kFirst) {
+    if (kFirst && kDeep) {
+      uint32_t kv[K];
+#pragma unroll
+      for (int i = 0; i < K; ++i) kv[i] = ok[r] ? in_key[i][j] : 0u;
+#pragma unroll
+      for (int i = 1; i < K; ++i) ok[r] &= kv[i] != kAbsent;
+      k0[r] = kv[0] == kAbsent ? kAbsent : kv[K - 1];  // (kv[0] absent: unbound, never counted)
+    } else if (kFirst) {
+      k0[r] = ok[r] ? in_key[0][j] : 0u;
 #pragma unroll
       for (int i = 1; i < K; ++i) ok[r] &= !(ok[r] && in_key[i][j] == kAbsent);
+    } else {
+      k0[r] = ok[r] ? pl.hcol[(pass - 1) & 1][j] : 0u;
     }
   }
   uint32_t myvalid = 0;
@@ -160,7 +169,7 @@ __device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
 // order (match masks of all rounds first, then the per-warp digit counters),
 // scatters them into shared memory in digit order together with their global
 // position, and the tile is written out digit run by digit run (coalesced).
-template <int K>
+template <int K, bool kDeep>
 __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
@@ -211,7 +220,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 #pragma unroll
     for (int k = 0; k < K; ++k) valid &= rk[r][k] != kAbsent;
     vd[r] = valid;
-    dg[r] = valid ? (salted_bucket(rk[r][0], pl.bits, pl.salt) >> lo) & dmask : 0u;
+    dg[r] = valid ? (salted_bucket(rk[r][kDeep ? K - 1 : 0], pl.bits, pl.salt) >> lo) & dmask : 0u;
   }
   if (pl.rank_ballot) {
 #pragma unroll
@@ -339,38 +348,45 @@ __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long lon
     return e_;                           \
   } while (0)
 
+template <int K, bool kDeep>
+static cudaError_t count_first(const PartPlan &p, int pass, const Launcher &L) {
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<K, true, kDeep><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+}
+
 cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
   if (pass == 0) {
+    const bool deep = p.hk != 0;
     switch (p.K) {
-      case 1: LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
-      case 2: LTL4C_LAUNCH(kKPartCount, part_count_kernel<2, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
-      default: LTL4C_LAUNCH(kKPartCount, part_count_kernel<3, true><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+      case 1: return count_first<1, false>(p, pass, L);
+      case 2: return deep ? count_first<2, true>(p, pass, L) : count_first<2, false>(p, pass, L);
+      default: return deep ? count_first<3, true>(p, pass, L) : count_first<3, false>(p, pass, L);
     }
   }
-  LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false, false><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
 }
 
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {
   LTL4C_LAUNCH(kKPartScan, part_scan_kernel<<<1u << p.width[pass], kScanThreads, 0, L.stream>>>(p, pass));
 }
 
-template <int K>
+template <int K, bool kDeep>
 static cudaError_t scatter(const PartPlan &p, int pass, const Launcher &L) {
   const size_t sm = sizeof(SweepSmem<K>);
-  cudaFuncSetAttribute(part_scatter_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
+  cudaFuncSetAttribute(part_scatter_kernel<K, kDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K, kDeep><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
 }
 
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) {
+  const bool deep = p.hk != 0;
   switch (p.K) {
-    case 1: return scatter<1>(p, pass, L);
-    case 2: return scatter<2>(p, pass, L);
-    default: return scatter<3>(p, pass, L);
+    case 1: return scatter<1, false>(p, pass, L);
+    case 2: return deep ? scatter<2, true>(p, pass, L) : scatter<2, false>(p, pass, L);
+    default: return deep ? scatter<3, true>(p, pass, L) : scatter<3, false>(p, pass, L);
   }
 }
 
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
-  const uint32_t *k0 = p.buf_key[(p.passes - 1) & 1][0];
+  const uint32_t *k0 = p.hcol[(p.passes - 1) & 1];
   const unsigned long long want = (p.n / kBoundsPer + 1 + 255) / 256;
   const unsigned grid = (unsigned)(want > 148 * 16 ? 148 * 16 : want);
   LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(k0, p.nvalid, p.bits, off, n_buckets));

@@ -165,6 +165,9 @@ struct ltl4c_state {
   DevBuf<uint32_t> totals, counts, bucket_off, oversize_list, medium_list, large_list, sched, unit_start;
   int n_sms = 148;
   int warp_cfg[4] = {4, 1, 1, 1};  // {warps/CTA, CTAs/SM} of the unit and the medium warp kernels
+  int online_cfg[2] = {4, 1};      // {warps/CTA, CTAs/SM} of online_leaf
+  uint32_t batch_id = 0;           // online: touch mark of the current batch
+  DevBuf<uint32_t> tlist[kMaxLevels], tcnt;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   Tables tab;
@@ -251,7 +254,7 @@ int ceil_log2(uint64_t x) {
 }
 
 ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_t node_cap, cudaStream_t s,
-                          bool aux = false) {
+                          bool aux = false, bool node_marks = false) {
   const int nl = (int)st->prog->n_levels;
   CU(t.leaf_slot.ensure(leaf_cap));
   CU(t.leaf_state.ensure(leaf_cap));
@@ -268,9 +271,10 @@ ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_
     CU(t.node_verdict[l].ensure(node_cap));
     CU(t.node_hist[l].ensure(node_cap * kMaxFormulas * 6));
     CU(cudaMemsetAsync(t.node_slot[l].p, 0, sizeof(uint4) * node_cap, s));
-    if (aux) {
+    if (aux || node_marks) {
       CU(t.node_aux[l].ensure(node_cap));
       t.d.node_aux[l] = t.node_aux[l].p;
+      if (node_marks) CU(cudaMemsetAsync(t.node_aux[l].p, 0, sizeof(uint32_t) * node_cap, s));
     }
     t.d.node_cap[l] = node_cap;
     t.d.node_slot[l] = t.node_slot[l].p;
@@ -300,13 +304,14 @@ ltl4c_status ensure_online_tables(ltl4c_state *st, uint64_t extra, cudaStream_t 
     if (ok) return LTL4C_OK;
   }
   if (fresh) {
-    ltl4c_status r = alloc_tables(st, t, want_leaf, want_node, s);
+    ltl4c_status r = alloc_tables(st, t, want_leaf, want_node, s, false, true);
     if (r) return r;
     t.d.epoch = st->epoch;
     return LTL4C_OK;
   }
   Tables nt;
-  ltl4c_status r = alloc_tables(st, nt, std::max<uint64_t>(want_leaf, t.d.leaf_cap), std::max<uint64_t>(want_node, t.d.node_cap[1]), s);
+  ltl4c_status r = alloc_tables(st, nt, std::max<uint64_t>(want_leaf, t.d.leaf_cap), std::max<uint64_t>(want_node, t.d.node_cap[1]), s,
+                                false, true);
   if (r) return r;
   nt.d.epoch = st->epoch;
   CU(launch_rehash(t.d, nt.d, (int)st->prog->n_levels, (int)st->prog->n_formulas,
@@ -460,6 +465,9 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.K = K;
     pl.bits = plan.B;
     pl.salt = kBucketSalt;
+    pl.hk = online ? K - 1 : 0;  // online: buckets by the deepest key (balanced leaves)
+    pl.hcol[0] = pl.buf_key[0][pl.hk];
+    pl.hcol[1] = pl.buf_key[1][pl.hk];
     pl.rank_ballot = rank_ballot();
     pl.passes = plan.P;
     int lo = 0;
@@ -499,7 +507,18 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       fp.list_len = &st->d_acc.p->large_buckets;
       CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
     } else {
-      CU(launch_bucket_global(bp, K, (int)prog->n_formulas, plan.NB, L));
+      // carried state: leaves (warp per unit), then touched nodes depth K-1 .. 1
+      OnlineParams op{};
+      op.b = bp;
+      op.b.warps_per_cta = st->online_cfg[0];
+      op.bid = st->batch_id;
+      for (int l = 1; l < K; ++l) op.tlist[l] = st->tlist[l].p;
+      op.tcnt = st->tcnt.p;
+      CU(cudaMemsetAsync(st->tcnt.p, 0, sizeof(uint32_t) * kMaxLevels, s));
+      CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
+      CU(launch_online_leaf(op, K, (int)prog->n_formulas, (uint32_t)(st->n_sms * st->online_cfg[1]), L));
+      for (int l = K - 1; l >= 1; --l)
+        CU(launch_online_nodes(op, (int)prog->n_formulas, l, (uint32_t)(st->n_sms * 8), L));
     }
   }
   if (finalize_now) {
@@ -544,6 +563,9 @@ ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_
     pl.bits = st->owner_bits;
     pl.passes = 1;
     pl.salt = kOwnerSalt;
+    pl.hk = 0;  // owner rank by level-0 key: whole subtrees per rank
+    pl.hcol[0] = pl.buf_key[0][0];
+    pl.hcol[1] = pl.buf_key[1][0];
     pl.rank_ballot = rank_ballot();
     pl.lo[0] = 0;
     pl.width[0] = st->owner_bits;
@@ -627,6 +649,9 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   if (online) {
     ltl4c_status r = ensure_online_tables(st, N, s, L);
     if (r) return r;
+    for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
+    CU(st->tcnt.ensure(kMaxLevels));
+    if (++st->batch_id == 0) st->batch_id = 1;  // wrap: marks of batch 0 never exist
   }
   const bool comm = st->comm && (st->n_ranks > 1 || st->force_exchange);
   uint64_t Nloc = N;
@@ -858,6 +883,9 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
     // most warps resident for this program's (K, F) shared-memory plan
     cudaError_t e = bucket_warp_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states,
                                        (int)prog->n_atoms, st->warp_cfg);
+    if (e == cudaSuccess)
+      e = online_leaf_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states, (int)prog->n_atoms,
+                             st->online_cfg);
     if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
   }
   cudaSetDevice(prev);
@@ -960,6 +988,8 @@ void ltl4c_state_free(ltl4c_state *st) {
   for (int l = 0; l < kMaxLevels; ++l) st->hkeys[l].release();
   st->hlet.release();
   st->tab.release();
+  for (int l = 0; l < kMaxLevels; ++l) st->tlist[l].release();
+  st->tcnt.release();
   st->h_part.release();
   st->h_lists.release();
   st->h_u32.release();
