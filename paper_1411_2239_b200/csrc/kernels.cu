@@ -18,10 +18,14 @@
 //           warp per long slice (ordered composition of transition maps)
 //        a5 ApplyQuantifiers: level by level, group children by parent prefix
 //           (P), histogram B, rule Def. 6
-//  bucket_global
-//      same steps in chunks of kCap events with carried leaf / node tables in
-//      global memory and delta propagation (online mode P:943, and buckets
-//      larger than one chunk).
+//  bucket_warp / bucket_warp_big
+//      warp per work unit (runs of consecutive buckets) with warp-private
+//      shared-memory tables; the CTA path above takes what does not fit.
+//  heavy
+//      oversized buckets: segmented transition-map scan through global tables.
+//  online_leaf / online_nodes
+//      online mode: carried global tables, verdict deltas propagated
+//      level by level through touched nodes.
 //  finalize
 //      root verdict from the depth-1 histogram, result record.
 #include <cuda_runtime.h>
@@ -34,7 +38,7 @@
 namespace ltl4c {
 
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
-                                                "bucket_warp", "bucket_fast", "bucket_global",
+                                                "bucket_warp", "bucket_fast",
                                                 "finalize", "rehash", "heavy", "unit_start",
                                                 "bucket_warp_big", "online_leaf", "online_nodes"};
 
@@ -828,134 +832,6 @@ __device__ unsigned long long table_find_insert(uint4 *slots, unsigned long long
 __device__ __forceinline__ void table_publish(uint4 *slots, unsigned long long slot, uint32_t epoch) {
   __threadfence();
   st_release(&slots[slot].x, (epoch << 1) | 1u);
-}
-
-// ----------------------------------------------- global path (online / oversize)
-template <int K>
-__global__ void __launch_bounds__(kBucketThreads) bucket_global_kernel(BucketParams p) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  uint32_t b;
-  if (p.list) {
-    if (blockIdx.x >= *p.list_len) return;
-    b = p.list[blockIdx.x];
-  } else {
-    b = blockIdx.x;
-  }
-  const uint32_t start = p.bucket_off[b], total = p.bucket_off[b + 1] - start;
-  if (total == 0) return;
-  const DevProg *prog = p.prog;
-  const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
-  const Smem s = carve(smem_raw, K, nf, 1);
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const DevTables &T = p.tab;
-  load_prog(s, prog);
-  __syncthreads();
-  for (uint32_t off = 0; off < total; off += kCap) {
-    const int n = load_chunk<K>(s, p, start + off, (int)min((uint32_t)kCap, total - off));
-    const int L = dedup<K>(s, n, K);
-    group_by_class(s, n, L);
-    order_segments(s, n, L);
-    // carried leaf state (merged submonitors)
-    for (int c = tid; c < L; c += nt) {
-      uint32_t k[kMaxLevels] = {0, 0, 0};
-      for (int i = 0; i < K; ++i) k[i] = s.key[i][s.rep[c]];
-      int ins;
-      const unsigned long long slot =
-          table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &p.acc->table_overflow);
-      s.cur[c] = (uint32_t)slot;  // slot index (cap <= 2^32)
-      if (ins == 1) {
-        // publish at once (state = q0): a thread of this CTA probing the slot
-        // must never wait across the barriers below
-        T.leaf_state[slot] = (uint8_t)prog->q0;
-        table_publish(T.leaf_slot, slot, T.epoch);
-        s.state[c] = (uint8_t)prog->q0;
-        for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = 0xFF;
-        atomicAdd(&p.acc->leaves, 1ull);
-      } else {
-        const uint8_t q = ins == 0 ? T.leaf_state[slot] : (uint8_t)prog->q0;
-        s.state[c] = q;
-        for (int f = 0; f < nf; ++f) s.ov[f * kCap + c] = ins == 0 ? s.lab[f * kMaxStates + q] : 0xFF;
-      }
-      s.owner[c] = (uint16_t)(ins < 0 ? 2 : 0);
-    }
-    __syncthreads();
-    step_leaves(s, L, nq, A);
-    for (int c = tid; c < L; c += nt) {
-      const unsigned long long slot = s.cur[c];
-      if (s.owner[c] != 2) T.leaf_state[slot] = s.state[c];
-      s.item_rep[c] = s.rep[c];
-      for (int f = 0; f < nf; ++f) {
-        const uint8_t v = s.lab[f * kMaxStates + s.state[c]], o = s.ov[f * kCap + c];
-        s.iv[f * kCap + c] = v;
-        if (o != v) {
-          if (o != 0xFF) atomicAdd(&s.acc[acc_idx(f, nl, o)], -1);
-          atomicAdd(&s.acc[acc_idx(f, nl, v)], 1);
-        }
-      }
-    }
-    __syncthreads();
-    // delta propagation up the tree: depth nl-1 .. 1
-    int items = L;
-    for (int l = nl - 1; l >= 1; --l) {
-      const int C = dedup<K>(s, items, l);
-      group_by_class(s, items, C);
-      for (int x = tid; x < C; x += nt) {
-        uint32_t k[kMaxLevels] = {0, 0, 0};
-        for (int i = 0; i < l; ++i) k[i] = s.key[i][s.rep[x]];
-        int ins;
-        const unsigned long long slot = table_find_insert(T.node_slot[l], T.node_cap[l], T.epoch, k, l,
-                                                          &ins, &p.acc->table_overflow);
-        uint32_t *hist = T.node_hist[l] + slot * (kMaxFormulas * 6);
-        uint32_t packed = 0xFFFFFFFFu;
-        if (ins == 1) {
-          for (int i = 0; i < kMaxFormulas * 6; ++i) hist[i] = 0;
-          T.node_verdict[l][slot] = 0xFFFFFFFFu;
-          table_publish(T.node_slot[l], slot, T.epoch);
-          atomicAdd(&p.acc->nodes[l], 1ull);
-        } else if (ins == 0) {
-          packed = T.node_verdict[l][slot];
-        }
-        uint32_t newpacked = 0xFFFFFFFFu;
-        const int a = s.scan[x], e = s.scan[x + 1];
-        for (int f = 0; f < nf; ++f) {
-          uint32_t h[6];
-          for (int v = 0; v < 6; ++v) h[v] = ins >= 0 ? hist[f * 6 + v] : 0;
-          for (int i = a; i < e; ++i) {
-            const int it = s.perm[i];
-            const uint8_t o = s.ov[f * kCap + it], v = s.iv[f * kCap + it];
-            if (o != v) {
-              if (o != 0xFF) h[o] -= 1;
-              h[v] += 1;
-            }
-          }
-          if (ins >= 0)
-            for (int v = 0; v < 6; ++v) hist[f * 6 + v] = h[v];
-          const int nvv = node_verdict(prog->qkind[f][l], prog->qcmp[f][l], prog->qnum[f][l],
-                                       prog->qden[f][l], h);
-          const uint8_t old = (uint8_t)((packed >> (8 * f)) & 0xFF);
-          s.nov[f * kCap + x] = old;
-          s.nv[f * kCap + x] = (uint8_t)nvv;
-          newpacked = (newpacked & ~(0xFFu << (8 * f))) | ((uint32_t)nvv << (8 * f));
-          if (old != nvv) {
-            if (old != 0xFF) atomicAdd(&s.acc[acc_idx(f, l, old)], -1);
-            atomicAdd(&s.acc[acc_idx(f, l, nvv)], 1);
-          }
-        }
-        if (ins >= 0) T.node_verdict[l][slot] = newpacked;
-      }
-      __syncthreads();
-      for (int x = tid; x < C; x += nt) {
-        s.item_rep[x] = s.rep[x];
-        for (int f = 0; f < nf; ++f) {
-          s.iv[f * kCap + x] = s.nv[f * kCap + x];
-          s.ov[f * kCap + x] = s.nov[f * kCap + x];
-        }
-      }
-      __syncthreads();
-      items = C;
-    }
-  }
-  flush_acc(s, p.acc, nf, nl);
 }
 
 // ----------------------------------------------- online path (carried state)
@@ -1828,18 +1704,6 @@ cudaError_t bucket_warp_config(int K, int nf, int nq, int na, int *cfg) {
 }
 
 uint32_t bucket_warp_hdr(int nq, int na) { return warp_hdr_bytes((uint32_t)nq, (uint32_t)na); }
-
-cudaError_t launch_bucket_global(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
-  const size_t sm = smem_bytes(K, nf, 1);
-  switch (K) {
-    case 1: cudaFuncSetAttribute(bucket_global_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
-    case 2: cudaFuncSetAttribute(bucket_global_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<2><<<grid, kBucketThreads, sm, L.stream>>>(p));
-    default: cudaFuncSetAttribute(bucket_global_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketGlobal, bucket_global_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
-  }
-}
 
 template <int K, int NF>
 static cudaError_t online_leaf_launch(const OnlineParams &p, uint32_t grid, const Launcher &L) {

@@ -2,11 +2,12 @@
 //
 // One ltl4c_verify = Algorithm 1 of arXiv:1411.2239 on a batch:
 //   SortTrace       -> P stable LSD passes (part_count, part_scan, part_scatter)
-//                      + bucket_scan                      (a1, a2)
+//                      + bucket_bounds (mu) + unit_start          (a1, a2)
 //   SpawnMonitors,
 //   Distribute,
-//   ApplyQuantifiers -> bucket_fast (offline) / bucket_global (online, or
-//                      buckets larger than one shared-memory chunk)  (a3-a5)
+//   ApplyQuantifiers -> offline: bucket_warp -> bucket_warp_big -> bucket_fast
+//                      -> heavy (each takes what the previous one spills);
+//                      online: online_leaf + online_nodes per level  (a3-a5)
 //   return           -> finalize + one <= 1 KB D2H copy              (a6)
 #include <cuda_runtime.h>
 #include <dlfcn.h>
