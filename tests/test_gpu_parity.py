@@ -295,3 +295,64 @@ def test_online_host_buffers(env):
         got = st.verify_host([x[lo:hi] for x in tr.keys], tr.letters[lo:hi], first_index=lo)[0]
         want = oracle.run_offline(tr.formula, [x[:hi] for x in tr.keys], tr.letters[:hi])
         _assert_same(got, want, hi)
+
+
+def test_forced_spill_chain():
+    """Few, large buckets (bucket bits capped through LTL4C_MAX_BITS in a fresh
+    process) route work through every spill tier: warp unit -> warp big ->
+    CTA bucket -> heavy path, for K = 1, 2 and 3."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+import oracle, tracegen, paper_1411_2239_b200 as ltl4c
+dev = torch.device("cuda:0")
+def proj(letters, prog_atoms, prop_atoms):
+    out = np.zeros_like(letters)
+    for j, a in enumerate(prop_atoms):
+        out |= ((letters >> prog_atoms.index(a)) & 1) << j
+    return out
+cases = [tracegen.login_trace(seed=21, n=300_000, users=3000, rid_events=2, p_unauth=0.05),
+         tracegen.proxy_trace(seed=22, n=300_000, videos=20_000),
+         tracegen.zipf_socket_trace(seed=23, n=300_000, support=1 << 12)]
+for tr in cases:
+    st = ltl4c.compile(tr.formula).state(0)
+    k = [torch.from_numpy(x.view(np.int32)).to(dev) for x in tr.keys]
+    got = st.verify(k, torch.from_numpy(tr.letters).to(dev))[0]
+    want = oracle.run_offline(tr.formula, tr.keys, tr.letters)
+    assert got.verdict == want["verdict"] and np.array_equal(got.hist, want["hist"]), (tr.meta, got.hist, want["hist"])
+tr = tracegen.c5_trace(seed=24, n=200_000, users=3000, hosts=64, span_events=50_000)
+prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+k = [torch.from_numpy(x.view(np.int32)).to(dev) for x in tr.keys]
+got = prog.state(0).verify(k, torch.from_numpy(tr.letters).to(dev))
+for f, text in enumerate(tracegen.C5_FORMULAS):
+    p = oracle.Property(text)
+    want = oracle.run_offline(text, tr.keys, proj(tr.letters, prog.atoms, p.atoms))
+    assert got[f].verdict == want["verdict"] and np.array_equal(got[f].hist, want["hist"]), (f, got[f].hist, want["hist"])
+print("ok")
+'''
+    root = os.path.dirname(os.path.dirname(__file__))
+    for bits in ("4", "7", "10"):
+        env_ = dict(os.environ, LTL4C_MAX_BITS=bits)
+        r = subprocess.run([sys.executable, "-c", code], env=env_, capture_output=True, text=True, timeout=600,
+                           cwd=root)
+        assert r.returncode == 0 and "ok" in r.stdout, (bits, r.stdout + r.stderr)
+
+
+def test_online_table_growth(env):
+    """Online batches whose distinct leaves outgrow the first carried tables: the
+    tables are rehashed into larger ones between batches and nothing is lost."""
+    ltl4c, torch, dev = env
+    n, b = 1_500_000, 250_000
+    tr = tracegen.login_trace(seed=31, n=n, users=3000, p_unauth=0.02)
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    st.profile(True)
+    for lo in range(0, n, b):
+        hi = min(n, lo + b)
+        k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+        got = st.verify(k, l, first_index=lo)[0]
+        if hi in (2 * b, n):
+            _assert_same(got, oracle.run_offline(tr.formula, [x[:hi] for x in tr.keys], tr.letters[:hi]), hi)
+    assert st.stats()["kernels"]["rehash"]["launches"] >= 1
