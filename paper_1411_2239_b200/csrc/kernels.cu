@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 #ifndef LTL4C_ILP
 #define LTL4C_ILP 4
 #endif
+#ifndef LTL4C_STATIC_UNITS
+#define LTL4C_STATIC_UNITS 0
+#endif
 #ifndef LTL4C_LS_MUL
 #define LTL4C_LS_MUL 2
 #endif
@@ -515,8 +518,15 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     if (listed) { lo = p.list[u]; hi = lo + 1; }
     else { lo = p.unit_start[u]; hi = p.unit_start[u + 1]; }
   };
-  uint32_t nraw = 0;
-  if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+#if LTL4C_STATIC_UNITS
+  // static round-robin over the warps of the grid (units are balanced by construction)
+  uint32_t snext = blockIdx.x * (blockDim.x >> 5) + wid;
+  const uint32_t sstep = gridDim.x * (blockDim.x >> 5);
+  auto take = [&]() { const uint32_t u = snext; snext += sstep; return u; };
+#else
+  auto take = [&]() { uint32_t u = 0; if (lane == 0) u = atomicAdd(p.bucket_counter, 1u); return u; };
+#endif
+  uint32_t nraw = take();
   uint32_t cu = __shfl_sync(0xffffffffu, nraw, 0);
   uint32_t cbl = 0, cbh = 0, cs0 = 0, cs1 = 0;
   if (cu < n_items) {
@@ -524,13 +534,13 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
     cs0 = p.bucket_off[cbl];
     cs1 = p.bucket_off[cbh];
   }
-  if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+  nraw = take();
   uint32_t ep = 0;
   while (cu < n_items) {
     const uint32_t nu = __shfl_sync(0xffffffffu, nraw, 0);
     uint32_t nbl = 0, nbh = 0, ns0 = 0, ns1 = 0;
     if (nu < n_items) item(nu, nbl, nbh);
-    if (lane == 0) nraw = atomicAdd(p.bucket_counter, 1u);
+    nraw = take();
     bool nres = false;
     auto resolve_next = [&]() {   // next unit's event range + L2 prefetch of its bytes
       if (nres) return;
@@ -772,16 +782,29 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
 
 // ----------------------------------------------- work units for bucket_warp
 // unit u = buckets [unit_start[u], unit_start[u+1]): the buckets whose first event
-// lies in [u * kUnitTarget, (u + 1) * kUnitTarget).  Thread per bucket c: the
-// units whose boundary u * kUnitTarget lies in (off[c-1], off[c]] start at c
-// (c = nb, the end: every remaining unit).
+// lies in [u * kUnitTarget, (u + 1) * kUnitTarget).  Lane per bucket c: the units
+// whose boundary u * kUnitTarget lies in (off[c-1], off[c]] start at c (c = nb,
+// the end: every remaining unit); the warp writes each lane's range together
+// (a skewed bucket can own thousands of unit boundaries).
 __global__ void unit_start_kernel(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units) {
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > nb) return;
-  if (c == 0) { ustart[0] = 0; return; }
-  const uint32_t u0 = off[c - 1] / kUnitTarget + 1;
-  const uint32_t u1 = c == nb ? n_units : min(n_units, off[c] / kUnitTarget);
-  for (uint32_t u = u0; u <= u1; ++u) ustart[u] = c;
+  const int lane = threadIdx.x & 31;
+  uint32_t u0 = 1, u1 = 0;  // empty
+  if (c <= nb) {
+    if (c == 0) { u0 = 0; u1 = 0; }
+    else {
+      u0 = off[c - 1] / kUnitTarget + 1;
+      u1 = c == nb ? n_units : min(n_units, off[c] / kUnitTarget);
+    }
+  }
+  uint32_t todo = __ballot_sync(0xffffffffu, u0 <= u1);
+  while (todo) {
+    const int l = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const uint32_t a = __shfl_sync(0xffffffffu, u0, l), b = __shfl_sync(0xffffffffu, u1, l);
+    const uint32_t cc = __shfl_sync(0xffffffffu, c, l);
+    for (uint32_t u = a + lane; u <= b; u += 32) ustart[u] = cc;
+  }
 }
 
 // ----------------------------------------------- global tables
@@ -1211,7 +1234,7 @@ __global__ void __launch_bounds__(1024) heavy_plan_kernel(HeavyParams h) {
     uint32_t v = 0;
     if (i < L) {
       const uint32_t b = h.list[i];
-      v = (h.bucket_off[b + 1] - h.bucket_off[b] + kCap - 1) / kCap;
+      v = (h.bucket_off[b + 1] - h.bucket_off[b] + h.seg_events - 1) / h.seg_events;
     }
     buf[threadIdx.x] = v;
     __syncthreads();
@@ -1261,7 +1284,7 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
     const uint32_t j = item - h.seg_base[i];
     const uint32_t boff = h.bucket_off[b], bcnt = h.bucket_off[b + 1] - boff;
     const uint32_t start = boff + j * kCap;
-    const int n = (int)min((uint32_t)kCap, bcnt - j * kCap);
+    const int n = (int)min((uint32_t)kCap, bcnt - j * kCap);  // (seg_events == kCap here)
     load_chunk<K>(s, bp, start, n);
     const int C = dedup<K>(s, n, K);
     group_by_class(s, n, C);
@@ -1305,6 +1328,195 @@ __global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h
       const unsigned long long m = s.lmap[c];
       h.part[pbase + c] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
     }
+  }
+}
+
+// H1 (warp form): segments of kSegW events, one warp each.  The segment is
+// staged into warp-private shared memory; its value vectors are deduplicated in
+// an epoch-tagged warp table; every leaf's transition maps are composed in trace
+// order (a window whose slots are all new and touched once takes the letter's
+// map; otherwise lanes sharing a slot are grouped and the leader composes in
+// lane order); one partial {dense leaf, segment, map} per leaf of the segment.
+constexpr int kSegW = 256;
+
+template <int K>
+struct alignas(16) SegTab {
+  static constexpr int LS = 2 * kSegW;
+  uint32_t key[K][kSegW + 4];
+  uint8_t let[kSegW + 32];
+  uint32_t ltag[LS];
+  unsigned long long lmap[LS];
+  uint16_t llist[kSegW];
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
+  using Tab = SegTab<K>;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  unsigned long long *smap = reinterpret_cast<unsigned long long *>(smem_raw);  // [256]
+  const DevProg *prog = h.prog;
+  const int nq = prog->nq, A = 1 << prog->na;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tab &w = reinterpret_cast<Tab *>(smem_raw + 8 * kMaxLetters)[wid];
+  for (int i = threadIdx.x; i < A; i += blockDim.x) smap[i] = prog->map[i];
+  for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+  __syncthreads();
+  const DevTables &T = h.tab;
+  unsigned long long ident = 0;
+  for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
+  const uint32_t L = (uint32_t)*h.list_len;
+  const uint32_t n_items = h.ctr[1];
+  uint32_t ep = 0;
+  while (true) {
+    uint32_t item = 0;
+    if (lane == 0) item = atomicAdd(&h.ctr[0], 1u);
+    item = __shfl_sync(0xffffffffu, item, 0);
+    if (item >= n_items) break;
+    // bucket of the item: last i with seg_base[i] <= item
+    uint32_t lo = 0, hi = L;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (h.seg_base[mid] <= item) lo = mid; else hi = mid;
+    }
+    const uint32_t b = h.list[lo];
+    const uint32_t j = item - h.seg_base[lo];
+    const uint32_t boff = h.bucket_off[b], bcnt = h.bucket_off[b + 1] - boff;
+    const uint32_t start = boff + j * kSegW;
+    const uint32_t cnt = min((uint32_t)kSegW, bcnt - j * kSegW);
+    if (++ep == 0x10000u) {
+      for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+      ep = 1;
+    }
+    const uint32_t koff = start & 3u, loff = start & 15u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const uint32_t *g = h.key[k] + (start - koff);
+      for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
+    }
+    {
+      const uint8_t *g = h.let + (start - loff);
+      for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    const uint32_t *kb[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
+    const uint8_t *lb = &w.let[loff];
+    uint32_t nleaf = 0;
+    for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
+      int slot[kIlp];
+      bool fresh[kIlp];
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r) {
+        const int e = (int)(base + 32 * r + lane);
+        slot[r] = -1;
+        fresh[r] = false;
+        if (e < (int)cnt) {
+          uint32_t kv[K];
+#pragma unroll
+          for (int i = 0; i < K; ++i) kv[i] = kb[i][e];
+          constexpr int shift = 32 - __builtin_ctz((unsigned)Tab::LS);
+          uint32_t hh = key_hash<K>(kv, K) >> shift;
+          volatile uint32_t *vt = w.ltag;
+          while (true) {
+            uint32_t t = vt[hh];
+            if ((t >> 16) != ep) {
+              const uint32_t o = atomicCAS(&w.ltag[hh], t, ep << 16 | (uint32_t)(e + 1));
+              if (o == t) { fresh[r] = true; break; }
+              t = o;
+            }
+            const int rep = (int)(t & 0xFFFFu) - 1;
+            bool eq = true;
+#pragma unroll
+            for (int i = 0; i < K; ++i) eq &= kb[i][rep] == kv[i];
+            if (eq) break;
+            hh = (hh + 1) & (uint32_t)(Tab::LS - 1);
+          }
+          slot[r] = (int)hh;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r) {
+        const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
+        if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
+        nleaf += __popc(nm);
+      }
+      bool old = false;
+#pragma unroll
+      for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
+      if (!__any_sync(0xffffffffu, old)) {
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r)
+          if (slot[r] >= 0) w.lmap[slot[r]] = smap[lb[base + 32 * r + lane]];
+      } else {
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r)
+          if (fresh[r]) w.lmap[slot[r]] = ident;
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < kIlp; ++r) {
+          if (base + 32 * r >= cnt) break;
+          const bool act = slot[r] >= 0;
+          const int s0 = __shfl_sync(0xffffffffu, slot[r], 0);
+          if (__all_sync(0xffffffffu, !act || slot[r] == s0)) {
+            // one leaf in the whole round (a skewed key): ordered tree composition
+            // of the 32 lanes' maps (lane order = trace order), 5 steps
+            unsigned long long m = act ? smap[lb[base + 32 * r + lane]] : ident;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const unsigned long long o = __shfl_down_sync(0xffffffffu, m, d);
+              if ((lane & (2 * d - 1)) == 0) m = map_apply(o, m, nq);
+            }
+            if (lane == 0) w.lmap[s0] = map_apply(m, w.lmap[s0], nq);
+          } else {
+            const uint32_t am = __ballot_sync(0xffffffffu, act);
+            if (act) {
+              const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
+              if ((peers & lanemask_lt()) == 0) {
+                unsigned long long m = w.lmap[slot[r]];
+                uint32_t pm = peers;
+                while (pm) {
+                  const int i = __ffs(pm) - 1;
+                  pm &= pm - 1;
+                  m = map_apply(smap[lb[base + 32 * r + i]], m, nq);
+                }
+                w.lmap[slot[r]] = m;
+              }
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncwarp();
+    }
+    // one partial per leaf of the segment
+    unsigned long long pbase = 0;
+    if (lane == 0) pbase = atomicAdd(h.n_part, (unsigned long long)nleaf);
+    pbase = __shfl_sync(0xffffffffu, pbase, 0);
+    for (uint32_t i = lane; i < nleaf; i += 32) {
+      const int s = w.llist[i];
+      const int rep = (int)(w.ltag[s] & 0xFFFFu) - 1;
+      uint32_t k[kMaxLevels] = {0, 0, 0};
+#pragma unroll
+      for (int x = 0; x < K; ++x) k[x] = kb[x][rep];
+      int ins;
+      const unsigned long long slot = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &h.acc->table_overflow);
+      if (ins < 0) { h.part[pbase + i] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u); continue; }
+      uint32_t dense;
+      if (ins == 1) {
+        dense = (uint32_t)atomicAdd(h.n_leaves, 1ull);
+        T.leaf_aux[slot] = dense;
+        h.leaf_slot_of[dense] = (uint32_t)slot;
+        table_publish(T.leaf_slot, slot, T.epoch);
+      } else {
+        dense = *(volatile uint32_t *)&T.leaf_aux[slot];
+      }
+      atomicAdd(&h.leaf_npart[dense], 1u);
+      const unsigned long long m = w.lmap[s];
+      h.part[pbase + i] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
+    }
+    __syncwarp();
   }
 }
 
@@ -1757,9 +1969,17 @@ template <int K>
 static cudaError_t heavy_all(const HeavyParams &h, int nf, int n_sms, const Launcher &L) {
   if (L.before) L.before(L.ctx, kKHeavy);
   heavy_plan_kernel<<<1, 1024, 0, L.stream>>>(h);
-  const size_t sm = smem_bytes(K, nf, 2);
-  cudaFuncSetAttribute(heavy_seg_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  heavy_seg_kernel<K><<<2 * n_sms, kBucketThreads, sm, L.stream>>>(h);
+  if (h.seg_events == kSegW) {
+    const size_t sm = 8 * kMaxLetters + 8 * sizeof(SegTab<K>);
+    cudaFuncSetAttribute(heavy_segw_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy_segw_kernel<K>, 256, sm);
+    heavy_segw_kernel<K><<<n_sms * (per_sm > 0 ? per_sm : 1), 256, sm, L.stream>>>(h);
+  } else {
+    const size_t sm = smem_bytes(K, nf, 2);
+    cudaFuncSetAttribute(heavy_seg_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    heavy_seg_kernel<K><<<2 * n_sms, kBucketThreads, sm, L.stream>>>(h);
+  }
   heavy_scan_blocks<<<2 * n_sms, 1024, 0, L.stream>>>(h);
   heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h);
   heavy_scan_add<<<2 * n_sms, 1024, 0, L.stream>>>(h);

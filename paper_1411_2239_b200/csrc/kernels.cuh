@@ -91,6 +91,7 @@ struct HeavyParams {
   unsigned long long *n_nodes;          // [kMaxLevels]
   uint32_t *scan_tmp;                   // block sums of the leaf_npart scan
   unsigned long long cap_leaves;        // upper bound of dense leaves (host)
+  uint32_t seg_events;                  // events per segment: 256 (warp segments) or kCap (CTA segments)
 };
 
 struct BucketParams {
