@@ -9,4 +9,11 @@ for spec in $SPECS; do
   echo "== $spec" >> gpurun_out/sweep.log
   env $lib ${e//,/ } timeout 300 python bench.py --no-cpu-baseline --config ${CFG:-C2} --steps 10 >> gpurun_out/sweep.log 2>&1
 done
-python scripts/show_exp.py gpurun_out/sweep.log
+python - <<"PY"
+import json
+for l in open("gpurun_out/sweep.log"):
+    if l.startswith("=="): print(l.strip())
+    elif l.startswith("{"):
+        d = json.loads(l); print(" ms %.4f" % d["ms_per_step"], {k: round(v, 3) for k, v in d["roofline"]["kernel_share"].items()})
+    elif "rror" in l: print(l[:300])
+PY
