@@ -405,8 +405,8 @@ struct alignas(16) WarpTab {
   uint8_t let[CAP + 32];                // staged letters; event i at [i + (start & 15)]
   uint32_t ltag[LS];                    // epoch << 16 | rep event + 1 (other epochs = empty)
   uint8_t lnode[K > 1 ? LS : 1];        // depth-(K-1) ancestor slot of the leaf
-  uint8_t lstate[LS];
-  uint16_t llist[CAP];                  // leaf slots in creation order
+  uint8_t lstate[LS];                   // state | 0x80 once the leaf's verdict is counted
+  int pleaf[NF * 6];                    // pending leaf-verdict deltas of the unit (replayed windows)
   uint32_t ntag[NL][NS];                // as ltag
   uint32_t nhist[NL][NS][NF * 3];       // two u16 counters per word: h[2x] | h[2x+1] << 16
   uint16_t nlist[NL][NS];
@@ -488,6 +488,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) sacc[i] = 0;
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
   for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
+  for (int i = lane; i < NF * 6; i += 32) w.pleaf[i] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
   const uint32_t node_limit = Tab::NSL / 2;
@@ -592,20 +593,42 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
 #pragma unroll
         for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
         const uint8_t *lb = &w.let[loff];
-        // a3 + a4 over windows of 32 x kIlp events
-        uint32_t nleaf = 0;
+        // a3 + a4 over windows of 32 x kIlp events; verdicts are counted as they
+        // change (a new leaf adds its verdict, a replayed leaf moves old -> new):
+        // per-lane pending counts (pl) and child counts of the lane's current
+        // ancestor (hv, flushed when the ancestor changes) -- committed only if the
+        // unit does not overflow the node tables
         bool ovf = false;
         int cslot = -1;                 // per-lane cache: deepest ancestor of the last new leaf
         uint32_t ck[K > 1 ? K - 1 : 1];
 #pragma unroll
         for (int i = 0; i < (K > 1 ? K - 1 : 1); ++i) ck[i] = 0;
+        int cur = -1;
+        unsigned long long hv[NF], pl[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) hv[f] = pl[f] = 0;
+        auto flush_hv = [&]() {
+#pragma unroll
+          for (int f = 0; f < NF; ++f) {
+            if (hv[f] && cur >= 0) {
+              uint32_t *hw = w.nhist[K > 1 ? K - 2 : 0][cur] + f * 3;
+              const uint32_t f0 = (uint32_t)hv[f] & 0xFFFFu, f1 = (uint32_t)(hv[f] >> 16) & 0xFFFFu;
+              const uint32_t f2 = (uint32_t)(hv[f] >> 32) & 0xFFFFu, f3 = (uint32_t)(hv[f] >> 48);
+              if (f0) atomicAdd(&hw[0], f0);
+              if (f1 | f2) atomicAdd(&hw[1], f1 | f2 << 16);
+              if (f3) atomicAdd(&hw[2], f3 << 16);
+            }
+            hv[f] = 0;
+          }
+        };
         for (uint32_t base = 0; base < cnt; base += 32 * kIlp) {
-          int slot[kIlp];
+          int slot[kIlp], par[kIlp];
           bool fresh[kIlp];
 #pragma unroll
           for (int r = 0; r < kIlp; ++r) {
             const int e = (int)(base + 32 * r + lane);
             slot[r] = -1;
+            par[r] = -1;
             fresh[r] = false;
             if (e < (int)cnt) {
               uint32_t kv[K];
@@ -649,23 +672,30 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
                   for (int i = 0; i < K - 1; ++i) ck[i] = kv[i];
                 }
                 if (!ovf) w.lnode[h] = (uint8_t)cslot;
+                par[r] = ovf ? -1 : cslot;
               }
             }
-          }
-#pragma unroll
-          for (int r = 0; r < kIlp; ++r) {  // append new leaves (warp-uniform count)
-            const uint32_t nm = __ballot_sync(0xffffffffu, fresh[r]);
-            if (fresh[r]) w.llist[nleaf + __popc(nm & lanemask_lt())] = (uint16_t)slot[r];
-            nleaf += __popc(nm);
           }
           bool old = false;
 #pragma unroll
           for (int r = 0; r < kIlp; ++r) old |= slot[r] >= 0 && !fresh[r];
           if (!__any_sync(0xffffffffu, old)) {
-            // every touched slot is new and touched once: one step from q0
+            // every touched slot is new and touched once: one step from q0, and the
+            // leaf's verdict is counted
 #pragma unroll
-            for (int r = 0; r < kIlp; ++r)
-              if (slot[r] >= 0) w.lstate[slot[r]] = sdelta[q0 * A + lb[base + 32 * r + lane]];
+            for (int r = 0; r < kIlp; ++r) {
+              if (slot[r] < 0) continue;
+              const uint32_t q1 = sdelta[q0 * A + lb[base + 32 * r + lane]];
+              w.lstate[slot[r]] = (uint8_t)(q1 | 0x80u);
+              if (K > 1 && par[r] != cur) { flush_hv(); cur = par[r]; }
+#pragma unroll
+              for (int f = 0; f < NF; ++f) {
+                const int v = slab[f * kMaxStates + q1];
+                const unsigned long long inc = 1ull << (16 * ((v + 1) >> 1));  // v = 0, 2, 3, 5 -> field 0..3
+                pl[f] += inc;
+                if (K > 1) hv[f] += inc;
+              }
+            }
           } else {
 #pragma unroll
             for (int r = 0; r < kIlp; ++r)
@@ -679,14 +709,33 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
               if (act) {
                 const uint32_t peers = __match_any_sync(am, (uint32_t)slot[r]);
                 if ((peers & lanemask_lt()) == 0) {  // leader: lowest lane of its group
-                  uint32_t q = w.lstate[slot[r]];
+                  const uint32_t raw = w.lstate[slot[r]];
+                  const uint32_t qo = raw & 0x7Fu;
+                  uint32_t q = qo;
                   uint32_t m = peers;
                   while (m) {
                     const int i = __ffs(m) - 1;
                     m &= m - 1;
                     q = sdelta[q * A + lb[base + 32 * r + i]];
                   }
-                  w.lstate[slot[r]] = (uint8_t)q;
+                  w.lstate[slot[r]] = (uint8_t)(q | 0x80u);
+                  const int pn = K > 1 ? (int)w.lnode[slot[r]] : 0;
+                  uint32_t *hw = w.nhist[K > 1 ? K - 2 : 0][pn < Tab::NS ? pn : 0];
+#pragma unroll
+                  for (int f = 0; f < NF; ++f) {
+                    const int vn = slab[f * kMaxStates + q], vo = slab[f * kMaxStates + qo];
+                    if (!(raw & 0x80u)) {
+                      atomicAdd(&w.pleaf[f * 6 + vn], 1);
+                      if (K > 1) atomicAdd(&hw[f * 3 + (vn >> 1)], 1u << (16 * (vn & 1)));
+                    } else if (vo != vn) {
+                      atomicAdd(&w.pleaf[f * 6 + vo], -1);
+                      atomicAdd(&w.pleaf[f * 6 + vn], 1);
+                      if (K > 1) {
+                        atomicAdd(&hw[f * 3 + (vn >> 1)], 1u << (16 * (vn & 1)));
+                        atomicSub(&hw[f * 3 + (vo >> 1)], 1u << (16 * (vo & 1)));
+                      }
+                    }
+                  }
                 }
               }
               __syncwarp();
@@ -695,56 +744,23 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
           __syncwarp();
         }
         resolve_next();
+        if (K > 1) flush_hv();
         ovf = __any_sync(0xffffffffu, ovf);
+        __syncwarp();
         if (ovf) {
           // too many distinct prefixes for the warp tables: hand the buckets on
           for (uint32_t x = bl + lane; x < bh; x += 32)
             if (p.bucket_off[x + 1] > p.bucket_off[x]) p.spill_list[atomicAdd(p.spill_len, 1ull)] = x;
         } else {
-          // a5 (i): leaf verdicts; lane takes a contiguous run of the leaf list so
-          // its child counts are aggregated per ancestor before one atomic flush
-          const uint32_t per = (nleaf + 31) >> 5;
-          const uint32_t i0 = min(nleaf, lane * per), i1 = min(nleaf, i0 + per);
-          int cur = -1;
-          unsigned long long hv[NF];
+          // a5 (i): commit the unit's leaf-verdict counts
 #pragma unroll
-          for (int f = 0; f < NF; ++f) hv[f] = 0;
-          auto flush_hv = [&]() {
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              if (hv[f]) {
-                uint32_t *hw = w.nhist[K > 1 ? K - 2 : 0][cur] + f * 3;
-                const uint32_t f0 = (uint32_t)hv[f] & 0xFFFFu, f1 = (uint32_t)(hv[f] >> 16) & 0xFFFFu;
-                const uint32_t f2 = (uint32_t)(hv[f] >> 32) & 0xFFFFu, f3 = (uint32_t)(hv[f] >> 48);
-                if (f0) atomicAdd(&hw[0], f0);
-                if (f1 | f2) atomicAdd(&hw[1], f1 | f2 << 16);
-                if (f3) atomicAdd(&hw[2], f3 << 16);
-                lcp[f] += hv[f];
-                hv[f] = 0;
-              }
-            }
-          };
-          for (uint32_t i = i0; i < i1; ++i) {
-            const int s = w.llist[i];
-            const int q = w.lstate[s];
-            if (K > 1) {
-              const int nd = w.lnode[s];
-              if (nd != cur) {
-                if (cur >= 0) flush_hv();
-                cur = nd;
-              }
-            }
-#pragma unroll
-            for (int f = 0; f < NF; ++f) {
-              const int v = slab[f * kMaxStates + q];
-              const unsigned long long inc = 1ull << (16 * ((v + 1) >> 1));  // v = 0, 2, 3, 5 -> field 0..3
-              if (K > 1) hv[f] += inc; else lcp[f] += inc;
-            }
+          for (int f = 0; f < NF; ++f) lcp[f] += pl[f];
+          for (int i = lane; i < NF * 6; i += 32) {
+            const int v = w.pleaf[i];
+            if (v) atomicAdd(&sacc[((i / 6) * (kMaxLevels + 1) + K) * 6 + i % 6], (uint32_t)v);
           }
-          if (K > 1 && cur >= 0) flush_hv();
-          since += per;
+          since += kWarpCap / 32;
           if (since > 60000u) { flush_lcp(); since = 0; }
-          __syncwarp();
           // a5 (ii): node verdicts by Def. 6, depth K-1 .. 1
           for (int l = K - 1; l >= 1; --l) {
             const uint32_t nn = w.ncnt[l];
@@ -764,6 +780,7 @@ __global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
             __syncwarp();
           }
         }
+        for (int i = lane; i < NF * 6; i += 32) w.pleaf[i] = 0;
         __syncwarp();
       }
       if (!split) break;
