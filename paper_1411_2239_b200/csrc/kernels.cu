@@ -471,8 +471,11 @@ __device__ __forceinline__ int node_probe(uint32_t *tag, uint32_t (*hist)[NF * 3
   }
 }
 
+#ifndef LTL4C_WARP_MINB
+#define LTL4C_WARP_MINB 4  // <= 64 registers: the shared-memory plan keeps up to 30 warps resident
+#endif
 template <int K, int NF, int CAP>
-__global__ void __launch_bounds__(256) bucket_warp_kernel(BucketParams p) {
+__global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(BucketParams p) {
   using Tab = WarpTab<K, NF, CAP>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const DevProg *prog = p.prog;
