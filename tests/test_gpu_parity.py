@@ -356,3 +356,42 @@ def test_online_table_growth(env):
         if hi in (2 * b, n):
             _assert_same(got, oracle.run_offline(tr.formula, [x[:hi] for x in tr.keys], tr.letters[:hi]), hi)
     assert st.stats()["kernels"]["rehash"]["launches"] >= 1
+
+
+@pytest.mark.parametrize("levels,nform", [(1, 2), (2, 2), (2, 4), (1, 4), (3, 2)])
+def test_formula_batches(env, levels, nform):
+    """Formula batches of F = 2 and 4 (one product monitor, shared guard keys) for
+    K = 1, 2, 3: every formula's verdict and counts against the oracle, offline
+    (sizes that reach the warp, CTA and heavy paths) and online."""
+    ltl4c, torch, dev = env
+    rng = random.Random(1000 * levels + nform)
+    ops = ["<", "<=", ">", ">=", "="]
+    # (the product of the batch must stay within 16 states)
+    bodies = (["F a", "G (a -> F b)", "a U b", "(a && b)", "X !a", "G a || (b U c)", "F (a && X c)"] if nform == 2
+              else ["F a", "G b", "F (a && b)", "G (a || b)"])
+    texts = []
+    for f in range(nform):
+        prefix = ""
+        for i in range(levels):
+            if rng.random() < 0.5:
+                prefix += f"forall[{rng.choice(ops)}{rng.choice(['0', '0.5', '1', '0.75'])}] x{i} : k{i}(x{i}) => "
+            else:
+                prefix += f"exists[{rng.choice(ops)}{rng.randint(0, 3)}] x{i} : k{i}(x{i}) => "
+        texts.append(prefix + bodies[(f + levels) % len(bodies)])
+    prog = ltl4c.compile_batch(texts)
+    props = [oracle.Property(t) for t in texts]
+    for n, values in [(5000, 40), (300_000, 3000), (400_000, 7)]:
+        keys, letters = tracegen.random_property_trace(7 * n + levels, levels, n, values=values,
+                                                       atoms=len(prog.atoms))
+        k, l = _dev(torch, dev, keys, letters)
+        got = prog.state(0).verify(k, l)
+        for f, (t, p) in enumerate(zip(texts, props)):
+            want = oracle.run_offline(t, keys, _project(letters, prog.atoms, p.atoms))
+            _assert_same(got[f], want, (t, n))
+        if n == 5000:
+            st = prog.state(0, online=True)
+            for lo, hi in [(0, 1200), (1200, 1201), (1201, 5000)]:
+                kk, ll = _dev(torch, dev, [x[lo:hi] for x in keys], letters[lo:hi])
+                got = st.verify(kk, ll, first_index=lo)
+            for f, (t, p) in enumerate(zip(texts, props)):
+                _assert_same(got[f], oracle.run_offline(t, keys, _project(letters, prog.atoms, p.atoms)), ("online", t))
