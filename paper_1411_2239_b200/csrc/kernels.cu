@@ -1862,15 +1862,22 @@ __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *
     return e_;                                         \
   } while (0)
 
-cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L) {
+template <int K>
+static cudaError_t fast_launch(const BucketParams &p, int nf, int n_sms, const Launcher &L) {
   const size_t sm = smem_bytes(K, nf, 0);
+  cudaFuncSetAttribute(bucket_fast_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  int per_sm = 2;  // every resident slot: the CTA per bucket is latency-bound
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bucket_fast_kernel<K>, kBucketThreads, sm) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 2;
+  LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<K><<<n_sms * per_sm, kBucketThreads, sm, L.stream>>>(p));
+}
+
+cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, int n_sms, const Launcher &L) {
   switch (K) {
-    case 1: cudaFuncSetAttribute(bucket_fast_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<1><<<grid, kBucketThreads, sm, L.stream>>>(p));
-    case 2: cudaFuncSetAttribute(bucket_fast_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<2><<<grid, kBucketThreads, sm, L.stream>>>(p));
-    default: cudaFuncSetAttribute(bucket_fast_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      LTL4C_LAUNCH(kKBucketFast, bucket_fast_kernel<3><<<grid, kBucketThreads, sm, L.stream>>>(p));
+    case 1: return fast_launch<1>(p, nf, n_sms, L);
+    case 2: return fast_launch<2>(p, nf, n_sms, L);
+    default: return fast_launch<3>(p, nf, n_sms, L);
   }
 }
 

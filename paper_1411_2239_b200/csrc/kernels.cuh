@@ -159,7 +159,7 @@ cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
-cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
+cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, int n_sms, const Launcher &L);
 cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 // {warps per CTA, CTAs per SM} of the unit kernel (cfg[0..1]) and of the

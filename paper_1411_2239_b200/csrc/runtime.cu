@@ -508,7 +508,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       BucketParams fp = bp;
       fp.list = st->large_list.p;
       fp.list_len = &st->d_acc.p->large_buckets;
-      CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, (uint32_t)(2 * st->n_sms), L));
+      CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, st->n_sms, L));
     } else {
       // carried state: leaves (warp per unit), then touched nodes depth K-1 .. 1
       OnlineParams op{};
