@@ -872,8 +872,9 @@ __device__ unsigned long long table_find_insert(uint4 *slots, unsigned long long
   return 0;
 }
 
+// st.release.gpu orders this thread's earlier writes (the slot's keys and the
+// payload it initialised) before the tag: no separate fence is needed
 __device__ __forceinline__ void table_publish(uint4 *slots, unsigned long long slot, uint32_t epoch) {
-  __threadfence();
   st_release(&slots[slot].x, (epoch << 1) | 1u);
 }
 
@@ -908,6 +909,8 @@ struct alignas(16) OnlineTab {
   uint8_t lstate[LS];
   uint8_t linit[LS];                    // state at chunk start, kNewLeaf for a leaf created now
   uint16_t llist[CAP];
+  uint32_t tstage[CAP];                 // nodes touched first by this chunk (appended together)
+  uint32_t tn;
 };
 
 // node of depth l (keys k[0..l-1]) in the carried tables; a new node starts with
@@ -953,6 +956,11 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
+  int lacc[NF][6];  // per-lane leaf-level verdict deltas
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int v = 0; v < 6; ++v) lacc[f][v] = 0;
   uint32_t ep = 0;
   while (true) {
     uint32_t u = 0;
@@ -1098,6 +1106,8 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
       long long pslot = -1;
       bool pok = false;
       uint32_t pk[kMaxLevels] = {0, 0, 0};
+      if (lane == 0) w.tn = 0;
+      __syncwarp();
       for (uint32_t i = i0; i < i1; ++i) {
         const int s = w.llist[i];
         const uint32_t qn = w.lstate[s], qi = w.linit[s];
@@ -1110,8 +1120,8 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
           vo[f] = qi == kNewLeaf ? -1 : (int)slab[f * kMaxStates + qi];
           if (vo[f] != vn[f]) {
             any = true;
-            if (vo[f] >= 0) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + vo[f]], -1);
-            atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + vn[f]], 1);
+#pragma unroll
+            for (int v = 0; v < 6; ++v) lacc[f][v] += (vn[f] == v) - (vo[f] == v);
           }
         }
         if (K > 1 && any) {
@@ -1127,7 +1137,8 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
             pslot = (long long)online_node(op, K - 1, k, &pok);
 #pragma unroll
             for (int x = 0; x < K - 1; ++x) pk[x] = k[x];
-            if (pok) online_touch(op, K - 1, (unsigned long long)pslot);
+            if (pok && atomicExch(&T.node_aux[K - 1][pslot], op.bid) != op.bid)
+              w.tstage[atomicAdd(&w.tn, 1u)] = (uint32_t)pslot;  // first touch this batch
           }
           if (pok) {
             uint32_t *hist = T.node_hist[K - 1] + (unsigned long long)pslot * kMaxFormulas * 6;
@@ -1142,8 +1153,25 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
         }
       }
       __syncwarp();
+      if (K > 1) {
+        // the chunk's newly touched nodes: one global append for the warp
+        const uint32_t tn = w.tn;
+        uint32_t tb = 0;
+        if (lane == 0 && tn) tb = atomicAdd(&op.tcnt[K - 1], tn);
+        tb = __shfl_sync(0xffffffffu, tb, 0);
+        for (uint32_t i = lane; i < tn; i += 32) op.tlist[K - 1][tb + i] = w.tstage[i];
+        __syncwarp();
+      }
     }
   }
+  // leaf-level verdict deltas: warp sums, then the CTA's
+#pragma unroll
+  for (int f = 0; f < NF; ++f)
+#pragma unroll
+    for (int v = 0; v < 6; ++v) {
+      const int c = __reduce_add_sync(0xffffffffu, lacc[f][v]);
+      if (lane == 0 && c) atomicAdd(&sacc[(f * (kMaxLevels + 1) + K) * 6 + v], c);
+    }
   __syncthreads();
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) {
     const int v = sacc[i];
