@@ -956,6 +956,7 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
   __syncthreads();
   const uint32_t q0 = prog->q0;
+  uint32_t newleaves = 0;  // leaves this lane inserted in the carried table
   int lacc[NF][6];  // per-lane leaf-level verdict deltas
 #pragma unroll
   for (int f = 0; f < NF; ++f)
@@ -1048,9 +1049,11 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
                                                              &p.acc->table_overflow);
               uint32_t q = q0;
               if (ins == 1) {
+                // publish at once: a lane of this warp probing through the slot spins
+                // on its busy tag (a deferred publish could deadlock the warp)
                 T.leaf_state[g] = (uint8_t)q0;
                 table_publish(T.leaf_slot, g, T.epoch);
-                atomicAdd(&p.acc->leaves, 1ull);
+                ++newleaves;
               } else if (ins == 0) {
                 q = T.leaf_state[g];
               }
@@ -1163,6 +1166,10 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
         __syncwarp();
       }
     }
+  }
+  {
+    const uint32_t c = __reduce_add_sync(0xffffffffu, newleaves);
+    if (lane == 0 && c) atomicAdd(&p.acc->leaves, (unsigned long long)c);
   }
   // leaf-level verdict deltas: warp sums, then the CTA's
 #pragma unroll
