@@ -1557,10 +1557,19 @@ __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
       for (int x = 0; x < K; ++x) k[x] = kb[x][rep];
       int ins;
       const unsigned long long slot = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &h.acc->table_overflow);
+      // dense ids of the new leaves: one counter update per group of converged lanes
+      uint32_t dense = 0;
+      const unsigned am = __activemask();
+      const unsigned nm = __ballot_sync(am, ins == 1);
+      if (nm) {
+        const int leader = __ffs(nm) - 1;
+        unsigned long long base = 0;
+        if (lane == leader) base = atomicAdd(h.n_leaves, (unsigned long long)__popc(nm));
+        base = __shfl_sync(am, base, leader);
+        dense = (uint32_t)base + __popc(nm & lanemask_lt());
+      }
       if (ins < 0) { h.part[pbase + i] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u); continue; }
-      uint32_t dense;
       if (ins == 1) {
-        dense = (uint32_t)atomicAdd(h.n_leaves, 1ull);
         T.leaf_aux[slot] = dense;
         h.leaf_slot_of[dense] = (uint32_t)slot;
         table_publish(T.leaf_slot, slot, T.epoch);
