@@ -61,7 +61,6 @@ struct Smem {
   uint8_t *ov;                // [kMaxFormulas][kCap] item verdicts (old, global path)
   uint8_t *nv;                // [kMaxFormulas][kCap] node verdicts
   uint8_t *nov;               // [kMaxFormulas][kCap] node old verdicts (global path)
-  unsigned long long *lmap;   // [kCap] heavy path: composed map per leaf
   uint8_t *delta;             // [kMaxStates * 256]
   unsigned long long *map;    // [256]
   uint8_t *lab;               // [kMaxFormulas * kMaxStates]
@@ -76,7 +75,7 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~size
 __host__ __device__ inline size_t smem_bytes(int K, int nf, int mode) {
   const bool global = mode == 1;
   const size_t fv = align16((size_t)nf * kCap);
-  return (mode == 2 ? align16(8 * kCap) : 0) + align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
+  return align16(sizeof(uint32_t) * kCap) * K + align16(kCap) + 3 * align16(2 * kCap) +
          align16(2 * 2 * kCap) + align16(2 * kCap) + 2 * align16(4 * (kCap + 1)) + align16(2 * kCap) +
          align16(kCap) + (global ? 4 : 2) * fv + align16(kMaxStates * 256) +
          align16(8 * 256) + align16(kMaxFormulas * kMaxStates) +
@@ -108,7 +107,6 @@ __device__ Smem carve(uint8_t *base, int K, int nf, int mode) {
   s.lab = take(kMaxFormulas * kMaxStates);
   s.acc = (int *)take(4 * kMaxFormulas * (kMaxLevels + 1) * 6);
   s.misc = (uint32_t *)take(4 * 64);
-  s.lmap = mode == 2 ? (unsigned long long *)take(8 * kCap) : nullptr;
   return s;
 }
 
@@ -1289,7 +1287,7 @@ __global__ void __launch_bounds__(1024) heavy_plan_kernel(HeavyParams h) {
     uint32_t v = 0;
     if (i < L) {
       const uint32_t b = h.list[i];
-      v = (h.bucket_off[b + 1] - h.bucket_off[b] + h.seg_events - 1) / h.seg_events;
+      v = (h.bucket_off[b + 1] - h.bucket_off[b] + kSegW - 1) / kSegW;
     }
     buf[threadIdx.x] = v;
     __syncthreads();
@@ -1301,98 +1299,12 @@ __global__ void __launch_bounds__(1024) heavy_plan_kernel(HeavyParams h) {
   if (threadIdx.x == 0) { h.seg_base[L] = carry; h.ctr[1] = carry; }
 }
 
-// H1: per segment, per leaf: composed transition map of its events (in order)
-template <int K>
-__global__ void __launch_bounds__(kBucketThreads) heavy_seg_kernel(HeavyParams h) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  const DevProg *prog = h.prog;
-  const int nf = prog->nf, nq = prog->nq;
-  const Smem s = carve(smem_raw, K, nf, 2);
-  load_prog(s, prog);
-  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
-  const DevTables &T = h.tab;
-  unsigned long long ident = 0;
-  for (int q = 0; q < nq; ++q) ident |= (unsigned long long)q << (4 * q);
-  BucketParams bp{};
-  for (int k = 0; k < K; ++k) bp.key[k] = h.key[k];
-  bp.let = h.let;
-  const uint32_t L = (uint32_t)*h.list_len;
-  while (true) {
-    __syncthreads();
-    if (tid == 0) {
-      const uint32_t item = atomicAdd(&h.ctr[0], 1u);
-      s.misc[50] = item;
-      if (item < h.ctr[1]) {  // bucket of the item: last i with seg_base[i] <= item
-        uint32_t lo = 0, hi = L;
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (h.seg_base[mid] <= item) lo = mid; else hi = mid;
-        }
-        s.misc[51] = lo;
-      }
-    }
-    __syncthreads();
-    const uint32_t item = s.misc[50];
-    if (item >= h.ctr[1]) break;
-    const uint32_t i = s.misc[51];
-    const uint32_t b = h.list[i];
-    const uint32_t j = item - h.seg_base[i];
-    const uint32_t boff = h.bucket_off[b], bcnt = h.bucket_off[b + 1] - boff;
-    const uint32_t start = boff + j * kCap;
-    const int n = (int)min((uint32_t)kCap, bcnt - j * kCap);  // (seg_events == kCap here)
-    load_chunk<K>(s, bp, start, n);
-    const int C = dedup<K>(s, n, K);
-    group_by_class(s, n, C);
-    order_segments(s, n, C);
-    for (int c = tid; c < C; c += nt) {
-      const int a = s.scan[c], e = s.scan[c + 1];
-      if (e - a > 32) continue;
-      unsigned long long m = ident;
-      for (int x = a; x < e; ++x) m = map_apply(s.map[s.let[s.perm[x]]], m, nq);
-      s.lmap[c] = m;
-    }
-    for (int c = wid; c < C; c += nw) {
-      if (s.scan[c + 1] - s.scan[c] <= 32) continue;
-      const unsigned long long total = long_class_map(s, n, c, nq, ident);
-      if (lane == 0) s.lmap[c] = total;
-      __syncwarp();
-    }
-    if (tid == 0) {  // one allocation of partial slots per segment
-      const unsigned long long pb = atomicAdd(h.n_part, (unsigned long long)C);
-      s.misc[52] = (uint32_t)pb;
-      s.misc[53] = (uint32_t)(pb >> 32);
-    }
-    __syncthreads();
-    const unsigned long long pbase = (unsigned long long)s.misc[52] | ((unsigned long long)s.misc[53] << 32);
-    for (int c = tid; c < C; c += nt) {
-      uint32_t k[kMaxLevels] = {0, 0, 0};
-      for (int x = 0; x < K; ++x) k[x] = s.key[x][s.rep[c]];
-      int ins;
-      const unsigned long long slot = table_find_insert(T.leaf_slot, T.leaf_cap, T.epoch, k, K, &ins, &h.acc->table_overflow);
-      if (ins < 0) { h.part[pbase + c] = make_uint4(0xFFFFFFFFu, 0u, 0u, 0u); continue; }
-      uint32_t dense;
-      if (ins == 1) {
-        dense = (uint32_t)atomicAdd(h.n_leaves, 1ull);
-        T.leaf_aux[slot] = dense;
-        h.leaf_slot_of[dense] = (uint32_t)slot;
-        table_publish(T.leaf_slot, slot, T.epoch);
-      } else {
-        dense = *(volatile uint32_t *)&T.leaf_aux[slot];
-      }
-      atomicAdd(&h.leaf_npart[dense], 1u);
-      const unsigned long long m = s.lmap[c];
-      h.part[pbase + c] = make_uint4(dense, item, (uint32_t)m, (uint32_t)(m >> 32));
-    }
-  }
-}
-
-// H1 (warp form): segments of kSegW events, one warp each.  The segment is
+// H1: segments of kSegW events, one warp each.  The segment is
 // staged into warp-private shared memory; its value vectors are deduplicated in
 // an epoch-tagged warp table; every leaf's transition maps are composed in trace
 // order (a window whose slots are all new and touched once takes the letter's
 // map; otherwise lanes sharing a slot are grouped and the leader composes in
 // lane order); one partial {dense leaf, segment, map} per leaf of the segment.
-constexpr int kSegW = 256;
 
 template <int K>
 struct alignas(16) SegTab {
@@ -2040,16 +1952,12 @@ template <int K>
 static cudaError_t heavy_all(const HeavyParams &h, int nf, int n_sms, const Launcher &L) {
   if (L.before) L.before(L.ctx, kKHeavy);
   heavy_plan_kernel<<<1, 1024, 0, L.stream>>>(h);
-  if (h.seg_events == kSegW) {
+  {
     const size_t sm = 8 * kMaxLetters + 8 * sizeof(SegTab<K>);
     cudaFuncSetAttribute(heavy_segw_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy_segw_kernel<K>, 256, sm);
     heavy_segw_kernel<K><<<n_sms * (per_sm > 0 ? per_sm : 1), 256, sm, L.stream>>>(h);
-  } else {
-    const size_t sm = smem_bytes(K, nf, 2);
-    cudaFuncSetAttribute(heavy_seg_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    heavy_seg_kernel<K><<<2 * n_sms, kBucketThreads, sm, L.stream>>>(h);
   }
   heavy_scan_blocks<<<2 * n_sms, 1024, 0, L.stream>>>(h);
   heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h);

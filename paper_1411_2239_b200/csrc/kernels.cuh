@@ -11,6 +11,7 @@ constexpr int kPartThreads = 512;    // 16 warps x 8 rounds x 32 lanes
 constexpr int kMaxDigitBits = 9;     // <= 512 digits per stable partition pass
 constexpr int kMaxDigits = 1 << kMaxDigitBits;
 constexpr int kMaxPasses = 3;        // bucket bits <= 27
+constexpr int kSegW = 256;           // events per heavy-path segment (one warp each)
 constexpr int kCap = 2048;           // events per bucket chunk held in shared memory (CTA paths)
 constexpr int kBucketThreads = 256;
 #ifndef LTL4C_WARP_CAP
@@ -91,7 +92,6 @@ struct HeavyParams {
   unsigned long long *n_nodes;          // [kMaxLevels]
   uint32_t *scan_tmp;                   // block sums of the leaf_npart scan
   unsigned long long cap_leaves;        // upper bound of dense leaves (host)
-  uint32_t seg_events;                  // events per segment: 256 (warp segments) or kCap (CTA segments)
 };
 
 struct BucketParams {

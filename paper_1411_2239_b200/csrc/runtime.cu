@@ -339,7 +339,6 @@ ltl4c_status run_heavy(ltl4c_state *st, const BucketParams &bp, int K, cudaStrea
   st->tab.d.epoch = ++st->epoch;
   const uint64_t nblk = (ev + 1023) / 1024 + 1;
   const size_t nseg = nb + 1;
-  static const uint32_t seg_events = std::getenv("LTL4C_CTA_SEGMENTS") ? (uint32_t)kCap : 256u;
   const size_t u32_need = nseg + 5 * ev + nblk + (size_t)(K - 1) * cap + 16;
   CU(st->h_part.ensure(ev + 1));
   CU(st->h_lists.ensure(ev + 1));
@@ -371,7 +370,6 @@ ltl4c_status run_heavy(ltl4c_state *st, const BucketParams &bp, int K, cudaStrea
   h.n_leaves = c + 1;
   h.n_nodes = c + 4;  // [kMaxLevels]
   h.cap_leaves = ev;
-  h.seg_events = seg_events;
   CU(cudaMemsetAsync(h.leaf_npart, 0, sizeof(uint32_t) * 2 * ev, s));  // npart, off
   CU(cudaMemsetAsync(h.leaf_fill, 0, sizeof(uint32_t) * ev, s));
   CU(cudaMemsetAsync(h.ctr, 0, sizeof(uint32_t) * 8, s));
