@@ -310,29 +310,32 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 constexpr int kBoundsPer = 16;
 __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, int bits,
                                      uint32_t *off, uint32_t nb) {
-  const unsigned long long n = *nvalid;
-  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; kBoundsPer * t <= n;
-       t += (unsigned long long)gridDim.x * blockDim.x) {
-    const unsigned long long i0 = kBoundsPer * t;
-    uint32_t kv[kBoundsPer];
+  // (n < 2^32 - 2^20: 32-bit positions; bucket ids are < 2^27, so b + 1 never wraps)
+  const uint32_t n = (uint32_t)*nvalid;
+  const uint32_t shift = 32 - bits;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= n / kBoundsPer; t += gridDim.x * blockDim.x) {
+    const uint32_t i0 = kBoundsPer * t;
+    uint32_t prev = 0;  // bucket of event i0 - 1, plus one (0 before the first event)
+    if (i0 > 0) prev = (bits == 0 ? 0u : fmix32(k0[i0 - 1] ^ kBucketSalt) >> shift) + 1;
     if (i0 + kBoundsPer <= n) {
+      uint32_t kv[kBoundsPer];
 #pragma unroll
       for (int q = 0; q < kBoundsPer / 4; ++q) {
         const uint4 v = __ldg(reinterpret_cast<const uint4 *>(k0 + i0) + q);
         kv[4 * q] = v.x; kv[4 * q + 1] = v.y; kv[4 * q + 2] = v.z; kv[4 * q + 3] = v.w;
       }
-    } else {
 #pragma unroll
-      for (int j = 0; j < kBoundsPer; ++j) kv[j] = i0 + j < n ? k0[i0 + j] : 0u;
-    }
-    const uint32_t kp = i0 == 0 ? 0u : k0[i0 - 1];
-    long long prev = i0 == 0 ? -1 : (long long)bucket_of(kp, bits);
-#pragma unroll
-    for (int j = 0; j < kBoundsPer; ++j) {
-      if (i0 + j > n) break;
-      const long long b = i0 + j < n ? (long long)bucket_of(kv[j], bits) : (long long)nb;
-      for (long long c = prev + 1; c <= b; ++c) off[c] = (uint32_t)(i0 + j);
-      prev = b;
+      for (int j = 0; j < kBoundsPer; ++j) {
+        const uint32_t b = bits == 0 ? 0u : fmix32(kv[j] ^ kBucketSalt) >> shift;
+        for (uint32_t c = prev; c <= b; ++c) off[c] = i0 + j;  // buckets (previous, b] start here
+        prev = max(prev, b + 1);
+      }
+    } else {  // the ragged end (t = n / 16) also writes the offsets after the last bucket
+      for (uint32_t j = 0; i0 + j <= n; ++j) {
+        const uint32_t b = i0 + j < n ? (bits == 0 ? 0u : fmix32(k0[i0 + j] ^ kBucketSalt) >> shift) : nb;
+        for (uint32_t c = prev; c <= b; ++c) off[c] = i0 + j;
+        prev = max(prev, b + 1);
+      }
     }
   }
 }
