@@ -176,6 +176,20 @@ ltl4c_status ltl4c_verify(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_
 ltl4c_status ltl4c_verify_host(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream,
                                ltl4c_result *out);
 
+/* Pipelined online monitoring (a stream of batches): enqueue one batch
+ * of an online state on `cuda_stream` and return at once with a ticket; the
+ * result is read later with ltl4c_result_get(ticket) (which waits for that
+ * batch only).  All batches of a state go on the same stream.  Batches must be
+ * contiguous as for ltl4c_verify, their device
+ * buffers must stay valid until the result is read, and at most 8 results may
+ * be outstanding (E_INVALID otherwise).  Single-GPU states only.  Carried tables
+ * grow on the bound "leaves of the last read result + events enqueued since".
+ * Errors: E_INVALID (offline state, communicator, too many outstanding, bad
+ * ticket), E_CUDA, E_OOM (table overflow: the state is poisoned). */
+ltl4c_status ltl4c_verify_async(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream,
+                                uint64_t *ticket);
+ltl4c_status ltl4c_result_get(ltl4c_state *st, uint64_t ticket, ltl4c_result *out);
+
 /* Forget all carried state (online) and clear the poisoned flag. */
 ltl4c_status ltl4c_state_reset(ltl4c_state *st);
 

@@ -92,6 +92,8 @@ _lib.ltl4c_nccl_unique_id.argtypes = [ctypes.c_void_p]
 _lib.ltl4c_nccl_unique_id.restype = ctypes.c_int
 _lib.ltl4c_verify.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
 _lib.ltl4c_verify_host.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(_Result)]
+_lib.ltl4c_verify_async.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_result_get.argtypes = [_P, ctypes.c_uint64, ctypes.POINTER(_Result)]
 _lib.ltl4c_state_reset.argtypes = [_P]
 _lib.ltl4c_state_free.argtypes = [_P]
 _lib.ltl4c_state_free.restype = None
@@ -101,7 +103,8 @@ _lib.ltl4c_state_stats_reset.argtypes = [_P]
 _lib.ltl4c_last_error.restype = ctypes.c_char_p
 _lib.ltl4c_version.restype = ctypes.c_char_p
 for _fn in ("ltl4c_compile", "ltl4c_compile_batch", "ltl4c_program_tables", "ltl4c_state_create",
-            "ltl4c_state_comm", "ltl4c_verify", "ltl4c_verify_host", "ltl4c_state_reset",
+            "ltl4c_state_comm", "ltl4c_verify", "ltl4c_verify_host", "ltl4c_verify_async", "ltl4c_result_get",
+            "ltl4c_state_reset",
             "ltl4c_state_profile", "ltl4c_state_stats", "ltl4c_state_stats_reset"):
     getattr(_lib, _fn).restype = ctypes.c_int
 
@@ -214,6 +217,7 @@ class State:
         _check(_lib.ltl4c_state_create(prog._h, device, capacity, ONLINE if online else 0,
                                        ctypes.byref(self._h)))
         self.next_index = 0
+        self._pending = {}  # ticket -> input tensors of a pipelined batch
 
     def __del__(self):
         try:
@@ -254,6 +258,33 @@ class State:
         res = (_Result * self.prog.n_formulas)()
         _check(_lib.ltl4c_verify(self._h, ctypes.byref(b), _stream_handle(stream), res))
         self.next_index = b.first_index + n
+        return self._results(res)
+
+    def verify_async(self, keys, letters, first_index=None, stream=None) -> int:
+        """Online states: enqueue one batch and return a ticket at once (the result is
+        read with result(ticket); the tensors are kept alive until then)."""
+        import torch
+        n = int(letters.numel())
+        keys = list(keys)[: self.prog.n_levels]
+        for k in keys:
+            if not (k.is_cuda and k.is_contiguous() and k.element_size() == 4 and k.numel() == n):
+                raise ValueError("keys must be contiguous 4-byte CUDA tensors of the same length as letters")
+        if not (letters.is_cuda and letters.is_contiguous() and letters.dtype == torch.uint8):
+            raise ValueError("letters must be a contiguous uint8 CUDA tensor")
+        b = self._batch(keys, letters, n, first_index, lambda t: t.data_ptr() if n else None)
+        t = ctypes.c_uint64()
+        _check(_lib.ltl4c_verify_async(self._h, ctypes.byref(b), _stream_handle(stream), ctypes.byref(t)))
+        self.next_index = b.first_index + n
+        self._pending[t.value] = (keys, letters)
+        return t.value
+
+    def result(self, ticket: int) -> list[Result]:
+        """Wait for the batch of `ticket` (from verify_async) and return its result."""
+        res = (_Result * self.prog.n_formulas)()
+        try:
+            _check(_lib.ltl4c_result_get(self._h, ticket, res))
+        finally:
+            self._pending.pop(ticket, None)
         return self._results(res)
 
     def verify_host(self, keys, letters, first_index=None, stream=None) -> list[Result]:

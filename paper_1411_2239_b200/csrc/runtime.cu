@@ -167,6 +167,16 @@ struct ltl4c_state {
   int n_sms = 148;
   int warp_cfg[4] = {4, 1, 1, 1};  // {warps/CTA, CTAs/SM} of the unit and the medium warp kernels
   int online_cfg[2] = {4, 1};      // {warps/CTA, CTAs/SM} of online_leaf
+  // pipelined online batches (ltl4c_verify_async / ltl4c_result_get): results land
+  // in a ring of pinned slots; table growth uses an upper bound of the carried
+  // leaves (the last read result + every event enqueued after it)
+  static constexpr int kRing = 8;
+  DevOut *ring_out = nullptr;                 // pinned [kRing]
+  cudaEvent_t ring_ev[kRing] = {};
+  uint64_t ring_ticket[kRing] = {};           // 0: free / consumed
+  uint64_t ring_seen[kRing] = {}, ring_cum[kRing] = {};
+  uint64_t next_ticket = 1, enq_events = 0, outstanding = 0;
+  uint64_t known_leaves = 0, known_nodes[kMaxLevels] = {}, known_cum = 0;
   uint32_t batch_id = 0;           // online: touch mark of the current batch
   DevBuf<uint32_t> tlist[kMaxLevels], tcnt;
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
@@ -288,22 +298,36 @@ ltl4c_status alloc_tables(ltl4c_state *st, Tables &t, uint64_t leaf_cap, uint64_
 // Online: make sure the carried tables can absorb `extra` more leaves/nodes at
 // load <= 1/2, rehashing the carried entries into larger tables if needed.
 ltl4c_status ensure_online_tables(ltl4c_state *st, uint64_t extra, cudaStream_t s, const Launcher &L) {
-  const uint64_t have = st->h_out->leaves;
-  uint64_t need_nodes = 0;
-  for (int l = 1; l < (int)st->prog->n_levels; ++l) need_nodes = std::max<uint64_t>(need_nodes, st->h_out->nodes[l]);
-  // load <= 1/2 after this batch; grow 4x at a time (rehash = alloc + copy + sync)
-  const uint64_t need_leaf = 2 * (have + extra) + 1, need_node = 2 * (need_nodes + extra) + 1;
-  uint64_t want_leaf = 1ull << std::max(20, ceil_log2(need_leaf));
-  uint64_t want_node = 1ull << std::max(16, ceil_log2(need_node));
-  if (st->tab.d.leaf_cap && st->tab.d.leaf_cap < want_leaf) want_leaf = std::max<uint64_t>(want_leaf, 4 * st->tab.d.leaf_cap);
-  if (st->tab.d.leaf_cap == 0) want_leaf = std::max<uint64_t>(want_leaf, 1ull << ceil_log2(8 * extra + 1));
   Tables &t = st->tab;
-  bool fresh = t.d.leaf_cap == 0;
-  if (!fresh && t.d.leaf_cap >= want_leaf) {
-    bool ok = true;
-    for (int l = 1; l < (int)st->prog->n_levels; ++l) ok &= t.d.node_cap[l] >= want_node;
-    if (ok) return LTL4C_OK;
+  uint64_t want_leaf = 0, want_node = 0;
+  bool fits = false;
+  for (int pass = 0; pass < 2; ++pass) {
+    // carried leaves / nodes: the last result read, plus (pipelined batches) every
+    // event enqueued since -- an upper bound, each event adds at most one of each
+    const uint64_t inflight = st->enq_events - st->known_cum;
+    const uint64_t have = st->known_leaves + inflight;
+    uint64_t need_nodes = 0;
+    for (int l = 1; l < (int)st->prog->n_levels; ++l) need_nodes = std::max<uint64_t>(need_nodes, st->known_nodes[l] + inflight);
+    // load <= 1/2 after this batch; grow 4x at a time (rehash = alloc + copy + sync)
+    const uint64_t need_leaf = 2 * (have + extra) + 1, need_node = 2 * (need_nodes + extra) + 1;
+    want_leaf = 1ull << std::max(20, ceil_log2(need_leaf));
+    want_node = 1ull << std::max(16, ceil_log2(need_node));
+    if (t.d.leaf_cap && t.d.leaf_cap < want_leaf) want_leaf = std::max<uint64_t>(want_leaf, 4 * t.d.leaf_cap);
+    if (t.d.leaf_cap == 0) want_leaf = std::max<uint64_t>(want_leaf, 1ull << ceil_log2(8 * extra + 1));
+    fits = t.d.leaf_cap && t.d.leaf_cap >= want_leaf;
+    for (int l = 1; l < (int)st->prog->n_levels; ++l) fits &= t.d.node_cap[l] >= want_node;
+    if (fits || inflight == 0 || t.d.leaf_cap == 0) break;
+    // the bound says grow while batches are in flight: wait for them and use the
+    // exact carried counts instead (growth is rare; the bound alone would over-allocate)
+    CU(cudaStreamSynchronize(s));
+    unsigned long long cnt[1 + kMaxLevels + 1];
+    CU(cudaMemcpy(cnt, &st->d_acc.p->leaves, sizeof cnt, cudaMemcpyDeviceToHost));
+    st->known_leaves = cnt[0];
+    for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = cnt[1 + l];
+    st->known_cum = st->enq_events;
   }
+  if (fits) return LTL4C_OK;
+  bool fresh = t.d.leaf_cap == 0;
   if (fresh) {
     ltl4c_status r = alloc_tables(st, t, want_leaf, want_node, s, false, true);
     if (r) return r;
@@ -444,7 +468,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
 // memsets, SortTrace (count / scan / scatter per pass), mu, the bucket kernels,
 // finalize and the D2H copy of the result record.
 ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *const *keys, const uint8_t *letters,
-                          cudaStream_t s, const Launcher &L, bool finalize_now = true) {
+                          cudaStream_t s, const Launcher &L, bool finalize_now = true, DevOut *dst = nullptr) {
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
@@ -524,7 +548,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
   }
   if (finalize_now) {
     CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
-    CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+    CU(cudaMemcpyAsync(dst ? dst : st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
   }
   return LTL4C_OK;
 }
@@ -637,8 +661,24 @@ void drop_graph(ltl4c_state *st) {
   st->graph_key.clear();
 }
 
+void fill_results(const ltl4c_state *st, const DevOut &o, uint64_t events_seen, bool comm, ltl4c_result *out) {
+  for (uint32_t f = 0; f < st->prog->n_formulas; ++f) {
+    const DevResult &r = o.res[f];
+    ltl4c_result &x = out[f];
+    std::memset(&x, 0, sizeof x);
+    x.verdict = r.verdict;
+    x.n_levels = r.n_levels;
+    for (int l = 0; l <= kMaxLevels; ++l)
+      for (int v = 0; v < 6; ++v) x.hist[l][v] = r.hist[l][v];
+    x.events_seen = comm ? r.events_seen : events_seen;
+    x.events_bound = r.events_bound;
+  }
+}
+
+// async_dst: pipelined online batch -- the result is copied to this pinned slot
+// and the call returns without waiting (ltl4c_result_get reads it)
 ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, ltl4c_result *out,
-                        const uint32_t *const *keys, const uint8_t *letters) {
+                        const uint32_t *const *keys, const uint8_t *letters, DevOut *async_dst = nullptr) {
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
@@ -653,6 +693,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
     CU(st->tcnt.ensure(kMaxLevels));
     if (++st->batch_id == 0) st->batch_id = 1;  // wrap: marks of batch 0 never exist
+    st->enq_events += N;
   }
   const bool comm = st->comm && (st->n_ranks > 1 || st->force_exchange);
   uint64_t Nloc = N;
@@ -719,8 +760,13 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     CU(cudaGraphLaunch(st->graph_exec, s));
     st->launches += st->graph_kernels;
   } else {
-    ltl4c_status r = enqueue_main(st, plan, keys, letters, s, L);
+    ltl4c_status r = enqueue_main(st, plan, keys, letters, s, L, true, async_dst);
     if (r) return r;
+  }
+  if (async_dst) {
+    for (int k = 0; k < kKNumKernels; ++k) st->k_launches_saved[k] = st->k_launches[k];
+    st->verifies++;
+    return LTL4C_OK;
   }
   CU(cudaStreamSynchronize(s));
   if (!online && N > 0 && st->h_out->oversize_buckets > 0) {
@@ -735,24 +781,19 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   for (int k = 0; k < kKNumKernels; ++k) st->k_launches_saved[k] = st->k_launches[k];
   if (st->h_out->table_overflow)
     return fail(LTL4C_E_OOM, "carried table overflow");
-  for (uint32_t f = 0; f < prog->n_formulas; ++f) {
-    const DevResult &r = st->h_out->res[f];
-    ltl4c_result &o = out[f];
-    std::memset(&o, 0, sizeof o);
-    o.verdict = r.verdict;
-    o.n_levels = r.n_levels;
-    for (int l = 0; l <= kMaxLevels; ++l)
-      for (int v = 0; v < 6; ++v) o.hist[l][v] = r.hist[l][v];
-    o.events_seen = comm ? r.events_seen : st->events_seen;
-    o.events_bound = r.events_bound;
+  if (online) {
+    st->known_leaves = st->h_out->leaves;
+    for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = st->h_out->nodes[l];
+    st->known_cum = st->enq_events;
   }
+  fill_results(st, *st->h_out, st->events_seen, comm, out);
   st->verifies++;
   return LTL4C_OK;
 }
 
 ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, ltl4c_result *out,
-                           bool host) {
-  if (!st || !b || !out) return fail(LTL4C_E_INVALID, "null argument");
+                           bool host, DevOut *async_dst = nullptr) {
+  if (!st || !b || (!out && !async_dst)) return fail(LTL4C_E_INVALID, "null argument");
   if (st->poisoned) return fail(LTL4C_E_POISONED, "state poisoned by an earlier failure; reset it");
   const int K = (int)st->prog->n_levels;
   if (b->n_events > (1ull << 32) - (1ull << 20))
@@ -787,7 +828,7 @@ ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, 
       letters = st->hlet.p;
     }
   }
-  if (!r) r = run_verify(st, b, s, out, keys, letters);
+  if (!r) r = run_verify(st, b, s, out, keys, letters, async_dst);
   if (prev != st->device) cudaSetDevice(prev);
   if (r) {
     if (online) st->poisoned = true;
@@ -948,6 +989,59 @@ ltl4c_status ltl4c_verify_host(ltl4c_state *st, const ltl4c_batch *batch, void *
   return verify_common(st, batch, cuda_stream, out, true);
 }
 
+ltl4c_status ltl4c_verify_async(ltl4c_state *st, const ltl4c_batch *batch, void *cuda_stream, uint64_t *ticket) {
+  if (!st || !batch || !ticket) return fail(LTL4C_E_INVALID, "null argument");
+  if (!(st->flags & LTL4C_STATE_ONLINE)) return fail(LTL4C_E_INVALID, "ltl4c_verify_async needs an online state");
+  if (st->comm) return fail(LTL4C_E_INVALID, "ltl4c_verify_async is single-GPU (no communicator)");
+  const uint64_t t = st->next_ticket;
+  const int slot = (int)(t % ltl4c_state::kRing);
+  if (st->ring_ticket[slot]) return fail(LTL4C_E_INVALID, "too many results outstanding (read them with ltl4c_result_get)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != st->device) CU(cudaSetDevice(st->device));
+  if (!st->ring_out) {
+    if (cudaMallocHost((void **)&st->ring_out, sizeof(DevOut) * ltl4c_state::kRing) != cudaSuccess) {
+      cudaSetDevice(prev);
+      return fail(LTL4C_E_OOM, "pinned allocation failed");
+    }
+    for (int i = 0; i < ltl4c_state::kRing; ++i) CU(cudaEventCreateWithFlags(&st->ring_ev[i], cudaEventDisableTiming));
+  }
+  ltl4c_status r = verify_common(st, batch, cuda_stream, nullptr, false, &st->ring_out[slot]);
+  if (!r) {
+    if (cudaEventRecord(st->ring_ev[slot], (cudaStream_t)cuda_stream) != cudaSuccess) r = fail(LTL4C_E_CUDA, "event record");
+  }
+  if (prev != st->device) cudaSetDevice(prev);
+  if (r) return r;
+  st->ring_ticket[slot] = t;
+  st->ring_seen[slot] = st->events_seen;
+  st->ring_cum[slot] = st->enq_events;
+  st->next_ticket = t + 1;
+  st->outstanding++;
+  *ticket = t;
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_result_get(ltl4c_state *st, uint64_t ticket, ltl4c_result *out) {
+  if (!st || !out) return fail(LTL4C_E_INVALID, "null argument");
+  const int slot = (int)(ticket % ltl4c_state::kRing);
+  if (ticket == 0 || st->ring_ticket[slot] != ticket) return fail(LTL4C_E_INVALID, "unknown or already read ticket");
+  CU(cudaEventSynchronize(st->ring_ev[slot]));
+  const DevOut &o = st->ring_out[slot];
+  st->ring_ticket[slot] = 0;
+  st->outstanding--;
+  if (o.table_overflow) {
+    st->poisoned = true;
+    return fail(LTL4C_E_OOM, "carried table overflow");
+  }
+  if (st->ring_cum[slot] >= st->known_cum) {
+    st->known_leaves = o.leaves;
+    for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = o.nodes[l];
+    st->known_cum = st->ring_cum[slot];
+  }
+  fill_results(st, o, st->ring_seen[slot], false, out);
+  return LTL4C_OK;
+}
+
 ltl4c_status ltl4c_state_reset(ltl4c_state *st) {
   if (!st) return fail(LTL4C_E_INVALID, "null state");
   int prev = 0;
@@ -955,6 +1049,11 @@ ltl4c_status ltl4c_state_reset(ltl4c_state *st) {
   CU(cudaSetDevice(st->device));
   CU(cudaMemset(st->d_acc.p, 0, sizeof(DevAcc)));
   std::memset(st->h_out, 0, sizeof(DevOut));
+  for (int i = 0; i < ltl4c_state::kRing; ++i)  // drain pipelined batches
+    if (st->ring_ticket[i]) { cudaEventSynchronize(st->ring_ev[i]); st->ring_ticket[i] = 0; }
+  st->outstanding = 0;
+  st->known_leaves = st->known_cum = st->enq_events = 0;
+  for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = 0;
   st->epoch++;  // every carried table slot becomes stale
   st->tab.d.epoch = st->epoch;
   st->poisoned = false;
@@ -1009,6 +1108,9 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->exlet.release();
   st->dc_cnt.release();
   if (st->hc_cnt) cudaFreeHost(st->hc_cnt);
+  for (int i = 0; i < ltl4c_state::kRing; ++i)
+    if (st->ring_ev[i]) cudaEventDestroy(st->ring_ev[i]);
+  if (st->ring_out) cudaFreeHost(st->ring_out);
   if (st->h_out) cudaFreeHost(st->h_out);
   cudaSetDevice(prev);
   delete st;

@@ -395,3 +395,43 @@ def test_formula_batches(env, levels, nform):
                 got = st.verify(kk, ll, first_index=lo)
             for f, (t, p) in enumerate(zip(texts, props)):
                 _assert_same(got[f], oracle.run_offline(t, keys, _project(letters, prog.atoms, p.atoms)), ("online", t))
+
+
+def test_online_async_pipeline(env):
+    """Pipelined online batches (ltl4c_verify_async / ltl4c_result_get) return the
+    same result per batch as synchronous verification, with carried tables growing
+    while batches are in flight; misuse is rejected."""
+    ltl4c, torch, dev = env
+    tr = tracegen.c5_trace(seed=41, n=2_400_000, users=3000, hosts=64, span_events=400_000)
+    prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+    sync_st, async_st = prog.state(0, online=True), prog.state(0, online=True)
+    k, l = _dev(torch, dev, tr.keys, tr.letters)
+    b = 200_000
+    tickets, want = [], []
+    for i, lo in enumerate(range(0, tr.n, b)):
+        hi = min(tr.n, lo + b)
+        want.append(sync_st.verify([x[lo:hi] for x in k], l[lo:hi], first_index=lo))
+        tickets.append(async_st.verify_async([x[lo:hi] for x in k], l[lo:hi], first_index=lo))
+        if len(tickets) > 4:  # read with a lag of 4 batches
+            j = len(want) - 5
+            got = async_st.result(tickets[j])
+            for f in range(len(got)):
+                _assert_same(got[f], {"verdict": want[j][f].verdict, "hist": want[j][f].hist,
+                                      "events_bound": want[j][f].events_bound}, ("async", j, f))
+    for j in range(len(want) - 4, len(want)):
+        got = async_st.result(tickets[j])
+        for f in range(len(got)):
+            assert got[f].verdict == want[j][f].verdict and np.array_equal(got[f].hist, want[j][f].hist)
+    for f, text in enumerate(tracegen.C5_FORMULAS):
+        p = oracle.Property(text)
+        _assert_same(want[-1][f], oracle.run_offline(text, tr.keys, _project(tr.letters, prog.atoms, p.atoms)), f)
+    with pytest.raises(ltl4c.Ltl4cError):
+        async_st.result(tickets[0])            # already read
+    with pytest.raises(ltl4c.Ltl4cError):
+        prog.state(0).verify_async([x[:10] for x in k], l[:10])   # offline state
+    st = prog.state(0, online=True)
+    ts = [st.verify_async([x[i:i + 10] for x in k], l[i:i + 10], first_index=i) for i in range(0, 80, 10)]
+    with pytest.raises(ltl4c.Ltl4cError):
+        st.verify_async([x[80:90] for x in k], l[80:90], first_index=80)   # 9th outstanding
+    for t in ts:
+        st.result(t)
