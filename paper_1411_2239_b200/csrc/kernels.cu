@@ -290,6 +290,7 @@ __device__ int load_chunk(const Smem &s, const BucketParams &p, uint32_t start, 
 template <int K>
 __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
+  if (blockIdx.x >= *p.list_len) return;  // (uniform per CTA) nothing for this CTA
   const DevProg *prog = p.prog;
   const int nf = prog->nf, nl = prog->nl, nq = prog->nq, A = 1 << prog->na;
   const Smem s = carve(smem_raw, K, nf, 0);
