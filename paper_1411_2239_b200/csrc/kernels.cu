@@ -2,14 +2,12 @@
 //
 // arXiv:1411.2239, Algorithm 1, re-designed for B200:
 //
-//  part_count / part_scan / part_scatter
-//      a1 epsilon (Eq. D) fused with a2 SortTrace:
-//      a STABLE LSD partition of the bound events by bucket = top bits of
-//      hash(k0).  Every node of the submonitor tree below the root is keyed by a
-//      vector that starts with k0, so a bucket holds whole level-0 subtrees, and
-//      stability keeps every slice u^D in trace order (reading A15).
-//  bucket_scan
-//      exclusive scan of the bucket histogram -> bucket offsets (mu).
+//  (partition.cu: part_count / part_scan / part_scatter / bucket_bounds --
+//      a1 epsilon fused with a2 SortTrace: a stable LSD partition of the bound
+//      events by bucket = top bits of hash(k0), so a bucket holds whole level-0
+//      subtrees and every slice u^D stays in trace order (reading A15).)
+//  unit_start
+//      work units = runs of consecutive buckets of ~kUnitTarget events.
 //  bucket_fast
 //      one CTA per bucket, everything in shared memory:
 //        a3 SpawnMonitors: dedup of value vectors (smem hash) = leaves
