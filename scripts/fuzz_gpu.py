@@ -69,18 +69,28 @@ def main():
         keys, letters = trace(rng, levels, n, len(prog.atoms))
         want = [oracle.run_offline(t, keys, project(letters, prog.atoms, oracle.Property(t).atoms)) for t in texts]
         online = rng.random() < 0.4
+        pipelined = online and rng.random() < 0.5  # ltl4c_verify_async, results read with a lag
         st = prog.state(0, online=online)
         if online:
-            cuts = sorted({0, n, *[rng.randint(0, n) for _ in range(rng.randint(0, 4))]})
+            cuts = sorted({0, n, *[rng.randint(0, n) for _ in range(rng.randint(0, 12))]})
         else:
             cuts = [0, n]
+        tickets = []
         for lo, hi in zip(cuts[:-1], cuts[1:]):
             k = [torch.from_numpy(x[lo:hi].view(np.int32)).to(dev) for x in keys]
-            got = st.verify(k, torch.from_numpy(letters[lo:hi]).to(dev), first_index=lo if online else None)
+            l = torch.from_numpy(letters[lo:hi]).to(dev)
+            if pipelined:
+                tickets.append(st.verify_async(k, l, first_index=lo))
+                if len(tickets) > 3:
+                    st.result(tickets.pop(0))
+            else:
+                got = st.verify(k, l, first_index=lo if online else None)
+        for t in tickets:
+            got = st.result(t)
         for f, w in enumerate(want):
             ok = got[f].verdict == w["verdict"] and np.array_equal(got[f].hist, w["hist"])
             if not ok:
-                print("MISMATCH", texts[f], n, levels, online, cuts, got[f].verdict, w["verdict"],
+                print("MISMATCH", texts[f], n, levels, online, pipelined, cuts, got[f].verdict, w["verdict"],
                       got[f].hist.tolist(), w["hist"].tolist(), flush=True)
                 sys.exit(1)
         cases += 1
