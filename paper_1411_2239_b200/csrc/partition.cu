@@ -169,12 +169,14 @@ __device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
 // order (match masks of all rounds first, then the per-warp digit counters),
 // scatters them into shared memory in digit order together with their global
 // position, and the tile is written out digit run by digit run (coalesced).
-template <int K, bool kDeep>
-__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
-  extern __shared__ __align__(16) uint8_t raw[];
-  SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
+//
+// kFirst: pass 0 (events may lack guard keys: the epsilon filter); kFull: a
+// tile without a ragged end (no range checks).  A later pass's input holds only
+// bound events, so a full tile of a later pass needs no validity test at all.
+template <int K, bool kDeep, bool kFirst, bool kFull>
+__device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, SweepSmem<K> &s) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const bool first = pass == 0;
+  constexpr bool first = kFirst;
   const uint32_t *const *in_key = first ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
   const uint8_t *in_let = first ? pl.in_let : pl.buf_let[(pass - 1) & 1];
   uint32_t *const *out_key = pl.buf_key[pass & 1];
@@ -191,7 +193,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const unsigned long long j = wbase + r * 32 + lane;
-    const bool in = j < n;
+    const bool in = kFull || j < n;
 #pragma unroll
     for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
     rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
@@ -217,8 +219,10 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     bool valid = true;
+    if (kFirst || !kFull) {
 #pragma unroll
-    for (int k = 0; k < K; ++k) valid &= rk[r][k] != kAbsent;
+      for (int k = 0; k < (kFirst ? K : 1); ++k) valid &= rk[r][k] != kAbsent;
+    }
     vd[r] = valid;
     dg[r] = valid ? (salted_bucket(rk[r][kDeep ? K - 1 : 0], pl.bits, pl.salt) >> lo) & dmask : 0u;
   }
@@ -305,6 +309,15 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
   }
 }
 
+template <int K, bool kDeep, bool kFirst>
+__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
+  extern __shared__ __align__(16) uint8_t raw[];
+  SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
+  const unsigned long long n = kFirst ? pl.n : *pl.nvalid;
+  if ((unsigned long long)(blockIdx.x + 1) * kTileEv <= n) scatter_tile<K, kDeep, kFirst, true>(pl, pass, s);
+  else scatter_tile<K, kDeep, kFirst, false>(pl, pass, s);
+}
+
 // off[c] = first position of bucket c in the final order, off[NB] = n.  Each
 // thread covers 16 consecutive positions (four 16-byte loads issued together).
 constexpr int kBoundsPer = 16;
@@ -375,8 +388,12 @@ cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {
 template <int K, bool kDeep>
 static cudaError_t scatter(const PartPlan &p, int pass, const Launcher &L) {
   const size_t sm = sizeof(SweepSmem<K>);
-  cudaFuncSetAttribute(part_scatter_kernel<K, kDeep>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K, kDeep><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
+  if (pass == 0) {
+    cudaFuncSetAttribute(part_scatter_kernel<K, kDeep, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K, kDeep, true><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
+  }
+  cudaFuncSetAttribute(part_scatter_kernel<K, kDeep, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  LTL4C_LAUNCH(kKPartScatter, part_scatter_kernel<K, kDeep, false><<<p.n_tiles, kPartThreads, sm, L.stream>>>(p, pass));
 }
 
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) {
