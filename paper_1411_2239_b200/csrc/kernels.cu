@@ -199,6 +199,27 @@ __device__ void order_segments(const Smem &s, int n, int C) {
   __syncthreads();
 }
 
+// (g o f) for monitors of at most NQB states (compile-time bound: the loop unrolls,
+// and maps of <= 8 states are 32-bit nibble vectors)
+template <int NQB>
+__device__ __forceinline__ unsigned long long map_apply_t(unsigned long long g, unsigned long long f) {
+  if constexpr (NQB <= 8) {
+    const uint32_t g32 = (uint32_t)g, f32 = (uint32_t)f;
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < NQB; ++q) r |= ((g32 >> (4 * ((f32 >> (4 * q)) & 15u))) & 15u) << (4 * q);
+    return r;
+  } else {
+    unsigned long long r = 0;
+#pragma unroll
+    for (int q = 0; q < NQB; ++q) {
+      const int fq = (int)((f >> (4 * q)) & 15ull);
+      r |= ((g >> (4 * fq)) & 15ull) << (4 * q);
+    }
+    return r;
+  }
+}
+
 __device__ __forceinline__ unsigned long long map_apply(unsigned long long g, unsigned long long f, int nq) {
   // (g o f)[q] = g[f[q]]
   unsigned long long r = 0;
@@ -1315,7 +1336,7 @@ struct alignas(16) SegTab {
   uint16_t llist[kSegW];
 };
 
-template <int K>
+template <int K, int NQB>
 __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
   using Tab = SegTab<K>;
   extern __shared__ __align__(16) uint8_t smem_raw[];
@@ -1432,9 +1453,9 @@ __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
               const unsigned long long o = __shfl_down_sync(0xffffffffu, m, d);
-              if ((lane & (2 * d - 1)) == 0) m = map_apply(o, m, nq);
+              if ((lane & (2 * d - 1)) == 0) m = map_apply_t<NQB>(o, m);
             }
-            if (lane == 0) w.lmap[s0] = map_apply(m, w.lmap[s0], nq);
+            if (lane == 0) w.lmap[s0] = map_apply_t<NQB>(m, w.lmap[s0]);
           } else {
             const uint32_t am = __ballot_sync(0xffffffffu, act);
             if (act) {
@@ -1445,7 +1466,7 @@ __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
                 while (pm) {
                   const int i = __ffs(pm) - 1;
                   pm &= pm - 1;
-                  m = map_apply(smap[lb[base + 32 * r + i]], m, nq);
+                  m = map_apply_t<NQB>(smap[lb[base + 32 * r + i]], m);
                 }
                 w.lmap[slot[r]] = m;
               }
@@ -1660,7 +1681,7 @@ __global__ void __launch_bounds__(256) heavy_short_kernel(HeavyParams h) {
 // bucket's contiguous item range, so partial maps are placed by item and
 // composed with an ordered tree reduction in shared memory.
 constexpr int kLongWin = 4096;
-template <int K>
+template <int K, int NQB>
 __global__ void __launch_bounds__(1024) heavy_long_kernel(HeavyParams h) {
   __shared__ unsigned long long M[kLongWin];
   __shared__ int acc[kMaxFormulas * (kMaxLevels + 1) * 6];
@@ -1718,10 +1739,10 @@ __global__ void __launch_bounds__(1024) heavy_long_kernel(HeavyParams h) {
       __syncthreads();
       for (int stride = 1; stride < kLongWin; stride <<= 1) {  // ordered tree: M[i] = M[i+s] o M[i]
         for (int x = tid * 2 * stride; x + stride < kLongWin; x += blockDim.x * 2 * stride)
-          M[x] = map_apply(M[x + stride], M[x], nq);
+          M[x] = map_apply_t<NQB>(M[x + stride], M[x]);
         __syncthreads();
       }
-      if (tid == 0) total = map_apply(M[0], total, nq);
+      if (tid == 0) total = map_apply_t<NQB>(M[0], total);
       __syncthreads();
     }
     if (tid == 0) heavy_leaf_done<K>(h, d, (int)((total >> (4 * prog->q0)) & 15ull), acc);
@@ -1947,34 +1968,42 @@ cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_leve
 }
 
 
-template <int K>
+template <int K, int NQB>
 static cudaError_t heavy_all(const HeavyParams &h, int nf, int n_sms, const Launcher &L) {
   if (L.before) L.before(L.ctx, kKHeavy);
   heavy_plan_kernel<<<1, 1024, 0, L.stream>>>(h);
   {
     const size_t sm = 8 * kMaxLetters + 8 * sizeof(SegTab<K>);
-    cudaFuncSetAttribute(heavy_segw_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(heavy_segw_kernel<K, NQB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy_segw_kernel<K>, 256, sm);
-    heavy_segw_kernel<K><<<n_sms * (per_sm > 0 ? per_sm : 1), 256, sm, L.stream>>>(h);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, heavy_segw_kernel<K, NQB>, 256, sm);
+    heavy_segw_kernel<K, NQB><<<n_sms * (per_sm > 0 ? per_sm : 1), 256, sm, L.stream>>>(h);
   }
   heavy_scan_blocks<<<2 * n_sms, 1024, 0, L.stream>>>(h);
   heavy_scan_sums<<<1, 1024, 0, L.stream>>>(h);
   heavy_scan_add<<<2 * n_sms, 1024, 0, L.stream>>>(h);
   heavy_group_kernel<<<4 * n_sms, 256, 0, L.stream>>>(h);
   heavy_short_kernel<K><<<4 * n_sms, 256, 0, L.stream>>>(h);
-  heavy_long_kernel<K><<<n_sms, 1024, 0, L.stream>>>(h);
+  heavy_long_kernel<K, NQB><<<n_sms, 1024, 0, L.stream>>>(h);
   for (int l = K - 1; l >= 1; --l) heavy_nodes_kernel<K><<<4 * n_sms, 256, 0, L.stream>>>(h, l);
   cudaError_t e = cudaGetLastError();
   if (L.after) L.after(L.ctx, kKHeavy);
   return e;
 }
 
-cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L) {
+template <int K>
+static cudaError_t heavy_nq(const HeavyParams &h, int nf, int nq, int n_sms, const Launcher &L) {
+  if (nq <= 2) return heavy_all<K, 2>(h, nf, n_sms, L);
+  if (nq <= 4) return heavy_all<K, 4>(h, nf, n_sms, L);
+  if (nq <= 8) return heavy_all<K, 8>(h, nf, n_sms, L);
+  return heavy_all<K, 16>(h, nf, n_sms, L);
+}
+
+cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int nq, int n_sms, const Launcher &L) {
   switch (K) {
-    case 1: return heavy_all<1>(h, nf, n_sms, L);
-    case 2: return heavy_all<2>(h, nf, n_sms, L);
-    default: return heavy_all<3>(h, nf, n_sms, L);
+    case 1: return heavy_nq<1>(h, nf, nq, n_sms, L);
+    case 2: return heavy_nq<2>(h, nf, nq, n_sms, L);
+    default: return heavy_nq<3>(h, nf, nq, n_sms, L);
   }
 }
 

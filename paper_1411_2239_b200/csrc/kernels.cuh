@@ -166,7 +166,7 @@ cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t gr
 // medium-bucket kernel (cfg[2..3])
 cudaError_t bucket_warp_config(int K, int nf, int nq, int na, int *cfg);
 uint32_t bucket_warp_hdr(int nq, int na);  // CTA header bytes of the warp kernels
-cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int n_sms, const Launcher &L);
+cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int nq, int n_sms, const Launcher &L);
 cudaError_t launch_online_leaf(const OnlineParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 cudaError_t launch_online_nodes(const OnlineParams &p, int nf, int l, uint32_t grid, const Launcher &L);
 cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {warps/CTA, CTAs/SM}

@@ -398,7 +398,7 @@ ltl4c_status run_heavy(ltl4c_state *st, const BucketParams &bp, int K, cudaStrea
   CU(cudaMemsetAsync(h.leaf_fill, 0, sizeof(uint32_t) * ev, s));
   CU(cudaMemsetAsync(h.ctr, 0, sizeof(uint32_t) * 8, s));
   CU(cudaMemsetAsync(c, 0, sizeof(unsigned long long) * 16, s));
-  CU(launch_heavy(h, K, (int)st->prog->n_formulas, st->n_sms, L));
+  CU(launch_heavy(h, K, (int)st->prog->n_formulas, (int)st->prog->n_states, st->n_sms, L));
   return LTL4C_OK;
 }
 
