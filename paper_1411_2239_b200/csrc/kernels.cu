@@ -1686,7 +1686,7 @@ __global__ void __launch_bounds__(1024) heavy_long_kernel(HeavyParams h) {
   __shared__ unsigned long long M[kLongWin];
   __shared__ int acc[kMaxFormulas * (kMaxLevels + 1) * 6];
   __shared__ uint32_t red[32];
-  __shared__ uint32_t leaf_i;
+  __shared__ uint32_t leaf_i, span_all;
   const DevProg *prog = h.prog;
   const int nq = prog->nq, tid = threadIdx.x;
   unsigned long long ident = 0;
@@ -1723,10 +1723,10 @@ __global__ void __launch_bounds__(1024) heavy_long_kernel(HeavyParams h) {
     if (tid < 32) {
       uint32_t v = tid < (int)(blockDim.x >> 5) ? red[tid] : 0u;
       for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
-      if (tid == 0) red[1] = v;
+      if (tid == 0) span_all = v;  // not red[1]: lane 1 reads that slot above
     }
     __syncthreads();
-    const uint32_t nspan = red[1];
+    const uint32_t nspan = span_all;
     for (uint32_t w0 = 0; w0 < nspan; w0 += kLongWin) {
       for (int x = tid; x < kLongWin; x += blockDim.x) M[x] = ident;
       __syncthreads();
