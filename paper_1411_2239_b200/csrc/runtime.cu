@@ -51,7 +51,12 @@ struct DevBuf {
     n = 0;
     size_t cap = std::max<size_t>(want, 1);
     cudaError_t e = cudaMalloc((void **)&p, cap * sizeof(T));
-    if (e == cudaSuccess) n = cap;
+    if (e != cudaSuccess) return e;
+    n = cap;
+    // zero once per allocation: 16-byte staging loads read the padding past N and the
+    // result copy reads unused DevOut fields (harmless values, but defined for initcheck)
+    e = cudaMemset(p, 0, cap * sizeof(T));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);
     return e;
   }
   void release() {

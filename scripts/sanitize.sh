@@ -4,7 +4,7 @@
 set -u
 mkdir -p gpurun_out
 N=${N:-40000}
-for tool in memcheck racecheck synccheck; do
+for tool in memcheck racecheck synccheck initcheck; do
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 9 --print-limit 50 \
     python scripts/sanitize_cases.py $N > gpurun_out/sanitize_$tool.log 2>&1
   echo "$tool rc=$?" | tee -a gpurun_out/sanitize_summary.txt
