@@ -14,6 +14,6 @@ import json
 for l in open("gpurun_out/sweep.log"):
     if l.startswith("=="): print(l.strip())
     elif l.startswith("{"):
-        d = json.loads(l); print(" ms %.4f" % d["ms_per_step"], {k: round(v, 3) for k, v in d["roofline"]["kernel_share"].items()})
+        d = json.loads(l); print(" ms %.4f" % d["ms_per_step"], {k: round(v, 3) for k, v in d.get("roofline", {}).get("kernel_share", {}).items()})
     elif "rror" in l: print(l[:300])
 PY
