@@ -40,7 +40,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (plain C11, -O2)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-Wall", "-pthread",
                                "-Wno-format-truncation", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
@@ -73,6 +73,9 @@ def lib():
             L.orc_evaluate.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), c_u64p,
                                        c_u64p, c_u64p]
             L.orc_node_verdict.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p]
+            L.orc_run_threads.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p),
+                                          ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_u64p,
+                                          c_u64p, c_u64p]
             _lib = L
     return _lib
 
@@ -176,8 +179,25 @@ class Monitor:
         return lib().orc_node_verdict(self._h, len(arr), arr.ctypes.data if len(arr) else None)
 
 
-def run_offline(text: str, keys, letters) -> dict:
+def run_offline(text: str, keys, letters, threads: int = 1) -> dict:
+    """Algorithm 1 offline.  threads > 1: the timing mode (orc_run_threads), level-0
+    subtrees partitioned by a hash of k0 over `threads` host threads."""
     p = Property(text)
-    m = Monitor(p)
-    m.feed(keys, letters)
-    return m.evaluate()
+    if threads <= 1 or p.levels < 1:
+        m = Monitor(p)
+        m.feed(keys, letters)
+        return m.evaluate()
+    n = p.levels
+    letters = np.ascontiguousarray(letters, dtype=np.uint8)
+    ks = [np.ascontiguousarray(k, dtype=np.uint32) for k in keys[:n]]
+    ptrs = (ctypes.c_void_p * MAX_LEVELS)()
+    for i in range(n):
+        ptrs[i] = ks[i].ctypes.data
+    v = ctypes.c_int()
+    hist = (ctypes.c_uint64 * ((MAX_LEVELS + 1) * 6))()
+    seen, bound = ctypes.c_uint64(), ctypes.c_uint64()
+    rc = lib().orc_run_threads(p._h, letters.shape[0], ptrs, letters.ctypes.data, int(threads),
+                               ctypes.byref(v), hist, ctypes.byref(seen), ctypes.byref(bound))
+    assert rc == 0
+    h = np.array(list(hist), dtype=np.uint64).reshape(MAX_LEVELS + 1, 6)[: n + 1]
+    return {"verdict": v.value, "hist": h, "events_seen": seen.value, "events_bound": bound.value}

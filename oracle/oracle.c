@@ -25,6 +25,7 @@
 #include "oracle.h"
 
 #include <ctype.h>
+#include <pthread.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1046,4 +1047,81 @@ int orc_node_verdict(orc_monitor *m, int m_len, const uint32_t *prefix) {
   int64_t id = vmap_find(&m->level[m_len], prefix);
   if (id < 0) return -1;
   return m->lvl_verdict[m_len][id];
+}
+
+/* ------------------------------------------------------------------------ */
+/* Timing mode: T threads, level-0 subtrees partitioned by a hash of k0.    */
+/* Every node below the root has a value vector starting with k0 (P), */
+/* so thread t's monitor holds exactly the subtrees whose k0 it owns and    */
+/* the depth-l node counts (l >= 1) are sums over threads; the root's        */
+/* children are the depth-1 nodes, so the root verdict is Def. 6 applied to  */
+/* the summed depth-1 histogram (the same orc_rule).                         */
+/* ------------------------------------------------------------------------ */
+typedef struct {
+  const orc_prop *p;
+  uint64_t n;
+  const uint32_t *const *keys;
+  const uint8_t *letters;
+  int t, T;
+  int verdict;
+  uint64_t hist[ORC_MAX_LEVELS + 1][6];
+  uint64_t seen, bound;
+} orc_job_t;
+
+static uint32_t owner_of(uint32_t k0, int T) {
+  uint64_t h = (uint64_t)k0 * 0x9E3779B97F4A7C15ull;
+  return (uint32_t)((h >> 32) % (uint64_t)T);
+}
+
+static void *orc_job(void *arg) {
+  orc_job_t *j = (orc_job_t *)arg;
+  orc_monitor *m = orc_monitor_new(j->p);
+  int n = j->p->nq;
+  const uint64_t chunk = 1u << 16;
+  uint32_t *kb[ORC_MAX_LEVELS];
+  for (int i = 0; i < n; i++) kb[i] = (uint32_t *)malloc(sizeof(uint32_t) * chunk);
+  uint8_t *lb = (uint8_t *)malloc(chunk);
+  /* feed this thread's events in trace order, in chunks */
+  for (uint64_t lo = 0; lo < j->n; lo += chunk) {
+    uint64_t hi = lo + chunk < j->n ? lo + chunk : j->n, c = 0;
+    for (uint64_t e = lo; e < hi; e++) {
+      if (owner_of(j->keys[0][e], j->T) != (uint32_t)j->t) continue;
+      for (int i = 0; i < n; i++) kb[i][c] = j->keys[i][e];
+      lb[c++] = j->letters[e];
+    }
+    orc_feed(m, c, (const uint32_t *const *)kb, lb);
+  }
+  orc_evaluate(m, &j->verdict, j->hist, &j->seen, &j->bound);
+  orc_monitor_free(m);
+  for (int i = 0; i < n; i++) free(kb[i]);
+  free(lb);
+  return NULL;
+}
+
+int orc_run_threads(const orc_prop *p, uint64_t n, const uint32_t *const *keys, const uint8_t *letters,
+                    int T, int *verdict, uint64_t hist[ORC_MAX_LEVELS + 1][6], uint64_t *events_seen,
+                    uint64_t *events_bound) {
+  if (T < 1 || p->nq < 1) return -1;
+  orc_job_t *jobs = (orc_job_t *)calloc((size_t)T, sizeof(orc_job_t));
+  pthread_t *th = (pthread_t *)calloc((size_t)T, sizeof(pthread_t));
+  for (int t = 0; t < T; t++) {
+    jobs[t].p = p; jobs[t].n = n; jobs[t].keys = keys; jobs[t].letters = letters;
+    jobs[t].t = t; jobs[t].T = T;
+    if (T == 1) orc_job(&jobs[0]);
+    else pthread_create(&th[t], NULL, orc_job, &jobs[t]);
+  }
+  if (T > 1) for (int t = 0; t < T; t++) pthread_join(th[t], NULL);
+  memset(hist, 0, sizeof(uint64_t) * (ORC_MAX_LEVELS + 1) * 6);
+  *events_bound = 0;
+  for (int t = 0; t < T; t++) {
+    for (int l = 1; l <= p->nq; l++)
+      for (int v = 0; v < 6; v++) hist[l][v] += jobs[t].hist[l][v];
+    *events_bound += jobs[t].bound;
+  }
+  const quant_t *q = &p->q[0];
+  *verdict = orc_rule(q->kind, q->cmp, q->num, q->den, hist[1]);
+  hist[0][*verdict] = 1;
+  *events_seen = n;
+  free(jobs); free(th);
+  return 0;
 }

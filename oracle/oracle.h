@@ -69,6 +69,13 @@ int  orc_evaluate(orc_monitor *m, int *verdict, uint64_t hist[ORC_MAX_LEVELS + 1
  * returns -1 if the vector is not in the tree (after orc_evaluate) */
 int  orc_node_verdict(orc_monitor *m, int m_len, const uint32_t *prefix);
 
+/* Timing mode: the same result computed by T threads,
+ * level-0 subtrees partitioned by a hash of k0 (results identical for every T). */
+int  orc_run_threads(const orc_prop *p, uint64_t n, const uint32_t *const *keys,
+                     const uint8_t *letters, int T, int *verdict,
+                     uint64_t hist[ORC_MAX_LEVELS + 1][6], uint64_t *events_seen,
+                     uint64_t *events_bound);
+
 #ifdef __cplusplus
 }
 #endif

@@ -175,14 +175,6 @@ class Program:
     def state(self, device: int = 0, online: bool = False, capacity: int = 0) -> "State":
         return State(self, device, online, capacity)
 
-    def run_word(self, word) -> list[int]:
-        """Host-side replay of the monitor tables on one word (for table checks;
-        the verification path itself runs on the GPU)."""
-        q = self.initial
-        for a in word:
-            q = int(self.delta[q, a])
-        return [int(self.label[f, q]) for f in range(self.n_formulas)]
-
 
 def compile(text: str) -> Program:  # noqa: A001 (mirrors ltl4c_compile)
     h = ctypes.c_void_p()

@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
             const int v = w.pleaf[i];
             if (v) atomicAdd(&sacc[((i / 6) * (kMaxLevels + 1) + K) * 6 + i % 6], (uint32_t)v);
           }
-          since += kWarpCap / 32;
+          since += CAP / 32;  // a lane adds at most CAP / 32 leaves per unit (16-bit fields)
           if (since > 60000u) { flush_lcp(); since = 0; }
           // a5 (ii): node verdicts by Def. 6, depth K-1 .. 1
           for (int l = K - 1; l >= 1; --l) {

@@ -45,6 +45,7 @@ struct PartPlan {
   uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
   uint32_t *counts;                     // [kMaxDigits][n_tiles] tile counts, scanned in place
   int rank_ballot;                      // stable rank by per-bit ballots instead of match.any
+  uint32_t let_mask;                    // (1 << n_atoms) - 1: pass 0 drops letter bits of no atom
   unsigned long long *nvalid;           // bound events of this batch
   DevAcc *acc;
 };

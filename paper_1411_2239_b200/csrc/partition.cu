@@ -196,7 +196,7 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
     const bool in = kFull || j < n;
 #pragma unroll
     for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
-    rl[r] = in ? __ldcs(&in_let[j]) : (uint8_t)0;
+    rl[r] = in ? (uint8_t)(__ldcs(&in_let[j]) & (kFirst ? pl.let_mask : 0xFFu)) : (uint8_t)0;
   }
   // digits 2t, 2t+1 belong to thread t < kMaxDigits / 2: global run start =
   // pass base (scan of the digit totals) + the tile's offset within the digit

@@ -191,6 +191,12 @@ struct ltl4c_state {
   void *comm = nullptr;
   int n_ranks = 1, rank = 0, owner_bits = 0;
   bool force_exchange = false;  // LTL4C_FORCE_EXCHANGE: run the exchange path with 1 rank (tests)
+  // tuning / test knobs, read from the environment once per state (ltl4c_state_create)
+  uint64_t bucket_mul = 6;         // LTL4C_BUCKET_MUL: buckets per kWarpCap events
+  int max_bits = kMaxPasses * kMaxDigitBits;  // LTL4C_MAX_BITS: cap on the bucket bits
+  bool max_bits_set = false;
+  uint32_t warp_grid = 0;          // LTL4C_WARP_GRID: cap on the warp kernels' grids (0 = none)
+  int rank_ballot = 1;             // LTL4C_RANK_BALLOT: stable rank by ballots (1) or match.any (0)
   DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
   DevBuf<uint32_t> exkey[kMaxLevels];
   DevBuf<uint8_t> exlet;
@@ -413,26 +419,18 @@ struct Plan {
   uint32_t NB = 0, n_tiles = 0;
 };
 
-static int rank_ballot() {
-  static const int v = std::getenv("LTL4C_RANK_BALLOT") ? std::atoi(std::getenv("LTL4C_RANK_BALLOT")) : 1;
-  return v;
-}
-
 // Buffer sizes for a batch of N events (all allocation happens here, outside
 // any stream capture).
 ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   const int K = (int)st->prog->n_levels;
   pl->N = N;
   if (N == 0) return LTL4C_OK;
-  static const uint64_t mul = std::getenv("LTL4C_BUCKET_MUL") ? std::atoi(std::getenv("LTL4C_BUCKET_MUL")) : 6;
-  const uint64_t target = std::max<uint64_t>(2, (mul * N + kWarpCap - 1) / kWarpCap);
-  static const int max_bits = std::getenv("LTL4C_MAX_BITS") ? std::atoi(std::getenv("LTL4C_MAX_BITS"))
-                                                             : kMaxPasses * kMaxDigitBits;
-  pl->B = std::min(std::min(kMaxPasses * kMaxDigitBits, max_bits), std::max(1, ceil_log2(target)));
+  const uint64_t target = std::max<uint64_t>(2, (st->bucket_mul * N + kWarpCap - 1) / kWarpCap);
+  pl->B = std::min(std::min(kMaxPasses * kMaxDigitBits, st->max_bits), std::max(1, ceil_log2(target)));
   // one level (leaves only, no node tables in the warp kernels): two partition
   // passes with larger buckets beat a third pass (C3: 5.17 -> 4.62 ms; with inner
   // levels the medium tiers fill up instead: C4 9.43 -> 10.0 ms)
-  if (K == 1 && !(st->flags & LTL4C_STATE_ONLINE) && !std::getenv("LTL4C_MAX_BITS"))
+  if (K == 1 && !(st->flags & LTL4C_STATE_ONLINE) && !st->max_bits_set)
     pl->B = std::min(pl->B, 2 * kMaxDigitBits);
   pl->P = (pl->B + kMaxDigitBits - 1) / kMaxDigitBits;
   pl->NB = 1u << pl->B;
@@ -449,6 +447,13 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
   return LTL4C_OK;
+}
+
+// grid of a warp kernel: every resident CTA slot (LTL4C_WARP_GRID caps it: tests
+// that push many units through one warp)
+uint32_t warp_grid(const ltl4c_state *st, int ctas_per_sm) {
+  const uint32_t g = (uint32_t)(st->n_sms * ctas_per_sm);
+  return st->warp_grid ? std::min(g, st->warp_grid) : g;
 }
 
 BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
@@ -503,7 +508,8 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.hk = online ? K - 1 : 0;  // online: buckets by the deepest key (balanced leaves)
     pl.hcol[0] = pl.buf_key[0][pl.hk];
     pl.hcol[1] = pl.buf_key[1][pl.hk];
-    pl.rank_ballot = rank_ballot();
+    pl.rank_ballot = st->rank_ballot;
+    pl.let_mask = (1u << prog->n_atoms) - 1u;
     pl.passes = plan.P;
     int lo = 0;
     for (int pass = 0; pass < plan.P; ++pass) {
@@ -528,7 +534,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       // kernel with kWarpCapBig, above that to the CTA kernel, and above kCap to
       // the heavy path (after the first result copy)
       CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
-      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, (uint32_t)(st->n_sms * st->warp_cfg[1]), L));
+      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[1]), L));
       BucketParams mp = bp;
       mp.list = st->medium_list.p;
       mp.list_len = &st->d_acc.p->medium_buckets;
@@ -536,7 +542,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       mp.spill_len = &st->d_acc.p->large_buckets;
       mp.bucket_counter = bp.bucket_counter + 1;
       mp.warps_per_cta = st->warp_cfg[2];
-      CU(launch_bucket_warp(mp, K, (int)prog->n_formulas, (uint32_t)(st->n_sms * st->warp_cfg[3]), L));
+      CU(launch_bucket_warp(mp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[3]), L));
       BucketParams fp = bp;
       fp.list = st->large_list.p;
       fp.list_len = &st->d_acc.p->large_buckets;
@@ -601,7 +607,8 @@ ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_
     pl.hk = 0;  // owner rank by level-0 key: whole subtrees per rank
     pl.hcol[0] = pl.buf_key[0][0];
     pl.hcol[1] = pl.buf_key[1][0];
-    pl.rank_ballot = rank_ballot();
+    pl.rank_ballot = st->rank_ballot;
+    pl.let_mask = (1u << st->prog->n_atoms) - 1u;
     pl.lo[0] = 0;
     pl.width[0] = st->owner_bits;
     pl.digit_hist = st->totals.p;
@@ -697,23 +704,25 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   Launcher L{s, before_launch, after_launch, st};
   if (!online) st->events_seen = 0;
   st->events_seen += N;
-  if (online) {
-    ltl4c_status r = ensure_online_tables(st, N, s, L);
-    if (r) return r;
-    for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
-    CU(st->tcnt.ensure(kMaxLevels));
-    if (++st->batch_id == 0) st->batch_id = 1;  // wrap: marks of batch 0 never exist
-    st->enq_events += N;
-  }
   const bool comm = st->comm && (st->n_ranks > 1 || st->force_exchange);
   uint64_t Nloc = N;
   const uint32_t *lkeys[kMaxLevels] = {keys[0], K > 1 ? keys[1] : nullptr, K > 2 ? keys[2] : nullptr};
   const uint8_t *llet = letters;
   if (comm) {
+    // route first: this rank then verifies the Nloc events it owns (up to G x N
+    // when level-0 keys are skewed), and the carried tables are sized for those
     ltl4c_status r = exchange(st, keys, letters, N, s, L, &Nloc);
     if (r) return r;
     for (int l = 0; l < K; ++l) lkeys[l] = st->exkey[l].p;
     llet = st->exlet.p;
+  }
+  if (online) {
+    ltl4c_status r = ensure_online_tables(st, Nloc, s, L);
+    if (r) return r;
+    for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
+    CU(st->tcnt.ensure(kMaxLevels));
+    if (++st->batch_id == 0) st->batch_id = 1;  // wrap: marks of batch 0 never exist
+    st->enq_events += Nloc;
   }
   Plan plan;
   {
@@ -746,6 +755,18 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   if (use_graph) {
     std::vector<uintptr_t> key = {(uintptr_t)N, (uintptr_t)letters};
     for (int l = 0; l < K; ++l) key.push_back((uintptr_t)keys[l]);
+    // the captured launches bake in every buffer pointer: a buffer reallocated by an
+    // ungraphed verify in between (profiling, another size) must not be replayed
+    for (int i = 0; i < 2; ++i) {
+      for (int l = 0; l < K; ++l) key.push_back((uintptr_t)st->bufkey[i][l].p);
+      key.push_back((uintptr_t)st->buflet[i].p);
+    }
+    for (const void *b : {(const void *)st->counts.p, (const void *)st->totals.p, (const void *)st->bucket_off.p,
+                          (const void *)st->oversize_list.p, (const void *)st->medium_list.p,
+                          (const void *)st->large_list.p, (const void *)st->unit_start.p,
+                          (const void *)st->d_acc.p, (const void *)st->d_out.p, (const void *)st->d_nvalid.p,
+                          (const void *)st->d_prog.p, (const void *)st->h_out})
+      key.push_back((uintptr_t)b);
     if (st->graph_key != key || !st->graph_exec) {
       drop_graph(st);
       if (!st->cap_stream) CU(cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking));
@@ -884,6 +905,13 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   st->flags = flags;
   st->graphs = std::getenv("LTL4C_NO_GRAPH") == nullptr;
   st->force_exchange = std::getenv("LTL4C_FORCE_EXCHANGE") != nullptr;
+  if (const char *e = std::getenv("LTL4C_BUCKET_MUL")) st->bucket_mul = std::max(1, std::atoi(e));
+  if (const char *e = std::getenv("LTL4C_MAX_BITS")) {
+    st->max_bits = std::max(1, std::min(kMaxPasses * kMaxDigitBits, std::atoi(e)));
+    st->max_bits_set = true;
+  }
+  if (const char *e = std::getenv("LTL4C_WARP_GRID")) st->warp_grid = (uint32_t)std::max(0, std::atoi(e));
+  if (const char *e = std::getenv("LTL4C_RANK_BALLOT")) st->rank_ballot = std::atoi(e);
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;
@@ -1057,10 +1085,14 @@ ltl4c_status ltl4c_state_reset(ltl4c_state *st) {
   int prev = 0;
   cudaGetDevice(&prev);
   CU(cudaSetDevice(st->device));
-  CU(cudaMemset(st->d_acc.p, 0, sizeof(DevAcc)));
-  std::memset(st->h_out, 0, sizeof(DevOut));
-  for (int i = 0; i < ltl4c_state::kRing; ++i)  // drain pipelined batches
+  // drain every batch still in flight (pipelined batches may run on a non-blocking
+  // stream) before the accumulators are cleared on that stream
+  for (int i = 0; i < ltl4c_state::kRing; ++i)
     if (st->ring_ticket[i]) { cudaEventSynchronize(st->ring_ev[i]); st->ring_ticket[i] = 0; }
+  CU(cudaStreamSynchronize(st->cur_stream));
+  CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), st->cur_stream));
+  CU(cudaStreamSynchronize(st->cur_stream));
+  std::memset(st->h_out, 0, sizeof(DevOut));
   st->outstanding = 0;
   st->known_leaves = st->known_cum = st->enq_events = 0;
   for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = 0;

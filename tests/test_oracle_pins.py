@@ -511,3 +511,128 @@ def test_parse_defaults_P224():
     assert oracle.Property("forall[>=50%] f : intrace(f) => true").quantifier(0)["den"] == 2
     p = oracle.Property("forall x : user(x) => (exists[<=3] r : rid(r) => (login && unauthorized))")
     assert p.levels == 2
+
+
+# ---------------------------------------------------------------- rule order (A3)
+def test_rule_overlapping_rows_golden_A3():
+    """Rows of Def. 6 that overlap for '=': the hand-derived verdicts of
+    tests/golden/rule_order.txt under reading A3 (SPEC's order is recorded beside)."""
+    n = 0
+    for line in open(os.path.join(GOLDEN, "rule_order.txt")):
+        r = line.split("#")[0].split()
+        if not r:
+            continue
+        h = [int(x) for x in r[3:9]]
+        assert oracle.rule(r[0], r[1], int(r[2]), 1, h) == NAME[r[9]], r
+        n += 1
+    assert n >= 6
+
+
+# ---------------------------------------------------------------- timing mode
+@pytest.mark.parametrize("threads", [2, 3, 8])
+def test_threads_mode_identical(threads):
+    """the level-0 hash partition over host threads gives the
+    same verdict and counts as the sequential run, for every thread count."""
+    rng = random.Random(1411 + threads)
+    for case in range(25):
+        levels = rng.randint(1, 3)
+        ops = ["<", "<=", ">", ">=", "="]
+        prefix = ""
+        for i in range(levels):
+            if rng.random() < 0.5:
+                prefix += f"forall[{rng.choice(ops)}{rng.choice(['0', '0.5', '1', '0.75'])}] x{i} : k{i}(x{i}) => "
+            else:
+                prefix += f"exists[{rng.choice(ops)}{rng.randint(0, 3)}] x{i} : k{i}(x{i}) => "
+        text = prefix + rng.choice(["a", "F a", "G (a -> F b)", "a U b", "X a && b"])
+        keys, letters = tracegen.random_property_trace(case, levels, rng.choice([0, 1, 50, 2000]),
+                                                       values=rng.choice([2, 5, 40]), atoms=2)
+        a = oracle.run_offline(text, keys, letters)
+        b = oracle.run_offline(text, keys, letters, threads=threads)
+        assert a["verdict"] == b["verdict"] and np.array_equal(a["hist"], b["hist"]), text
+        assert a["events_bound"] == b["events_bound"] and a["events_seen"] == b["events_seen"]
+
+
+# ---------------------------------------------------------------- three levels (C5)
+def _first_events(keys, letters):
+    """(key tuples, letter) of the first event of every bound value vector."""
+    k = [np.asarray(x) for x in keys]
+    ok = np.ones(k[0].shape[0], bool)
+    for x in k:
+        ok &= x != tracegen.ABSENT
+    k = [x[ok] for x in k]
+    a = np.asarray(letters)[ok]
+    order = np.lexsort((np.arange(a.shape[0]), *k[::-1]))
+    sk = [x[order] for x in k]
+    first = np.ones(a.shape[0], bool)
+    first[1:] = np.any([x[1:] != x[:-1] for x in sk], axis=0) if a.shape[0] else first[1:]
+    return [x[first] for x in sk], a[order][first]
+
+
+def _group_any(keys, flag):
+    """per distinct key tuple: any(flag) (keys sorted lexicographically)."""
+    order = np.lexsort(keys[::-1])
+    sk = [x[order] for x in keys]
+    start = np.ones(flag.shape[0], bool)
+    start[1:] = np.any([x[1:] != x[:-1] for x in sk], axis=0)
+    seg = np.cumsum(start) - 1
+    out = np.zeros(int(seg[-1]) + 1 if flag.shape[0] else 0, bool)
+    np.logical_or.at(out, seg, flag[order])
+    return [x[start] for x in sk], out
+
+
+def _group_count(keys, flag):
+    order = np.lexsort(keys[::-1])
+    sk = [x[order] for x in keys]
+    start = np.ones(flag.shape[0], bool)
+    start[1:] = np.any([x[1:] != x[:-1] for x in sk], axis=0)
+    seg = np.cumsum(start) - 1
+    return [x[start] for x in sk], np.bincount(seg, weights=flag[order].astype(np.float64)).astype(np.int64)
+
+
+@pytest.mark.parametrize("seed,p_admin,p_ext", [(0, 0.01, 0.05), (1, 0.0005, 0.01)])
+def test_three_level_closed_form_c(seed, p_admin, p_ext):
+    """C5 formula (c): A_{>=0.99} h => E_{=0} u => E s => (admin && external).
+    Hand-derived: leaf (h,u,s) is T iff the slice's first event has admin & external,
+    else F (Def. 4); (h,u) [E, default >= 1, P:226] is T iff one T session, else Fc
+    (Table 1 '>=' latch); h [E_{=0}] is F iff one T child (Table 1 '=': > 0),
+    else Tc; root [A_{>=0.99}] is Tc iff 100 * #Tc-hosts >= 99 * #hosts, else Fc
+    (no A latch for k in (0,1), children are only F / Tc)."""
+    tr = tracegen.c5_trace(seed=seed, n=400_000, hosts=64, users=3000, span_events=100_000,
+                           p=(0.01, 0.3, 0.3, p_admin, p_ext))
+    text = tracegen.C5_FORMULAS[2]
+    lk, la = _first_events(tr.keys, tr.letters)
+    leaf_t = (la & 0x18) == 0x18               # admin = bit 3, external = bit 4 of the C5 union
+    prop = oracle.Property(text)
+    assert prop.atoms == ["admin", "external"]
+    r = oracle.run_offline(text, tr.keys, ((tr.letters >> 3) & 3).astype(np.uint8))
+    hu, hu_t = _group_any(lk[:2], leaf_t)
+    h, h_bad = _group_any(hu[:1], hu_t)
+    root = Tc if 100 * int((~h_bad).sum()) >= 99 * h_bad.shape[0] else Fc
+    assert list(r["hist"][3][[T, F]]) == [leaf_t.sum(), (~leaf_t).sum()] and r["hist"][3].sum() == leaf_t.shape[0]
+    assert list(r["hist"][2][[T, Fc]]) == [hu_t.sum(), (~hu_t).sum()] and r["hist"][2].sum() == hu_t.shape[0]
+    assert list(r["hist"][1][[F, Tc]]) == [h_bad.sum(), (~h_bad).sum()] and r["hist"][1].sum() == h_bad.shape[0]
+    assert r["verdict"] == root
+
+
+def test_three_level_closed_form_a():
+    """C5 formula (a): A_{>=0.95} h => A u => E_{<=2} s => F authfail.
+    Leaf T once authfail occurs in the slice, else Fp (Def. 4 of F x);
+    (h,u) [E_{<=2}] is F iff > 2 T sessions (Table 1 '<='), else Tc; h [A = A_{=1}]
+    is F iff one F child, else Tc; root Tc iff 100 * #Tc >= 95 * #hosts, else Fc."""
+    tr = tracegen.c5_trace(seed=3, n=300_000, hosts=32, users=400, span_events=100_000,
+                           p=(0.0008, 0.3, 0.3, 0.01, 0.05))
+    text = tracegen.C5_FORMULAS[0]
+    assert oracle.Property(text).atoms == ["authfail"]
+    k = list(tr.keys)
+    ok = (k[0] != tracegen.ABSENT) & (k[1] != tracegen.ABSENT) & (k[2] != tracegen.ABSENT)
+    lk, leaf_t = _group_any([x[ok] for x in k], (tr.letters[ok] & 1) == 1)
+    hu, ntrue = _group_count(lk[:2], leaf_t)
+    hu_bad = ntrue > 2
+    h, h_bad = _group_any(hu[:1], hu_bad)
+    root = Tc if 100 * int((~h_bad).sum()) >= 95 * h_bad.shape[0] else Fc
+    r = oracle.run_offline(text, tr.keys, (tr.letters & 1).astype(np.uint8))
+    assert list(r["hist"][3][[T, Fp]]) == [leaf_t.sum(), (~leaf_t).sum()]
+    assert list(r["hist"][2][[F, Tc]]) == [hu_bad.sum(), (~hu_bad).sum()]
+    assert list(r["hist"][1][[F, Tc]]) == [h_bad.sum(), (~h_bad).sum()]
+    assert r["verdict"] == root
+    assert 0 < h_bad.sum() < h_bad.shape[0]  # both host verdicts occur

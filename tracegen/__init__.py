@@ -57,19 +57,6 @@ def _ids(rng: np.random.Generator, count: int) -> np.ndarray:
     return v
 
 
-def _zipf_ranks(rng: np.random.Generator, n: int, support: int, s: float) -> np.ndarray:
-    w = np.arange(1, support + 1, dtype=np.float64) ** (-s)
-    cdf = np.cumsum(w)
-    cdf /= cdf[-1]
-    out = np.empty(n, dtype=np.int64)
-    chunk = 1 << 24
-    for lo in range(0, n, chunk):
-        hi = min(n, lo + chunk)
-        out[lo:hi] = np.searchsorted(cdf, rng.random(hi - lo), side="right")
-    np.minimum(out, support - 1, out=out)
-    return out
-
-
 def socket_trace(seed: int = 0, n: int = 10_000, sockets: int = 100, noise: float = 0.02,
                  p_receive: float = 0.04, p_respond: float = 0.95, p_drop: float = 0.005) -> Trace:
     """C1: web-server socket trace. bit0 = receive(s), bit1 = respond(s).
@@ -153,42 +140,105 @@ def login_trace(seed: int = 0, n: int = 10_000_000, users: int = 100_000, p_logi
                  {"config": "C2", "seed": seed, "users": users, "variant": variant})
 
 
+BLOCK = 1 << 20  # events per independently generated block (C3, C4): any slice [lo, hi)
+                 # of a trace can be generated alone (multi-GPU ranks generate their own)
+
+
+def _blocks(n: int, lo: int, hi, fn):
+    """Run fn(b, a, z) for every block b intersecting [lo, hi) (a, z = the part of
+    block b inside the slice, block-relative), in parallel threads; returns the
+    results in block order."""
+    from concurrent.futures import ThreadPoolExecutor
+    hi = n if hi is None else hi
+    assert 0 <= lo <= hi <= n
+    jobs = []
+    for b in range(lo // BLOCK, (hi + BLOCK - 1) // BLOCK):
+        a0, z0 = max(lo, b * BLOCK) - b * BLOCK, min(hi, (b + 1) * BLOCK) - b * BLOCK
+        jobs.append((b, a0, z0))
+    if len(jobs) <= 1:
+        return [fn(*j) for j in jobs]
+    import os
+    with ThreadPoolExecutor(max_workers=min(len(jobs), max(1, (os.cpu_count() or 1)))) as ex:
+        return list(ex.map(lambda j: fn(*j), jobs))
+
+
+def _zipf_cdf(support: int, s: float) -> np.ndarray:
+    w = np.arange(1, support + 1, dtype=np.float64) ** (-s)
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    return cdf
+
+
 def zipf_socket_trace(seed: int = 0, n: int = 100_000_000, support: int = 1 << 20, s: float = 1.1,
-                      p_receive: float = 0.3, p_respond: float = 0.3, formula: str = SOCKET) -> Trace:
+                      p_receive: float = 0.3, p_respond: float = 0.3, formula: str = SOCKET,
+                      lo: int = 0, hi=None) -> Trace:
     """C3: Zipf(s)-skewed keys over `support` ids; i.i.d. letters over {receive, respond}
-    (the G(r -> F s) automaton has two non-trap states, so every event does work)."""
-    rng = np.random.default_rng(SEED_BASE + 3 + seed)
-    ranks = _zipf_ranks(rng, n, support, s)
-    ids = _ids(rng, support)
-    keys = ids[ranks]
-    letters = ((rng.random(n) < p_receive).astype(np.uint8)
-               | ((rng.random(n) < p_respond).astype(np.uint8) << 1))
-    return Trace(formula, [keys], letters, {"config": "C3", "seed": seed, "support": support, "s": s})
+    (the G(r -> F s) automaton has two non-trap states, so every event does work).
+    Events [lo, hi) of the n-event trace; blocks of BLOCK events are drawn from their
+    own seeded stream, so any slice is generated alone."""
+    ids = _ids(np.random.default_rng(SEED_BASE + 3 + seed), support)
+    cdf = _zipf_cdf(support, s)
+    blen = n  # events of the last block may be fewer
+
+    def block(b, a0, z0):
+        rng = np.random.default_rng([SEED_BASE + 3, seed, b])
+        m = min(BLOCK, blen - b * BLOCK)
+        r = np.searchsorted(cdf, rng.random(m), side="right")
+        np.minimum(r, support - 1, out=r)
+        let = ((rng.random(m) < p_receive).astype(np.uint8)
+               | ((rng.random(m) < p_respond).astype(np.uint8) << 1))
+        return ids[r[a0:z0]], let[a0:z0]
+
+    parts = _blocks(n, lo, hi, block)
+    keys = np.concatenate([p[0] for p in parts]) if parts else np.zeros(0, np.uint32)
+    letters = np.concatenate([p[1] for p in parts]) if parts else np.zeros(0, np.uint8)
+    return Trace(formula, [keys], letters, {"config": "C3", "seed": seed, "support": support, "s": s,
+                                            "n": n, "lo": lo})
+
+
+def _unique_id(i: np.ndarray, mul: int) -> np.ndarray:
+    """bijection of [0, 2^32 - 1) onto u32 values != ABSENT: (i + 1) * mul - 1 mod 2^32"""
+    return (((i.astype(np.uint64) + np.uint64(1)) * np.uint64(mul) - np.uint64(1))
+            & np.uint64(0xFFFFFFFF)).astype(np.uint32)
 
 
 def proxy_trace(seed: int = 0, n: int = 1_000_000, videos: int = 1_000_000, s: float = 0.8,
                 p_cached: float = 0.6, p_ext: float = 0.5, p_ext_cached: float = 0.001,
-                max_req_events: int = 4) -> Trace:
+                max_req_events: int = 4, lo: int = 0, hi=None) -> Trace:
     """C4: YouTube proxy cache. bit0 = cached(v), bit1 = external(r).
-    Videos Zipf(s); requests unique with 1..max_req_events events each."""
-    rng = np.random.default_rng(SEED_BASE + 4 + seed)
-    per = rng.integers(1, max_req_events + 1, size=n // 2 + 1)
-    cs = np.cumsum(per)
-    nreq = int(np.searchsorted(cs, n) + 1)
-    req_of = np.repeat(np.arange(nreq), per[:nreq])[:n]
-    # requests interleave: each request's events are placed near its start
-    jitter = rng.random(n) * 64.0
-    order = np.argsort(req_of.astype(np.float64) * 2.5 + jitter, kind="stable")
-    req_of = req_of[order]
-    vrank = _zipf_ranks(rng, nreq, videos, s)
-    vids = _ids(rng, videos)[vrank]
-    rids = _ids(rng, nreq)
-    cached_req = rng.random(nreq) < p_cached
-    cached = cached_req[req_of]
-    ext = np.where(cached, rng.random(n) < p_ext_cached, rng.random(n) < p_ext)
-    letters = cached.astype(np.uint8) | (ext.astype(np.uint8) << 1)
-    return Trace(PROXY, [vids[req_of], rids[req_of]], letters,
-                 {"config": "C4", "seed": seed, "videos": videos})
+    Videos Zipf(s); requests unique with 1..max_req_events events each, each request's
+    events placed near each other.  Events [lo, hi) of the n-event trace: every block
+    of BLOCK events holds whole requests and is drawn from its own seeded stream (a
+    request's id is unique over the whole trace), so any slice is generated alone."""
+    grng = np.random.default_rng(SEED_BASE + 4 + seed)
+    vids = _ids(grng, videos)
+    rmul = int(grng.integers(1, 2**31)) * 2 + 1
+    cdf = _zipf_cdf(videos, s)
+
+    def block(b, a0, z0):
+        rng = np.random.default_rng([SEED_BASE + 4, seed, b])
+        m = min(BLOCK, n - b * BLOCK)
+        per = rng.integers(1, max_req_events + 1, size=m // 2 + 1)
+        cs = np.cumsum(per)
+        nreq = int(np.searchsorted(cs, m) + 1)
+        req_of = np.repeat(np.arange(nreq), per[:nreq])[:m]
+        jitter = rng.random(m) * 64.0
+        order = np.argsort(req_of.astype(np.float64) * 2.5 + jitter, kind="stable")
+        req_of = req_of[order]
+        vr = np.searchsorted(cdf, rng.random(nreq), side="right")
+        np.minimum(vr, videos - 1, out=vr)
+        rid = _unique_id(np.uint64(b) * np.uint64(BLOCK) + np.arange(nreq, dtype=np.uint64), rmul)
+        cached_req = rng.random(nreq) < p_cached
+        cached = cached_req[req_of]
+        ext = np.where(cached, rng.random(m) < p_ext_cached, rng.random(m) < p_ext)
+        let = cached.astype(np.uint8) | (ext.astype(np.uint8) << 1)
+        sl = slice(a0, z0)
+        return vids[vr[req_of[sl]]], rid[req_of[sl]], let[sl]
+
+    parts = _blocks(n, lo, hi, block)
+    cat = (lambda i, dt: np.concatenate([p[i] for p in parts]) if parts else np.zeros(0, dt))
+    return Trace(PROXY, [cat(0, np.uint32), cat(1, np.uint32)], cat(2, np.uint8),
+                 {"config": "C4", "seed": seed, "videos": videos, "n": n, "lo": lo})
 
 
 def worked_example() -> Trace:
