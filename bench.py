@@ -1,29 +1,35 @@
 #!/usr/bin/env python
 """Benchmark of the LTL4-C verification hot path (BASELINE.json metric:
-"trace events verified/sec ...; achieved HBM GB/s vs peak").
+"trace events verified/sec at 1/2/4/8 B200; achieved HBM GB/s vs peak").
 
-Default workload (N=1): BASELINE.json configs[1] = C2, the nested property
-  A x : user(x) => E_{<=3} r : rid(r) => (login && unauthorized)
-over a 10M-event synthetic web-server log with 100k users (tracegen.login_trace).
-A step = one ltl4c_verify of the whole 10M-event batch (all of SURVEY §8(a):
-epsilon + clustering, dedup, stepping, level reduction, root verdict, result
-copy).  Inputs are resident in HBM before the timed region; L2 (126 MB) is
-flushed between steps by writing a 256 MiB buffer (the input is 90 MB).
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C]
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+N = 1 (default): BASELINE.json configs[2] = C3, the largest single-GPU config:
+  A_{>=0.95} s : socket(s) => G (receive(s) -> F respond(s))
+over a 100M-event trace whose socket ids are Zipf(1.1)-skewed over 2^20 ids (a few
+huge clusters: the segmented transition-map scan).  The same line carries C2
+(configs[1], 10M events, nested login property) and C4 at 125M events per GPU as
+extra fields (`extra`).
+N > 1: BASELINE.json configs[3] = C4, ONE 1B-event proxy-cache trace
+  A v : vid(v) => E_{=0} r : req(r) => (cached(v) && external(r))
+sharded over the ranks (rank r holds the contiguous slice r of the trace and
+generates only that slice): ltl4c_verify routes every event to the owner of its
+video (hash of k0) with NCCL over NVLink, verifies the owned subtrees and
+all-reduces the per-level counts.  Strong scaling (total work
+fixed); time is the max over ranks.  Without torchrun, `--gpus N` re-launches
+itself under `python -m torch.distributed.run --nproc-per-node N`.
 
-N>1 runs under torch.distributed.run, one rank per GPU, on ONE global trace of
-N x 10M events (N x 100k users): rank r holds the contiguous slice r (weak
-scaling: 10M events per GPU); ltl4c_verify routes every event to the owner of
-its user (hash of k0) with an NCCL all-to-all over NVLink, verifies the owned
-subtrees and all-reduces the per-level counts.  Rank 0 prints
-one JSON line; time is the max over ranks.
+A step = one ltl4c_verify of the whole batch (all of SURVEY §8(a): epsilon +
+clustering, dedup, stepping, level reduction, root verdict, result copy).  Inputs
+are resident in HBM before the timed region; L2 (126 MB) is flushed between steps
+by writing a 256 MiB buffer outside the timed interval (C3's input is 500 MB).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -38,11 +44,34 @@ import tracegen  # noqa: E402
 
 METRIC = "trace events verified/sec"
 UNIT = "events/s"
-WORKLOAD = ("C2: A x:user(x) => E_{<=3} r:rid(r) => (login && unauthorized), "
-            "10M-event synthetic web-server log, 100k users (BASELINE.json configs[1])")
-ALG_BYTES_PER_EVENT = 9  # 2 x u32 keys + u8 letter read once
 RESULT_BYTES = 928       # sizeof(DevOut) copied device -> host per verify
 FLUSH_BYTES = 256 << 20
+
+# name -> (workload text, total events, generator(lo, hi), algorithmic bytes per event)
+CONFIGS = {
+    "C1": ("C1: A_{>=0.95} s:socket(s) => G(receive(s) -> F respond(s)), 10k events, 100 sockets "
+           "(BASELINE.json configs[0])", 10_000,
+           lambda lo, hi: _cut(tracegen.socket_trace(seed=0), lo, hi), 5),
+    "C2": ("C2: A x:user(x) => E_{<=3} r:rid(r) => (login && unauthorized), 10M-event synthetic "
+           "web-server log, 100k users (BASELINE.json configs[1])", 10_000_000,
+           lambda lo, hi: _cut(tracegen.login_trace(seed=0), lo, hi), 9),
+    "C3": ("C3: A_{>=0.95} s:socket(s) => G(receive(s) -> F respond(s)), 100M events, socket ids "
+           "Zipf(1.1) over 2^20 (BASELINE.json configs[2])", 100_000_000,
+           lambda lo, hi: tracegen.zipf_socket_trace(seed=0, lo=lo, hi=hi), 5),
+    "C4": ("C4 (one GPU's share): A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), "
+           "125M events, 10^6 videos Zipf(0.8), unique requests of 1-4 events", 125_000_000,
+           lambda lo, hi: tracegen.proxy_trace(seed=0, n=125_000_000, lo=lo, hi=hi), 9),
+    "C4B": ("C4: A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), 1B-event proxy-cache "
+            "trace, 10^6 videos Zipf(0.8), sharded by hash(video) over the GPUs (BASELINE.json configs[3])",
+            1_000_000_000,
+            lambda lo, hi: tracegen.proxy_trace(seed=0, n=1_000_000_000, lo=lo, hi=hi), 9),
+}
+
+
+def _cut(tr, lo, hi):
+    if lo == 0 and hi == tr.n:
+        return tr
+    return tracegen.Trace(tr.formula, [k[lo:hi].copy() for k in tr.keys], tr.letters[lo:hi].copy(), tr.meta)
 
 
 def _peaks():
@@ -52,6 +81,16 @@ def _peaks():
         return float(pk["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor() or "unknown"
 
 
 class Clocks:
@@ -99,39 +138,24 @@ class Clocks:
                 "samples": len(rows)}
 
 
-CONFIGS = {
-    "C1": ("C1: A_{>=0.95} s:socket(s) => G(receive(s) -> F respond(s)), 10k events, 100 sockets",
-           lambda r: tracegen.socket_trace(seed=r), 5),
-    "C2": (WORKLOAD, lambda r: tracegen.login_trace(seed=r), 9),
-    "C3": ("C3: socket formula, 100M events, keys Zipf(1.1) over 2^20 ids",
-           lambda r: tracegen.zipf_socket_trace(seed=r), 5),
-    "C4": ("C4 (single-GPU slice): A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), "
-           "125M events, 10^6 videos Zipf(0.8)",
-           lambda r: tracegen.proxy_trace(seed=r, n=125_000_000), 9),
-}
-CONFIG = "C2"
+def rank_slice(n: int, world: int, rank: int):
+    """rank r holds the contiguous events [r n / G, (r+1) n / G)."""
+    return n * rank // world, n * (rank + 1) // world
 
 
-def make_trace(rank: int):
-    return CONFIGS[CONFIG][1](rank)
-
-
-def run_ours(args, rank, world, local_rank):
+def run_config(name, args, rank, world, local_rank, with_e2e=True, profile=True):
+    """Time `args.steps` verifies of config `name` (this rank's slice) after
+    `args.warmup` untimed ones; returns the measurements (max over ranks)."""
     import torch
     import paper_1411_2239_b200 as ltl4c
 
+    text, n_total, gen, bpe = CONFIGS[name]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    if world > 1:
-        # one global trace, rank r holds slice r (same seed on every rank)
-        from paper_1411_2239_b200 import dist as ldist
-        full = tracegen.login_trace(seed=0, n=10_000_000 * world, users=100_000 * world) if CONFIG == "C2" \
-            else make_trace(0)
-        lo, hi = ldist.rank_slice(full.n, world, rank)
-        tr = tracegen.Trace(full.formula, [k[lo:hi].copy() for k in full.keys], full.letters[lo:hi].copy(), full.meta)
-        del full
-    else:
-        tr = make_trace(rank)
+    lo, hi = rank_slice(n_total, world, rank)
+    t0 = time.perf_counter()
+    tr = gen(lo, hi)
+    gen_s = time.perf_counter() - t0
     n = tr.n
     keys = [torch.from_numpy(k.view(np.int32)).to(dev) for k in tr.keys]
     letters = torch.from_numpy(tr.letters).to(dev)
@@ -139,8 +163,12 @@ def run_ours(args, rank, world, local_rank):
     prog = ltl4c.compile(tr.formula)
     st = prog.state(local_rank, capacity=n)
     if world > 1:
+        from paper_1411_2239_b200 import dist as ldist
         ldist.join(st)
     stream = torch.cuda.current_stream(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
 
     def step():
         return st.verify(keys, letters, stream=stream)[0]
@@ -148,9 +176,7 @@ def run_ours(args, rank, world, local_rank):
     for _ in range(args.warmup):
         flush.zero_()
         res = step()
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
+    if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
     st.stats_reset()
@@ -165,58 +191,130 @@ def run_ours(args, rank, world, local_rank):
     ms = [a.elapsed_time(b) for a, b in ev]
     total_ms = float(sum(ms))
     launches = st.stats()["launches"]
-    # kernel-level profile (CUDA events around every library kernel; this runs the
-    # launch sequence directly instead of the CUDA graph, so it is a separate pass)
-    st.stats_reset()
-    st.profile(True)
-    for i in range(args.steps):
-        flush.zero_()
-        step()
-    torch.cuda.synchronize(dev)
-    st.profile(False)
-    stats = st.stats()
-    stats["launches"] = launches
+    stats = None
+    if profile:
+        # kernel-level profile (CUDA events around every library kernel on the stream it
+        # is launched on; the launch sequence runs directly instead of the CUDA graph, so
+        # this is a separate pass)
+        st.stats_reset()
+        st.profile(True)
+        for i in range(args.steps):
+            flush.zero_()
+            step()
+        torch.cuda.synchronize(dev)
+        st.profile(False)
+        stats = st.stats()
     if dist is not None:
         t = torch.tensor([total_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
-    # e2e: the same call with HOST (pinned) buffers, H2D copies inside the timed region
-    hkeys = [torch.from_numpy(k.view(np.int32)).pin_memory() for k in tr.keys]
-    hlet = torch.from_numpy(tr.letters).pin_memory()
-    st_h = prog.state(local_rank, capacity=n)
-    if world > 1:
-        ldist.join(st_h)
-    for _ in range(max(1, args.warmup)):
-        st_h.verify_host(hkeys, hlet, stream=stream)
-    torch.cuda.synchronize(dev)
-    e2e_ms = []
-    for _ in range(args.steps):
-        flush.zero_()
+    out = {"n": n, "n_total": n_total, "total_ms": total_ms, "ms": ms, "stats": stats, "clocks": clk.summary(),
+           "verdict": res.verdict, "launches": launches, "gen_s": gen_s, "bpe": bpe, "text": text}
+    del keys, letters
+    if with_e2e:
+        # e2e: the same call with HOST (pinned) buffers, H2D copies inside the timed region
+        hkeys = [torch.from_numpy(k.view(np.int32)).pin_memory() for k in tr.keys]
+        hlet = torch.from_numpy(tr.letters).pin_memory()
+        st_h = prog.state(local_rank, capacity=n)
+        if world > 1:
+            ldist.join(st_h)
+        for _ in range(max(1, args.warmup)):
+            st_h.verify_host(hkeys, hlet, stream=stream)
         torch.cuda.synchronize(dev)
-        t0 = time.perf_counter()
-        r2 = st_h.verify_host(hkeys, hlet, stream=stream)[0]   # returns after the D2H result copy
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-    assert r2.verdict == res.verdict
-    e2e_total = float(sum(e2e_ms))
-    if dist is not None:
-        t = torch.tensor([e2e_total], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_total = float(t.item())
-    return {"n": n, "total_ms": total_ms, "ms": ms, "stats": stats, "clocks": clk.summary(),
-            "verdict": res.verdict, "e2e_total_ms": e2e_total, "tr": tr,
-            "h2d": int(sum(k.numel() * 4 for k in hkeys) + hlet.numel())}
+        e2e_ms = []
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize(dev)
+            if dist is not None:
+                dist.barrier()
+            t0 = time.perf_counter()
+            r2 = st_h.verify_host(hkeys, hlet, stream=stream)[0]   # returns after the D2H result copy
+            e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        assert r2.verdict == res.verdict
+        e2e_total = float(sum(e2e_ms))
+        if dist is not None:
+            t = torch.tensor([e2e_total], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_total = float(t.item())
+        out["e2e_total_ms"] = e2e_total
+        out["h2d"] = int(sum(k.numel() * 4 for k in hkeys) + hlet.numel())
+        del st_h, hkeys, hlet
+    out["tr"] = tr
+    del st
+    torch.cuda.empty_cache()
+    return out
 
 
-def cpu_baseline(tr, max_s=30.0):
-    """The oracle as it stands, single-threaded, on the bench trace (or a prefix)."""
+def roofline(r, steps, peak, peak_kind, config):
+    """Dominant kernel (largest share of the profiled step): algorithmic bytes per
+    launch (bytes/event x the events one launch processes) / its mean
+    CUDA-event launch time."""
+    ks = r["stats"]["kernels"]
+    tot = sum(v["ms"] for v in ks.values())
+    dom = max(ks, key=lambda k: ks[k]["ms"])
+    per_launch_ms = ks[dom]["ms"] / max(1, ks[dom]["launches"])
+    alg = r["bpe"] * r["n"]
+    achieved = alg / (per_launch_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            traffic = json.load(f).get(config, {}).get(dom)
+    except Exception:
+        traffic = None
+    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "peak_kind": peak_kind,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": alg,
+            "path_achieved": alg * steps / (r["total_ms"] / 1e3) / 1e9,
+            "path_frac": alg * steps / (r["total_ms"] / 1e3) / 1e9 / peak,
+            "kernel_share": {k: round(v["ms"] / max(1e-9, tot), 4) for k, v in ks.items() if v["launches"]},
+            "kernel_ms_per_step": tot / steps}
+
+
+def cpu_baseline(name, tr, max_events=10_000_000):
+    """The oracle as it stands on the host cores, on a bounded sample (a prefix) of the
+    bench trace: one thread, then every host thread (the oracle's timing mode: level-0
+    subtrees partitioned by a hash of k0; identical results)."""
     import oracle
-    n = tr.n
+    m = min(tr.n, max_events)
+    keys = [k[:m] for k in tr.keys]
+    let = tr.letters[:m]
+    nproc = os.cpu_count() or 1
     t0 = time.perf_counter()
-    oracle.run_offline(tr.formula, tr.keys, tr.letters)
-    dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"whole bench trace ({n} events, seed 0), one pass, {dt:.1f} s"}
+    r1 = oracle.run_offline(tr.formula, keys, let)
+    d1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    rn = oracle.run_offline(tr.formula, keys, let, threads=nproc)
+    dn = time.perf_counter() - t0
+    assert r1["verdict"] == rn["verdict"] and np.array_equal(r1["hist"], rn["hist"])
+    return {"value": m / dn, "unit": UNIT, "cores": nproc, "kind": "oracle",
+            "cpu": _cpu_model(), "nproc": nproc,
+            "single_thread": {"value": m / d1, "cores": 1, "seconds": round(d1, 2)},
+            "sample": f"first {m} events of the {name} bench trace (seed 0), one pass per thread count, "
+                      f"{dn:.1f} s on {nproc} threads"}
+
+
+def line_for(r, args, world, peak, peak_kind, name):
+    n_total = r["n_total"] if world > 1 else r["n"]
+    value = n_total * args.steps / (r["total_ms"] / 1e3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (tracegen, seeded)",
+        "config": {"workload": r["text"], "name": name, "events": n_total, "events_per_gpu": r["n"],
+                   "l2": "flushed between steps (256 MiB write, untimed)",
+                   "parallelism": (f"{world} GPUs, one global trace sharded by hash(k0): NCCL send/recv + "
+                                   "all-reduce" if world > 1 else "1 GPU"),
+                   "root_verdict": r["verdict"]},
+        "gpu_launches": int(r["launches"]),
+        "clocks": r["clocks"],
+    }
+    if r["stats"] is not None:
+        line["roofline"] = roofline(r, args.steps, peak, peak_kind, name)
+    if "e2e_total_ms" in r:
+        line["e2e"] = {"value": n_total * args.steps / (r["e2e_total_ms"] / 1e3), "unit": UNIT,
+                       "h2d_bytes_per_step": r["h2d"] * world, "d2h_bytes_per_step": RESULT_BYTES * world}
+    return line
 
 
 def main():
@@ -225,66 +323,53 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS) + ["C5"])
+    ap.add_argument("--config", default=None, choices=sorted(CONFIGS) + ["C5"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C2 / C4 extra fields")
     args = ap.parse_args()
-    global CONFIG, WORKLOAD, ALG_BYTES_PER_EVENT
-    if args.config == "C5":
-        return run_c5(args)
-    CONFIG = args.config
-    WORKLOAD = CONFIGS[CONFIG][0]
-    ALG_BYTES_PER_EVENT = CONFIGS[CONFIG][2]
     args.warmup = max(3, args.warmup)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # honour --gpus without torchrun: one rank per GPU on this node
+        import socket
+        with socket.socket() as s:
+            s.bind(("127.0.0.1", 0))
+            port = s.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"[bench] note: --gpus {args.gpus} but WORLD_SIZE={world}; measuring {world} GPUs", file=sys.stderr)
+    name = args.config or ("C3" if world == 1 else "C4B")
+    if name == "C5":
+        return run_c5(args)
     if args.impl == "reference":
-        return run_reference(args, rank, world)
+        return run_reference(args, rank, world, name)
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    r = run_ours(args, rank, world, local_rank)
+    peak, peak_kind = _peaks()
+    r = run_config(name, args, rank, world, local_rank)
+    line = line_for(r, args, world, peak, peak_kind, name) if rank == 0 else None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(name, r["tr"])
+    r = None
+    if world == 1 and not args.no_extra and name == "C3" and rank == 0:
+        # extra fields: C2 (configs[1]) and C4 at 125M events on this GPU
+        extra = {}
+        for x in ("C2", "C4"):
+            rx = run_config(x, args, 0, 1, local_rank, with_e2e=False)
+            lx = line_for(rx, args, 1, peak, peak_kind, x)
+            extra[x] = {k: lx[k] for k in ("value", "ms_per_step", "roofline", "gpu_launches")}
+            extra[x]["workload"] = rx["text"]
+            extra[x]["root_verdict"] = rx["verdict"]
+            rx = None
+        line["extra"] = extra
     if rank == 0:
-        peak, peak_kind = _peaks()
-        n_total = r["n"] * world
-        value = n_total * args.steps / (r["total_ms"] / 1e3)
-        ks = r["stats"]["kernels"]
-        dom = max(ks, key=lambda k: ks[k]["ms"])
-        per_launch_ms = ks[dom]["ms"] / max(1, ks[dom]["launches"])
-        kernel_ms_step = sum(v["ms"] for v in ks.values()) / args.steps
-        alg_bytes = ALG_BYTES_PER_EVENT * r["n"]
-        achieved = alg_bytes / (per_launch_ms / 1e3) / 1e9
-        traffic = None
-        try:
-            with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-                traffic = json.load(f).get(dom)
-        except Exception:
-            traffic = None
-        shares = {k: round(v["ms"] / max(1e-9, sum(x["ms"] for x in ks.values())), 4)
-                  for k, v in ks.items() if v["launches"]}
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": r["total_ms"] / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (tracegen, seeded)",
-            "config": {"workload": WORKLOAD, "events_per_gpu": r["n"], "name": CONFIG,
-                       "l2": "flushed between steps (256 MiB write, untimed)",
-                       "parallelism": (f"{world} GPUs, one global trace sharded by hash(k0), NCCL all-to-all + "
-                                       "all-reduce" if world > 1 else "1 GPU"),
-                       "root_verdict": r["verdict"]},
-            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
-                         "path_achieved": alg_bytes * args.steps / (r["total_ms"] / 1e3) / 1e9,
-                         "kernel_share": shares, "kernel_ms_per_step": kernel_ms_step},
-            "e2e": {"value": n_total * args.steps / (r["e2e_total_ms"] / 1e3), "unit": UNIT,
-                    "h2d_bytes_per_step": r["h2d"], "d2h_bytes_per_step": RESULT_BYTES},
-            "gpu_launches": int(r["stats"]["launches"]),
-            "clocks": r["clocks"],
-        }
-        if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(r["tr"])
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -344,30 +429,33 @@ def run_c5(args):
     print(json.dumps(line), flush=True)
 
 
-def run_reference(args, rank, world):
-    """Reference arm: the oracle (oracle/), as it stands, on the host cores; each
-    step verifies a bounded 1M-event sample (prefix) of the same C2 workload."""
+def run_reference(args, rank, world, name):
+    """Reference arm (tier framing: the oracle is the reference): the oracle, as it
+    stands, on the host cores -- every host thread (timing mode, level-0 hash
+    partition) -- each step verifying a bounded sample (the first 10M events) of the
+    same workload.  Under torchrun only rank 0 runs."""
     if rank != 0:
         return
     import oracle
-    tr = make_trace(0)
-    m = 1_000_000
-    keys = [k[:m] for k in tr.keys]
-    letters = tr.letters[:m]
+    text, n_total, gen, _ = CONFIGS[name]
+    m = min(n_total, 10_000_000)
+    tr = gen(0, m)
+    nproc = os.cpu_count() or 1
     for _ in range(args.warmup):
-        oracle.run_offline(tr.formula, keys, letters)
+        oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=nproc)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.run_offline(tr.formula, keys, letters)
+        oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=nproc)
     dt = time.perf_counter() - t0
     value = m * args.steps / dt
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic (tracegen, seeded)",
-            "config": {"workload": WORKLOAD, "events_per_gpu": tr.n, "users": 100_000},
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (tracegen, seeded)",
+            "config": {"workload": text, "name": name, "events": n_total, "sample_events": m},
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"first {m} events of the C2 trace per step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": nproc, "kind": "oracle", "cpu": _cpu_model(),
+                             "sample": f"first {m} events of the {name} trace per step, {nproc} host threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
