@@ -202,6 +202,39 @@ ltl4c_status ltl4c_state_profile(ltl4c_state *st, int enable);
 ltl4c_status ltl4c_state_stats(ltl4c_state *st, ltl4c_stats *out);
 ltl4c_status ltl4c_state_stats_reset(ltl4c_state *st);
 
+/* --- trace encoder (host) ------------------------------------------------- */
+
+/* Turns key -> value records into the encoded batch layout above: arXiv:1411.2239
+ * §4.1 "Valuation Extraction" ("the trace event is a key-value
+ * structure"; epsilon(u_i, K)), Def. 1/2.  Input: JSON lines, one
+ * object per line (UTF-8; blank lines skipped; other JSON values are E_SYNTAX).
+ *   keys[l][j]  = dense id of event j's value of guard key p_l (the key named by
+ *                 quantifier l), or LTL4C_ABSENT if the record maps p_l to no
+ *                 string/number.  Values are identified by their canonical string
+ *                 (strings as written; numbers as canonical decimals: 12, 12.0,
+ *                 1.2e1 and "12" are one value).  Ids are 0, 1, 2, ... per level in
+ *                 order of first appearance and persist for the encoder's life
+ *                 (the batches of an online stream share them).
+ *   letters[j]  bit a = atom a of the program holds: a 0-ary atom q holds iff the
+ *                 record maps q to true; a parametric atom q(x_i, ...) holds iff
+ *                 the record maps q to true or to the event's own value(s) of
+ *                 x_i, ... (a scalar for one argument, an array in argument order
+ *                 for several) -- reading A12.  Other keys are ignored.
+ * Reads whole lines from text[0 .. len) until `capacity` events are written;
+ * *consumed = bytes read (resume there), *n_events = events written.  Buffers are
+ * HOST memory owned by the caller (keys: n_levels arrays of `capacity` u32).
+ * Errors: E_INVALID (null argument), E_SYNTAX (malformed record; the message
+ * names the record number; nothing of that record is written), E_BUDGET (more
+ * than 2^32 - 1 distinct values of one key).  An encoder is single-threaded. */
+typedef struct ltl4c_encoder ltl4c_encoder;
+ltl4c_status ltl4c_encoder_create(const ltl4c_program *prog, ltl4c_encoder **out);
+ltl4c_status ltl4c_encode_jsonl(ltl4c_encoder *enc, const char *text, uint64_t len,
+                                uint32_t *const *keys, uint8_t *letters, uint64_t capacity,
+                                uint64_t *n_events, uint64_t *consumed);
+/* number of distinct values of guard key `level` seen so far */
+ltl4c_status ltl4c_encoder_values(const ltl4c_encoder *enc, uint32_t level, uint64_t *count);
+void ltl4c_encoder_free(ltl4c_encoder *enc);
+
 /* Thread-local message of the last non-OK status ("" if none). */
 const char *ltl4c_last_error(void);
 

@@ -76,6 +76,11 @@ def lib():
             L.orc_run_threads.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p),
                                           ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int), c_u64p,
                                           c_u64p, c_u64p]
+            L.orc_reader_new.argtypes = [ctypes.c_void_p]
+            L.orc_reader_new.restype = ctypes.c_void_p
+            L.orc_reader_free.argtypes = [ctypes.c_void_p]
+            L.orc_feed_jsonl.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_char_p, ctypes.c_uint64]
+            L.orc_feed_jsonl.restype = ctypes.c_int64
             _lib = L
     return _lib
 
@@ -177,6 +182,34 @@ class Monitor:
     def node_verdict(self, prefix) -> int:
         arr = np.ascontiguousarray(prefix, dtype=np.uint32)
         return lib().orc_node_verdict(self._h, len(arr), arr.ctypes.data if len(arr) else None)
+
+
+class RecordMonitor(Monitor):
+    """A Monitor fed from JSON-lines records by the oracle's own reader."""
+
+    def __init__(self, prop: Property):
+        super().__init__(prop)
+        self._r = lib().orc_reader_new(prop._h)
+
+    def __del__(self):
+        if getattr(self, "_r", None) and _lib is not None:
+            _lib.orc_reader_free(self._r)
+            self._r = None
+        super().__del__()
+
+    def feed_records(self, text) -> int:
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        n = lib().orc_feed_jsonl(self._r, self._h, data, len(data))
+        if n < 0:
+            raise ValueError(f"malformed record on line {-n}")
+        return n
+
+
+def run_records(text: str, records) -> dict:
+    """Algorithm 1 offline over JSON-lines records (the oracle's own reader)."""
+    m = RecordMonitor(Property(text))
+    m.feed_records(records)
+    return m.evaluate()
 
 
 def run_offline(text: str, keys, letters, threads: int = 1) -> dict:

@@ -1125,3 +1125,340 @@ int orc_run_threads(const orc_prop *p, uint64_t n, const uint32_t *const *keys, 
   free(jobs); free(th);
   return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Records: the oracle's own reader of key -> value events (P:922-935,       */
+/* "the trace event is a key-value structure"), one JSON object per line.    */
+/* Written independently of the product's encoder; readings (A12,  */
+/* A25-A27): a guard key's value is a JSON string or number, identified by   */
+/* its canonical text (numbers as canonical decimals); a 0-ary atom q holds  */
+/* iff q maps to true; q(x_i, ...) holds iff q maps to true or to the       */
+/* event's own value(s) of x_i, ... (array in argument order for several).  */
+/* Value ids are the oracle's own (first-appearance order per level); the    */
+/* verdicts and counts do not depend on the labelling.                       */
+/* ------------------------------------------------------------------------ */
+typedef struct { char *s; uint32_t id; } ostr_t;
+typedef struct { ostr_t *slot; uint64_t cap, n; } odict_t;
+
+static uint64_t str_hash(const char *s) {
+  uint64_t h = 0xcbf29ce484222325ull;
+  for (; *s; s++) { h ^= (unsigned char)*s; h *= 0x100000001b3ull; }
+  return h;
+}
+static uint32_t odict_id(odict_t *d, const char *s) {
+  if ((d->n + 1) * 2 > d->cap) {
+    uint64_t nc = d->cap ? d->cap * 2 : 1024;
+    ostr_t *ns = (ostr_t *)calloc(nc, sizeof(ostr_t));
+    for (uint64_t i = 0; i < d->cap; i++) {
+      if (!d->slot[i].s) continue;
+      uint64_t j = str_hash(d->slot[i].s) & (nc - 1);
+      while (ns[j].s) j = (j + 1) & (nc - 1);
+      ns[j] = d->slot[i];
+    }
+    free(d->slot); d->slot = ns; d->cap = nc;
+  }
+  uint64_t j = str_hash(s) & (d->cap - 1);
+  while (d->slot[j].s) {
+    if (strcmp(d->slot[j].s, s) == 0) return d->slot[j].id;
+    j = (j + 1) & (d->cap - 1);
+  }
+  size_t sl = strlen(s) + 1;
+  d->slot[j].s = (char *)malloc(sl);
+  memcpy(d->slot[j].s, s, sl);
+  d->slot[j].id = (uint32_t)d->n++;
+  return d->slot[j].id;
+}
+
+/* a JSON value as the reader keeps it */
+enum { JV_OTHER = 0, JV_TRUE, JV_SCALAR, JV_ARRAY };
+#define JV_MAXITEMS 8
+typedef struct {
+  int kind;
+  char text[256];                 /* JV_SCALAR: canonical text */
+  int nitems;
+  char items[JV_MAXITEMS][256];   /* JV_ARRAY: canonical text of scalar items ("" if not scalar) */
+} jval_t;
+
+typedef struct { const char *p, *e; int bad; } jrd_t;
+
+static void jws(jrd_t *r) { while (r->p < r->e && (*r->p == ' ' || *r->p == '\t' || *r->p == '\r')) r->p++; }
+
+/* string at '"' into out (UTF-8, escapes decoded; truncated to outlen - 1) */
+static void jstring(jrd_t *r, char *out, int outlen) {
+  int n = 0;
+  r->p++;
+  while (r->p < r->e && *r->p != '"') {
+    unsigned int c = (unsigned char)*r->p++;
+    if (c == '\\') {
+      if (r->p >= r->e) { r->bad = 1; return; }
+      char e = *r->p++;
+      if (e == 'u') {
+        unsigned int u = 0;
+        for (int i = 0; i < 4; i++) {
+          if (r->p >= r->e || !isxdigit((unsigned char)*r->p)) { r->bad = 1; return; }
+          char h = *r->p++;
+          u = u * 16 + (unsigned)(isdigit((unsigned char)h) ? h - '0' : (tolower((unsigned char)h) - 'a' + 10));
+        }
+        if (u >= 0xD800 && u < 0xDC00 && r->e - r->p >= 6 && r->p[0] == '\\' && r->p[1] == 'u') {
+          unsigned int lo = 0;
+          const char *save = r->p;
+          r->p += 2;
+          for (int i = 0; i < 4; i++) {
+            char h = *r->p++;
+            if (!isxdigit((unsigned char)h)) { r->bad = 1; return; }
+            lo = lo * 16 + (unsigned)(isdigit((unsigned char)h) ? h - '0' : (tolower((unsigned char)h) - 'a' + 10));
+          }
+          if (lo >= 0xDC00 && lo < 0xE000) u = 0x10000 + ((u - 0xD800) << 10) + (lo - 0xDC00);
+          else r->p = save;
+        }
+        /* UTF-8 encode */
+        unsigned char b[4]; int nb;
+        if (u < 0x80) { b[0] = (unsigned char)u; nb = 1; }
+        else if (u < 0x800) { b[0] = (unsigned char)(0xC0 | (u >> 6)); b[1] = (unsigned char)(0x80 | (u & 63)); nb = 2; }
+        else if (u < 0x10000) { b[0] = (unsigned char)(0xE0 | (u >> 12)); b[1] = (unsigned char)(0x80 | ((u >> 6) & 63)); b[2] = (unsigned char)(0x80 | (u & 63)); nb = 3; }
+        else { b[0] = (unsigned char)(0xF0 | (u >> 18)); b[1] = (unsigned char)(0x80 | ((u >> 12) & 63)); b[2] = (unsigned char)(0x80 | ((u >> 6) & 63)); b[3] = (unsigned char)(0x80 | (u & 63)); nb = 4; }
+        for (int i = 0; i < nb; i++) if (n < outlen - 1) out[n++] = (char)b[i];
+        continue;
+      }
+      switch (e) {
+        case 'n': c = '\n'; break; case 't': c = '\t'; break; case 'r': c = '\r'; break;
+        case 'b': c = '\b'; break; case 'f': c = '\f'; break;
+        case '"': case '\\': case '/': c = (unsigned char)e; break;
+        default: r->bad = 1; return;
+      }
+    }
+    if (n < outlen - 1) out[n++] = (char)c;
+  }
+  if (r->p >= r->e) { r->bad = 1; return; }
+  r->p++;
+  out[n] = 0;
+}
+
+/* number -> canonical decimal text: the value m x 10^(x) with m an integer whose
+ * digits have no leading or trailing zeros, written positionally */
+static void jnumber(jrd_t *r, char *out, int outlen) {
+  int neg = 0;
+  char dig[512]; int nd = 0;
+  long exp10 = 0;
+  if (*r->p == '-') { neg = 1; r->p++; }
+  if (r->p >= r->e || !isdigit((unsigned char)*r->p)) { r->bad = 1; return; }
+  while (r->p < r->e && isdigit((unsigned char)*r->p)) { if (nd < 500) dig[nd++] = *r->p; else exp10++; r->p++; }
+  if (r->p < r->e && *r->p == '.') {
+    r->p++;
+    if (r->p >= r->e || !isdigit((unsigned char)*r->p)) { r->bad = 1; return; }
+    while (r->p < r->e && isdigit((unsigned char)*r->p)) { if (nd < 500) { dig[nd++] = *r->p; exp10--; } r->p++; }
+  }
+  if (r->p < r->e && (*r->p == 'e' || *r->p == 'E')) {
+    r->p++;
+    int es = 1; long ev = 0;
+    if (r->p < r->e && (*r->p == '+' || *r->p == '-')) { if (*r->p == '-') es = -1; r->p++; }
+    if (r->p >= r->e || !isdigit((unsigned char)*r->p)) { r->bad = 1; return; }
+    while (r->p < r->e && isdigit((unsigned char)*r->p)) { ev = ev * 10 + (*r->p++ - '0'); if (ev > 4096) { r->bad = 1; return; } }
+    exp10 += es * ev;
+  }
+  /* value = digits x 10^exp10; drop leading zeros, fold trailing zeros into exp10 */
+  int a = 0;
+  while (a < nd && dig[a] == '0') a++;
+  while (nd > a && dig[nd - 1] == '0') { nd--; exp10++; }
+  if (a == nd) { snprintf(out, (size_t)outlen, "0"); return; }
+  int m = nd - a;            /* significant digits */
+  long ip = m + exp10;       /* digits before the decimal point */
+  char buf[12000]; int k = 0;
+  if (neg) buf[k++] = '-';
+  if (ip <= 0) {
+    buf[k++] = '0'; buf[k++] = '.';
+    for (long i = 0; i < -ip && k < 11000; i++) buf[k++] = '0';
+    for (int i = a; i < nd && k < 11990; i++) buf[k++] = dig[i];
+  } else {
+    for (long i = 0; i < ip && k < 11990; i++) buf[k++] = i < m ? dig[a + i] : '0';
+    if (ip < m) { buf[k++] = '.'; for (int i = a + (int)ip; i < nd && k < 11990; i++) buf[k++] = dig[i]; }
+  }
+  buf[k] = 0;
+  snprintf(out, (size_t)outlen, "%s", buf);
+}
+
+static void jvalue(jrd_t *r, jval_t *v, int depth);
+
+static void jskip_container(jrd_t *r, char open, int depth) {
+  (void)open;
+  jval_t tmp;
+  if (*r->p == '[') {
+    r->p++; jws(r);
+    if (r->p < r->e && *r->p == ']') { r->p++; return; }
+    for (;;) {
+      jvalue(r, &tmp, depth + 1); if (r->bad) return;
+      jws(r);
+      if (r->p < r->e && *r->p == ',') { r->p++; continue; }
+      if (r->p < r->e && *r->p == ']') { r->p++; return; }
+      r->bad = 1; return;
+    }
+  }
+  r->p++; jws(r);
+  if (r->p < r->e && *r->p == '}') { r->p++; return; }
+  for (;;) {
+    char key[256];
+    jws(r);
+    if (r->p >= r->e || *r->p != '"') { r->bad = 1; return; }
+    jstring(r, key, sizeof key); if (r->bad) return;
+    jws(r);
+    if (r->p >= r->e || *r->p != ':') { r->bad = 1; return; }
+    r->p++;
+    jvalue(r, &tmp, depth + 1); if (r->bad) return;
+    jws(r);
+    if (r->p < r->e && *r->p == ',') { r->p++; continue; }
+    if (r->p < r->e && *r->p == '}') { r->p++; return; }
+    r->bad = 1; return;
+  }
+}
+
+static void jvalue(jrd_t *r, jval_t *v, int depth) {
+  jws(r);
+  v->kind = JV_OTHER;
+  v->nitems = 0;
+  if (r->p >= r->e || depth > 64) { r->bad = 1; return; }
+  char c = *r->p;
+  if (c == '"') { v->kind = JV_SCALAR; jstring(r, v->text, sizeof v->text); return; }
+  if (c == '-' || isdigit((unsigned char)c)) { v->kind = JV_SCALAR; jnumber(r, v->text, sizeof v->text); return; }
+  if (c == 't' && r->e - r->p >= 4 && strncmp(r->p, "true", 4) == 0) { r->p += 4; v->kind = JV_TRUE; return; }
+  if (c == 'f' && r->e - r->p >= 5 && strncmp(r->p, "false", 5) == 0) { r->p += 5; return; }
+  if (c == 'n' && r->e - r->p >= 4 && strncmp(r->p, "null", 4) == 0) { r->p += 4; return; }
+  if (c == '[') {
+    /* keep the scalar items (for parametric atoms with several arguments) */
+    v->kind = JV_ARRAY;
+    r->p++; jws(r);
+    if (r->p < r->e && *r->p == ']') { r->p++; return; }
+    for (;;) {
+      jval_t it;
+      jvalue(r, &it, depth + 1); if (r->bad) return;
+      if (v->nitems < JV_MAXITEMS) snprintf(v->items[v->nitems], 256, "%s", it.kind == JV_SCALAR ? it.text : "\x01");
+      v->nitems++;
+      jws(r);
+      if (r->p < r->e && *r->p == ',') { r->p++; continue; }
+      if (r->p < r->e && *r->p == ']') { r->p++; return; }
+      r->bad = 1; return;
+    }
+  }
+  if (c == '{') { jskip_container(r, '{', depth); return; }
+  r->bad = 1;
+}
+
+struct orc_reader {
+  const orc_prop *p;
+  odict_t dict[ORC_MAX_LEVELS];
+  /* per atom: predicate name and the level of each argument */
+  char pred[MAXATOMS][128];
+  int nargs[MAXATOMS];
+  int argl[MAXATOMS][ORC_MAX_LEVELS];
+};
+
+orc_reader *orc_reader_new(const orc_prop *p) {
+  orc_reader *r = (orc_reader *)calloc(1, sizeof(orc_reader));
+  r->p = p;
+  for (int j = 0; j < p->natoms; j++) {
+    const char *nm = p->atoms[j];
+    const char *lp = strchr(nm, '(');
+    int len = lp ? (int)(lp - nm) : (int)strlen(nm);
+    snprintf(r->pred[j], sizeof r->pred[j], "%.*s", len, nm);
+    r->nargs[j] = 0;
+    if (lp) {
+      const char *a = lp + 1;
+      while (*a && *a != ')') {
+        char var[64]; int k = 0;
+        while (*a && *a != ',' && *a != ')' && k < 63) var[k++] = *a++;
+        var[k] = 0;
+        for (int i = 0; i < p->nq; i++)
+          if (strcmp(p->q[i].var, var) == 0 && r->nargs[j] < ORC_MAX_LEVELS) r->argl[j][r->nargs[j]++] = i;
+        if (*a == ',') a++;
+      }
+    }
+  }
+  return r;
+}
+
+void orc_reader_free(orc_reader *r) {
+  if (!r) return;
+  for (int l = 0; l < ORC_MAX_LEVELS; l++) {
+    for (uint64_t i = 0; i < r->dict[l].cap; i++) free(r->dict[l].slot[i].s);
+    free(r->dict[l].slot);
+  }
+  free(r);
+}
+
+/* Read every record of text[0, len) and feed the monitor one event per record.
+ * Returns the number of records, or -(line number) of the first malformed one. */
+int64_t orc_feed_jsonl(orc_reader *rd, orc_monitor *m, const char *text, uint64_t len) {
+  const orc_prop *p = rd->p;
+  const char *s = text, *end = text + len;
+  int64_t nrec = 0, line = 0;
+  enum { MAXKV = 64 };
+  static __thread char keys[MAXKV][128];
+  static __thread jval_t vals[MAXKV];
+  while (s < end) {
+    const char *nl = memchr(s, '\n', (size_t)(end - s));
+    const char *le = nl ? nl : end;
+    line++;
+    jrd_t r = {s, le, 0};
+    jws(&r);
+    if (r.p == le) { s = nl ? nl + 1 : end; continue; }
+    int nkv = 0;
+    if (*r.p != '{') return -line;
+    r.p++; jws(&r);
+    if (r.p < le && *r.p == '}') r.p++;
+    else {
+      for (;;) {
+        char key[128]; jval_t v;
+        jws(&r);
+        if (r.p >= le || *r.p != '"') return -line;
+        jstring(&r, key, sizeof key); if (r.bad) return -line;
+        jws(&r);
+        if (r.p >= le || *r.p != ':') return -line;
+        r.p++;
+        jvalue(&r, &v, 0); if (r.bad) return -line;
+        /* one value per key (reading A11): a repeated key keeps its last value */
+        int at = -1;
+        for (int i = 0; i < nkv; i++) if (strcmp(keys[i], key) == 0) at = i;
+        if (at < 0 && nkv < MAXKV) at = nkv++;
+        if (at >= 0) { snprintf(keys[at], 128, "%s", key); vals[at] = v; }
+        jws(&r);
+        if (r.p < le && *r.p == ',') { r.p++; continue; }
+        if (r.p < le && *r.p == '}') { r.p++; break; }
+        return -line;
+      }
+    }
+    jws(&r);
+    if (r.p != le) return -line;
+    /* epsilon(u_j, K): the value of each guard key p_i */
+    uint32_t D[ORC_MAX_LEVELS];
+    const char *gv[ORC_MAX_LEVELS];
+    for (int i = 0; i < p->nq; i++) {
+      gv[i] = NULL;
+      for (int k = 0; k < nkv; k++)
+        if (strcmp(keys[k], p->q[i].key) == 0 && vals[k].kind == JV_SCALAR) gv[i] = vals[k].text;
+      D[i] = gv[i] ? odict_id(&rd->dict[i], gv[i]) : ORC_ABSENT;
+    }
+    uint8_t a = 0;
+    for (int j = 0; j < p->natoms; j++) {
+      const jval_t *v = NULL;
+      for (int k = 0; k < nkv; k++) if (strcmp(keys[k], rd->pred[j]) == 0) v = &vals[k];
+      if (!v) continue;
+      int holds = v->kind == JV_TRUE;
+      if (!holds && rd->nargs[j] == 1 && v->kind == JV_SCALAR)
+        holds = gv[rd->argl[j][0]] && strcmp(gv[rd->argl[j][0]], v->text) == 0;
+      if (!holds && rd->nargs[j] >= 1 && v->kind == JV_ARRAY && v->nitems == rd->nargs[j]) {
+        holds = 1;
+        for (int i = 0; i < rd->nargs[j]; i++) {
+          const char *g = gv[rd->argl[j][i]];
+          if (!g || strcmp(g, v->items[i]) != 0) holds = 0;
+        }
+      }
+      if (holds) a |= (uint8_t)(1u << j);
+    }
+    const uint32_t *kp[ORC_MAX_LEVELS];
+    uint32_t col[ORC_MAX_LEVELS][1];
+    for (int i = 0; i < p->nq; i++) { col[i][0] = D[i]; kp[i] = col[i]; }
+    orc_feed(m, 1, kp, &a);
+    nrec++;
+    s = nl ? nl + 1 : end;
+  }
+  return nrec;
+}

@@ -76,6 +76,14 @@ int  orc_run_threads(const orc_prop *p, uint64_t n, const uint32_t *const *keys,
                      uint64_t hist[ORC_MAX_LEVELS + 1][6], uint64_t *events_seen,
                      uint64_t *events_bound);
 
+/* Records (JSON lines, one key -> value object per line) read by the oracle's
+ * own reader and fed to a monitor one event per record; returns the number of
+ * records, or -(line) of the first malformed record. */
+typedef struct orc_reader orc_reader;
+orc_reader *orc_reader_new(const orc_prop *p);
+void orc_reader_free(orc_reader *r);
+int64_t orc_feed_jsonl(orc_reader *r, orc_monitor *m, const char *text, uint64_t len);
+
 #ifdef __cplusplus
 }
 #endif

@@ -100,12 +100,19 @@ _lib.ltl4c_state_free.restype = None
 _lib.ltl4c_state_profile.argtypes = [_P, ctypes.c_int]
 _lib.ltl4c_state_stats.argtypes = [_P, ctypes.POINTER(_Stats)]
 _lib.ltl4c_state_stats_reset.argtypes = [_P]
+_lib.ltl4c_encoder_create.argtypes = [_P, ctypes.POINTER(_P)]
+_lib.ltl4c_encode_jsonl.argtypes = [_P, ctypes.c_char_p, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_encoder_values.argtypes = [_P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_encoder_free.argtypes = [_P]
+_lib.ltl4c_encoder_free.restype = None
 _lib.ltl4c_last_error.restype = ctypes.c_char_p
 _lib.ltl4c_version.restype = ctypes.c_char_p
 for _fn in ("ltl4c_compile", "ltl4c_compile_batch", "ltl4c_program_tables", "ltl4c_state_create",
             "ltl4c_state_comm", "ltl4c_verify", "ltl4c_verify_host", "ltl4c_verify_async", "ltl4c_result_get",
             "ltl4c_state_reset",
-            "ltl4c_state_profile", "ltl4c_state_stats", "ltl4c_state_stats_reset"):
+            "ltl4c_state_profile", "ltl4c_state_stats", "ltl4c_state_stats_reset",
+            "ltl4c_encoder_create", "ltl4c_encode_jsonl", "ltl4c_encoder_values"):
     getattr(_lib, _fn).restype = ctypes.c_int
 
 
@@ -174,6 +181,46 @@ class Program:
 
     def state(self, device: int = 0, online: bool = False, capacity: int = 0) -> "State":
         return State(self, device, online, capacity)
+
+    def encoder(self) -> "Encoder":
+        """Host trace encoder for this program's guard keys and atoms (ltl4c_encode_jsonl)."""
+        return Encoder(self)
+
+
+class Encoder:
+    """JSON-lines records -> (keys, letters) host arrays in the layout verify() takes
+    (ltl4c_encode_jsonl: per-key dictionaries persist across calls)."""
+
+    def __init__(self, prog: Program):
+        self.prog = prog
+        self._h = ctypes.c_void_p()
+        _check(_lib.ltl4c_encoder_create(prog._h, ctypes.byref(self._h)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.ltl4c_encoder_free(self._h)
+        except Exception:
+            pass
+        self._h = None
+
+    def encode(self, text) -> tuple[list[np.ndarray], np.ndarray]:
+        """Encode every record of `text` (str or bytes, one JSON object per line)."""
+        data = text.encode() if isinstance(text, str) else bytes(text)
+        cap = data.count(b"\n") + 1
+        keys = [np.empty(cap, np.uint32) for _ in range(self.prog.n_levels)]
+        letters = np.empty(cap, np.uint8)
+        kp = (ctypes.c_void_p * MAX_LEVELS)(*[k.ctypes.data for k in keys])
+        n, used = ctypes.c_uint64(), ctypes.c_uint64()
+        _check(_lib.ltl4c_encode_jsonl(self._h, data, len(data), kp, letters.ctypes.data, cap,
+                                       ctypes.byref(n), ctypes.byref(used)))
+        m = int(n.value)
+        return [k[:m].copy() for k in keys], letters[:m].copy()
+
+    def values(self, level: int) -> int:
+        c = ctypes.c_uint64()
+        _check(_lib.ltl4c_encoder_values(self._h, level, ctypes.byref(c)))
+        return int(c.value)
 
 
 def compile(text: str) -> Program:  # noqa: A001 (mirrors ltl4c_compile)

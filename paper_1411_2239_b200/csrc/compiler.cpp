@@ -125,6 +125,7 @@ struct Formula {
   std::vector<Node> nodes;
   std::map<std::tuple<int, int, int, int>, int> intern;
   std::vector<std::string> atoms;
+  std::vector<std::vector<int>> atom_levels;  // per atom: quantifier level of each argument
   int root = -1;
 
   int make(Op op, int a = -1, int b = -1, int atom = -1) {
@@ -308,6 +309,7 @@ class Parser {
     if (is_word(cur(), "false")) { ++pos_; return mk_not(f_.make(kTrue)); }
     if (is_word(cur(), "U")) err(LTL4C_E_SYNTAX, "unexpected U");
     std::string name = toks_[pos_++].s;
+    std::vector<int> levels;
     if (cur().k == Tk::LParen) {
       ++pos_;
       name += "(";
@@ -315,7 +317,8 @@ class Parser {
       while (true) {
         if (cur().k != Tk::Ident) err(LTL4C_E_SYNTAX, "expected a variable");
         bool bound = false;
-        for (auto &q : f_.q) bound |= q.var == cur().s;
+        for (size_t l = 0; l < f_.q.size(); ++l)
+          if (f_.q[l].var == cur().s) { bound = true; levels.push_back((int)l); }
         if (!bound) err(LTL4C_E_UNBOUND, "unbound variable '" + cur().s + "'");
         name += (first ? "" : ",") + cur().s;
         first = false;
@@ -331,6 +334,7 @@ class Parser {
     if (it == f_.atoms.end()) {
       if (f_.atoms.size() >= LTL4C_MAX_ATOMS) err(LTL4C_E_BUDGET, "more than 8 atoms");
       f_.atoms.push_back(name);
+      f_.atom_levels.push_back(levels);
     }
     return f_.make(kAtom, -1, -1, j);
   }
@@ -665,13 +669,20 @@ ltl4c_status compile_many(const char *const *texts, int nf, ltl4c_program **out)
     // atom union in order of first occurrence
     std::vector<std::vector<int>> gbit(nf);
     for (int i = 0; i < nf; ++i)
-      for (auto &a : fs[i].atoms) {
+      for (size_t j = 0; j < fs[i].atoms.size(); ++j) {
+        const std::string &a = fs[i].atoms[j];
         auto it = std::find(prog->atom_names.begin(), prog->atom_names.end(), a);
         if (it == prog->atom_names.end()) {
           prog->atom_names.push_back(a);
+          prog->atom_levels.push_back(fs[i].atom_levels[j]);
           gbit[i].push_back((int)prog->atom_names.size() - 1);
         } else {
-          gbit[i].push_back((int)(it - prog->atom_names.begin()));
+          const int g = (int)(it - prog->atom_names.begin());
+          if (prog->atom_levels[g] != fs[i].atom_levels[j]) {
+            delete prog;
+            return fail(LTL4C_E_INVALID, "atom " + a + " binds different quantifier levels in the batch");
+          }
+          gbit[i].push_back(g);
         }
       }
     if (prog->atom_names.size() > LTL4C_MAX_ATOMS) {

@@ -12,6 +12,7 @@ struct ltl4c_program {
   std::vector<uint8_t> label;             // [n_formulas][n_states], B6 codes {0,2,3,5}
   std::vector<ltl4c_quantifier> quant;    // [n_formulas][n_levels]
   std::vector<std::string> atom_names;    // [n_atoms]
+  std::vector<std::vector<int>> atom_levels;  // [n_atoms]: quantifier level of each argument
   std::vector<const char *> atom_ptrs;    // views into atom_names
   std::vector<std::string> key_names;     // [n_levels]
   std::vector<std::string> texts;         // source formulas
