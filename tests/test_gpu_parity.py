@@ -435,3 +435,36 @@ def test_online_async_pipeline(env):
         st.verify_async([x[80:90] for x in k], l[80:90], first_index=80)   # 9th outstanding
     for t in ts:
         st.result(t)
+
+
+def test_records_through_encoder_and_gpu(env):
+    """JSON-lines records -> host encoder (ltl4c_encode_jsonl) -> sm_100a path, against
+    the oracle reading the SAME records with its own reader: the worked example
+    (tests/golden/login_example.jsonl) and a C2-shaped file."""
+    import os
+    ltl4c, torch, dev = env
+    golden = open(os.path.join(os.path.dirname(__file__), "golden", "login_example.jsonl")).read()
+    tr = tracegen.login_trace(seed=17, n=300_000, users=3000, rid_events=2, p_unauth=0.05)
+    big = tracegen.to_jsonl(tr, ["user", "rid"], ["login", "unauthorized"], [[], []], seed=2, style="mixed")
+    sock = tracegen.zipf_socket_trace(seed=18, n=200_000, support=1 << 12)
+    sock_txt = tracegen.to_jsonl(sock, ["socket"], ["receive", "respond"], [[0], [0]], seed=3, style="mixed")
+    for formula, text in ((tracegen.LOGIN, golden), (tracegen.LOGIN, big), (tracegen.SOCKET, sock_txt)):
+        prog = ltl4c.compile(formula)
+        keys, letters = prog.encoder().encode(text)
+        k, l = _dev(torch, dev, keys, letters)
+        got = prog.state(0).verify(k, l)[0]
+        want = oracle.run_records(formula, text)
+        _assert_same(got, want, (formula, len(text)))
+    # online: records streamed in chunks through one encoder (dictionaries persist)
+    prog = ltl4c.compile(tracegen.LOGIN)
+    enc = prog.encoder()
+    st = prog.state(0, online=True)
+    lines = big.splitlines(keepends=True)
+    mon = oracle.RecordMonitor(oracle.Property(tracegen.LOGIN))
+    for lo in range(0, len(lines), 70_000):
+        chunk = "".join(lines[lo:lo + 70_000])
+        keys, letters = enc.encode(chunk)
+        k, l = _dev(torch, dev, keys, letters)
+        got = st.verify(k, l)[0]
+        mon.feed_records(chunk)
+        _assert_same(got, mon.evaluate(), ("online records", lo))

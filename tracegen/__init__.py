@@ -290,3 +290,55 @@ def c5_trace(seed: int = 0, n: int = 2_000_000, hosts: int = 256, users: int = 1
         letters |= (rng.random(ev_sess.shape[0]) < pj).astype(np.uint8) << j
     keys = [hid[host_of[ev_sess]], uid[user_of[ev_sess]], sid[ev_sess]]
     return Trace("\n".join(C5_FORMULAS), keys, letters, {"config": "C5", "seed": seed})
+
+
+def to_jsonl(tr: Trace, key_names, atom_preds, atom_args, seed: int = 0, style: str = "mixed") -> str:
+    """Write a trace as JSON-lines key -> value records (the paper's key-value events,
+    P:922-925): guard key i -> the event's value (absent keys omitted), 0-ary atom ->
+    `true` when it holds, parametric atom q(x_i) -> the event's own value of x_i (or
+    `true`).  No method arithmetic: values are formatted, never interpreted.
+
+    style "mixed" writes each value in one of several spellings that denote the same
+    value (integer, string, decimal with trailing zeros, exponent) plus noise keys, so
+    readers must canonicalise; "plain" writes integers only."""
+    import json as _json
+    rng = np.random.default_rng(SEED_BASE + 900 + seed)
+    n = tr.n
+    pick = rng.integers(0, 4, size=(len(key_names), n)) if style == "mixed" else np.zeros((len(key_names), n), int)
+    atom_true = rng.random(n) < 0.5
+    noise = rng.random(n) < 0.1
+    lines = []
+
+    def spell(v: int, how: int):
+        if how == 0:
+            return str(v)
+        if how == 1:
+            return _json.dumps(str(v))
+        if how == 2:
+            return f"{v}.000"
+        return f"{v / 10:.1f}e1" if v % 10 == 0 and v else str(v) if v < 10 else f"{v // 10}.{v % 10}e1"
+
+    for j in range(n):
+        parts = []
+        vals = []
+        for i, k in enumerate(key_names):
+            v = int(tr.keys[i][j])
+            vals.append(None if v == 0xFFFFFFFF else v)
+            if v != 0xFFFFFFFF:
+                parts.append(f'{_json.dumps(k)}: {spell(v, int(pick[i, j]))}')
+        a = int(tr.letters[j])
+        for b, (q, args) in enumerate(zip(atom_preds, atom_args)):
+            if not (a >> b) & 1:
+                continue
+            if not args or atom_true[j] or any(vals[x] is None for x in args):
+                if args and any(vals[x] is None for x in args):
+                    continue  # the atom cannot hold without its argument's value (A12)
+                parts.append(f'{_json.dumps(q)}: true')
+            elif len(args) == 1:
+                parts.append(f'{_json.dumps(q)}: {vals[args[0]]}')
+            else:
+                parts.append(f'{_json.dumps(q)}: [{", ".join(str(vals[x]) for x in args)}]')
+        if noise[j]:
+            parts.append('"note": {"level": "info", "tags": ["a", 1, null]}')
+        lines.append("{" + ", ".join(parts) + "}")
+    return "\n".join(lines) + "\n"
