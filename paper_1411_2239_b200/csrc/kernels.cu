@@ -38,7 +38,7 @@ namespace ltl4c {
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast",
                                                 "finalize", "rehash", "heavy", "unit_start",
-                                                "bucket_warp_big", "online_leaf", "online_nodes"};
+                                                "bucket_warp_big", "online_leaf", "online_nodes", "hot"};
 
 namespace {
 
@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
   // A unit above CAP events is split back into its buckets; a bucket above CAP
   // (or overflowing the node tables) is spilled to the next path's list.
   const bool listed = p.list != nullptr;
-  const uint32_t n_items = listed ? (uint32_t)*p.list_len : p.n_units;
+  const uint32_t n_items = listed ? (uint32_t)*p.list_len
+                                  : min(p.n_units, (uint32_t)(*p.nvalid / kUnitTarget) + 2u);
   auto item = [&](uint32_t u, uint32_t &lo, uint32_t &hi) {
     if (listed) { lo = p.list[u]; hi = lo + 1; }
     else { lo = p.unit_start[u]; hi = p.unit_start[u + 1]; }
@@ -981,11 +982,12 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
 #pragma unroll
     for (int v = 0; v < 6; ++v) lacc[f][v] = 0;
   uint32_t ep = 0;
+  const uint32_t n_units = min(p.n_units, (uint32_t)(*p.nvalid / kUnitTarget) + 2u);
   while (true) {
     uint32_t u = 0;
     if (lane == 0) u = atomicAdd(p.bucket_counter, 1u);
     u = __shfl_sync(0xffffffffu, u, 0);
-    if (u >= p.n_units) break;
+    if (u >= n_units) break;
     const uint32_t ubl = p.unit_start[u], ubh = p.unit_start[u + 1];
     if (ubh <= ubl) continue;
     const uint32_t us = p.bucket_off[ubl], ue = p.bucket_off[ubh];

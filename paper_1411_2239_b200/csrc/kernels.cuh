@@ -40,6 +40,7 @@ struct PartPlan {
   int K, bits, passes;
   int hk;                               // key column hashed for the bucket (0; K-1 in online mode)
   const uint32_t *hcol[2];              // that column in buf_key[0] / buf_key[1]
+  const uint32_t *hot_mask;             // K = 1 offline: hot-event bits (pass 0 drops those events), or null
   uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
@@ -47,6 +48,33 @@ struct PartPlan {
   int rank_ballot;                      // stable rank by per-bit ballots instead of match.any
   uint32_t let_mask;                    // (1 << n_atoms) - 1: pass 0 drops letter bits of no atom
   unsigned long long *nvalid;           // bound events of this batch
+  DevAcc *acc;
+};
+
+// Heavy hitters of single-level properties (hot.cu): the most frequent keys are
+// composed in trace order during the first counting pass and never partitioned.
+constexpr int kHotBuckets = 1024;     // hot table: 1024 buckets of 4 keys (one 16-byte probe)
+constexpr int kHotKeys = 1024;        // at most this many hot keys (dense ids 0 .. kHotKeys-1)
+constexpr int kHotSamples = 65536;    // evenly spaced sample of the batch
+constexpr int kHotCountCap = 1 << 17; // sample-count table slots
+constexpr int kHotMinCount = 3;       // a key with >= 3 of 65536 samples (~5e-5 of the events) is hot
+// hot-table bucket: the LOW bits of the partition hash fmix32(k ^ kBucketSalt) (a
+// partition bucket is its HIGH bits), so the counting kernel hashes a key once
+__device__ __forceinline__ uint32_t hot_bucket_of_hash(uint32_t h) { return h & (kHotBuckets - 1); }
+__device__ __forceinline__ uint32_t hot_bucket(uint32_t k) { return hot_bucket_of_hash(fmix32(k ^ kBucketSalt)); }
+struct HotParams {
+  const uint32_t *k0;                   // the batch's key column (K = 1)
+  const uint8_t *let;
+  unsigned long long n;
+  uint32_t *cnt_key, *cnt_val;          // [kHotCountCap] sample counts (key = ABSENT: empty)
+  uint32_t *hot;                        // [kHotBuckets * 4] hot keys (ABSENT: empty)
+  uint16_t *hid;                        // [kHotBuckets * 4] dense id of the key in that slot
+  uint32_t *key_of;                     // [kHotKeys] key of each dense id (ABSENT: unused id)
+  uint32_t *nhot;                       // [0]: dense ids handed out, [1 + c]: keys sampled c times (c < 64)
+  void *partial;                        // [n_chunks][kHotKeys] per-warp-chunk maps (byte form, 4 or 8 B)
+  uint32_t *mask;                       // [n / 32 + 1]: bit j % 32 of word j / 32 = event j is hot
+  int n_chunks;                         // warps of part_count_hot (contiguous tile ranges each)
+  const DevProg *prog;
   DevAcc *acc;
 };
 
@@ -110,7 +138,8 @@ struct BucketParams {
   unsigned long long *spill_len;
   uint32_t *bucket_counter;             // warp path: dynamic unit scheduler
   const uint32_t *unit_start;           // warp path: [n_units + 1] first bucket of each unit
-  uint32_t n_units;
+  uint32_t n_units;                     // for the batch's N events (host)
+  const unsigned long long *nvalid;     // bound events (device): units past nvalid / kUnitTarget + 1 are empty
   const DevProg *prog;
   DevAcc *acc;
   DevTables tab;
@@ -152,6 +181,7 @@ enum KernelId {
   kKBucketWarpBig,
   kKOnlineLeaf,
   kKOnlineNodes,
+  kKHot,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -174,5 +204,9 @@ cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {wa
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);
+cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L);
+cudaError_t launch_part_count_hot(const PartPlan &p, const HotParams &hp, int nq, const Launcher &L);
+cudaError_t launch_hot_finish(const HotParams &hp, int nq, const Launcher &L);
+int hot_ctas_per_sm(int nq);  // resident CTAs of part_count_hot
 
 }  // namespace ltl4c

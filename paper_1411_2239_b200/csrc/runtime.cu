@@ -197,6 +197,9 @@ struct ltl4c_state {
   bool max_bits_set = false;
   uint32_t warp_grid = 0;          // LTL4C_WARP_GRID: cap on the warp kernels' grids (0 = none)
   int rank_ballot = 1;             // LTL4C_RANK_BALLOT: stable rank by ballots (1) or match.any (0)
+  bool hot = true;                 // LTL4C_NO_HOT: no heavy-hitter path for K = 1 (hot.cu)
+  DevBuf<uint32_t> hot_cnt, hot_tab, hot_partial, hot_mask;  // sample counts [2][cap], table [slots + 1], chunk maps, event bits
+  int hot_per_sm = 2;              // resident part_count_hot CTAs per SM
   DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
   DevBuf<uint32_t> exkey[kMaxLevels];
   DevBuf<uint8_t> exlet;
@@ -419,6 +422,15 @@ struct Plan {
   uint32_t NB = 0, n_tiles = 0;
 };
 
+// K = 1 offline batches take the heavy-hitter path (hot.cu) for monitors of <= 8 states
+bool use_hot(const ltl4c_state *st) {
+  return st->hot && st->prog->n_levels == 1 && !(st->flags & LTL4C_STATE_ONLINE) && st->prog->n_states <= 8;
+}
+uint32_t hot_chunks(const ltl4c_state *st, uint32_t n_tiles) {  // one per warp of part_count_hot
+  const uint32_t g = (uint32_t)(st->hot_per_sm * st->n_sms * 8);
+  return n_tiles < g ? n_tiles : g;
+}
+
 // Buffer sizes for a batch of N events (all allocation happens here, outside
 // any stream capture).
 ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
@@ -446,6 +458,12 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->medium_list.ensure(pl->NB));
   CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
+  if (use_hot(st)) {
+    CU(st->hot_cnt.ensure(2 * (size_t)kHotCountCap));
+    CU(st->hot_tab.ensure(4 * kHotBuckets + 2 * kHotBuckets + kHotKeys + 72));  // keys, ids (u16), key_of, nhot + count bins
+    CU(st->hot_partial.ensure((size_t)hot_chunks(st, pl->n_tiles) * kHotKeys * 2));  // 8-byte maps
+    CU(st->hot_mask.ensure(N / 32 + 2));
+  }
   return LTL4C_OK;
 }
 
@@ -473,6 +491,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.spill_len = &st->d_acc.p->medium_buckets;
   bp.unit_start = st->unit_start.p;
   bp.n_units = (uint32_t)(pl.N / kUnitTarget + 2);
+  bp.nvalid = st->d_nvalid.p;
   bp.prog = st->d_prog.p;
   bp.acc = st->d_acc.p;
   bp.tab = st->tab.d;
@@ -522,11 +541,39 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.counts = st->counts.p;
     pl.nvalid = st->d_nvalid.p;
     pl.acc = st->d_acc.p;
+    HotParams hp{};
+    const bool hot = use_hot(st);
+    if (hot) {
+      // heavy hitters: sampled, then composed during the first counting pass
+      hp.k0 = keys[0];
+      hp.let = letters;
+      hp.n = plan.N;
+      hp.cnt_key = st->hot_cnt.p;
+      hp.cnt_val = st->hot_cnt.p + kHotCountCap;
+      hp.hot = st->hot_tab.p;
+      hp.hid = reinterpret_cast<uint16_t *>(st->hot_tab.p + 4 * kHotBuckets);
+      hp.key_of = st->hot_tab.p + 6 * kHotBuckets;
+      hp.nhot = hp.key_of + kHotKeys;
+      hp.partial = st->hot_partial.p;
+      hp.mask = st->hot_mask.p;
+      hp.n_chunks = (int)hot_chunks(st, plan.n_tiles);
+      hp.prog = st->d_prog.p;
+      hp.acc = st->d_acc.p;
+      CU(cudaMemsetAsync(hp.cnt_key, 0xFF, sizeof(uint32_t) * kHotCountCap, s));
+      CU(cudaMemsetAsync(hp.cnt_val, 0, sizeof(uint32_t) * kHotCountCap, s));
+      CU(cudaMemsetAsync(hp.hot, 0xFF, sizeof(uint32_t) * 4 * kHotBuckets, s));
+      CU(cudaMemsetAsync(hp.key_of, 0xFF, sizeof(uint32_t) * kHotKeys, s));
+      CU(cudaMemsetAsync(hp.nhot, 0, sizeof(uint32_t) * 72, s));
+      CU(launch_hot_select(hp, L));
+      pl.hot_mask = hp.mask;
+    }
     for (int pass = 0; pass < plan.P; ++pass) {
-      CU(launch_part_count(pl, pass, L));
+      if (pass == 0 && hot) CU(launch_part_count_hot(pl, hp, (int)prog->n_states, L));
+      else CU(launch_part_count(pl, pass, L));
       CU(launch_part_scan(pl, pass, L));
       CU(launch_part_scatter(pl, pass, L));
     }
+    if (hot) CU(launch_hot_finish(hp, (int)prog->n_states, L));
     CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
@@ -765,7 +812,9 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
                           (const void *)st->oversize_list.p, (const void *)st->medium_list.p,
                           (const void *)st->large_list.p, (const void *)st->unit_start.p,
                           (const void *)st->d_acc.p, (const void *)st->d_out.p, (const void *)st->d_nvalid.p,
-                          (const void *)st->d_prog.p, (const void *)st->h_out})
+                          (const void *)st->d_prog.p, (const void *)st->h_out, (const void *)st->hot_cnt.p,
+                          (const void *)st->hot_tab.p, (const void *)st->hot_partial.p,
+                          (const void *)st->hot_mask.p})
       key.push_back((uintptr_t)b);
     if (st->graph_key != key || !st->graph_exec) {
       drop_graph(st);
@@ -912,6 +961,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   }
   if (const char *e = std::getenv("LTL4C_WARP_GRID")) st->warp_grid = (uint32_t)std::max(0, std::atoi(e));
   if (const char *e = std::getenv("LTL4C_RANK_BALLOT")) st->rank_ballot = std::atoi(e);
+  st->hot = std::getenv("LTL4C_NO_HOT") == nullptr;
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;
@@ -967,6 +1017,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
       e = online_leaf_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states, (int)prog->n_atoms,
                              st->online_cfg);
     if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
+    if (prog->n_levels == 1 && prog->n_states <= 8) st->hot_per_sm = hot_ctas_per_sm((int)prog->n_states);
   }
   cudaSetDevice(prev);
   *out = st;
@@ -1136,6 +1187,10 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->h_lists.release();
   st->h_u32.release();
   st->h_cnt.release();
+  st->hot_cnt.release();
+  st->hot_tab.release();
+  st->hot_partial.release();
+  st->hot_mask.release();
   for (auto &t : st->pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);

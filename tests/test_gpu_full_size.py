@@ -166,3 +166,25 @@ def test_graph_replay_after_reallocation(env):
     _same(st.verify(kb, lb)[0], oracle.run_offline(big.formula, big.keys, big.letters, threads=NPROC), "big")
     st.profile(False)
     _same(st.verify(ks, ls)[0], oracle.run_offline(small.formula, small.keys, small.letters), "small again")
+
+
+def test_K1_heavy_hitter_path_on_and_off(env):
+    """K = 1: the heavy-hitter path (hot.cu; LTL4C_NO_HOT disables it) and the plain
+    partition + heavy segmented scan give the oracle's result, on a Zipf head, on a
+    single giant key, and on a trace with no key frequent enough to be hot."""
+    rng = np.random.default_rng(3)
+    n = 20_000_000
+    cases = [tracegen.zipf_socket_trace(seed=4, n=n, support=1 << 16, s=1.3),
+             tracegen.Trace(tracegen.FILES, [np.where(rng.random(n) < 0.9, 7, rng.integers(0, 1000, n)).astype(np.uint32)],
+                            rng.choice(np.array([0, 1, 2, 3], np.uint8), size=n, p=[0.2, 0.7, 0.05, 0.05])),
+             tracegen.zipf_socket_trace(seed=5, n=n, support=1 << 24, s=0.5)]
+    for tr in cases:
+        want = oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=NPROC)
+        for off in (False, True):
+            if off:
+                os.environ["LTL4C_NO_HOT"] = "1"
+            try:
+                got = _verify(env, tr.formula, tr.keys, tr.letters)[0]
+            finally:
+                os.environ.pop("LTL4C_NO_HOT", None)
+            _same(got, want, (tr.formula, off))
