@@ -175,21 +175,23 @@ __global__ void __launch_bounds__(256, 3) part_count_hot_kernel(PartPlan pl, Hot
   const int lo = pl.lo[0];
   const uint32_t chunk = blockIdx.x * kHotCtaWarps + wid;
   const uint32_t per = (pl.n_tiles + hp.n_chunks - 1) / hp.n_chunks;
-  const uint32_t t0 = min(pl.n_tiles, chunk * per), t1 = min(pl.n_tiles, t0 + per);
+  const uint32_t t0 = chunk * per;
   uint32_t *hist = s.hist[wid];
   M *wmap = s.wmap[wid];
   M *stage = s.stage[wid];
   const uint32_t shift = 32 - pl.bits;  // (K = 1 batches have bits >= 1)
   uint32_t my_cold = 0, my_bound = 0;     // warp-uniform
-  for (uint32_t tile = t0; tile < t1; ++tile) {
+  // trip counts are the same in every warp (collectives stay provably convergent):
+  // a warp's tiles past the batch just see no events
+  for (uint32_t i = 0; i < per; ++i) {
+    const uint32_t tile = t0 + i;
     for (int d = lane; d < kMaxDigits; d += 32) hist[d] = 0;
     __syncwarp();
     const unsigned long long tbase = (unsigned long long)tile * kTileEv;
-    const uint32_t tn = (uint32_t)min((unsigned long long)kTileEv, n - tbase);  // events of the tile
+    const uint32_t tn = tbase < n ? (uint32_t)min((unsigned long long)kTileEv, n - tbase) : 0u;  // events of the tile
     const uint32_t *tk = in_k0 + tbase;
     const uint8_t *tl = in_let + tbase;
     for (uint32_t r0 = 0; r0 < (uint32_t)kTileEv; r0 += 32 * kBatch) {
-      if (r0 >= tn) break;
       uint32_t kk[kBatch];
       uint8_t ll[kBatch];
 #pragma unroll
@@ -232,7 +234,8 @@ __global__ void __launch_bounds__(256, 3) part_count_hot_kernel(PartPlan pl, Hot
       if (lane < kBatch && r0 + 32 * lane < tn) hp.mask[((tbase + r0) >> 5) + lane] = hmask;
     }
     __syncwarp();
-    for (uint32_t d = lane; d <= dmask; d += 32) pl.counts[(size_t)d * pl.n_tiles + tile] = hist[d];
+    if (tile < pl.n_tiles)
+      for (uint32_t d = lane; d <= dmask; d += 32) pl.counts[(size_t)d * pl.n_tiles + tile] = hist[d];
     __syncwarp();
   }
   if (chunk < (uint32_t)hp.n_chunks)
