@@ -196,6 +196,7 @@ struct ltl4c_state {
   int max_bits = kMaxPasses * kMaxDigitBits;  // LTL4C_MAX_BITS: cap on the bucket bits
   bool max_bits_set = false;
   uint32_t warp_grid = 0;          // LTL4C_WARP_GRID: cap on the warp kernels' grids (0 = none)
+  int vshards = 1;                 // LTL4C_VIRTUAL_SHARDS: test-only owner shards on one GPU (run_virtual)
   int rank_ballot = 1;             // LTL4C_RANK_BALLOT: stable rank by ballots (1) or match.any (0)
   bool hot = true;                 // LTL4C_NO_HOT: no heavy-hitter path for K = 1 (hot.cu)
   DevBuf<uint32_t> hot_cnt, hot_tab, hot_partial, hot_mask;  // sample counts [2][cap], table [slots + 1], chunk maps, event bits
@@ -502,11 +503,12 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
 // memsets, SortTrace (count / scan / scatter per pass), mu, the bucket kernels,
 // finalize and the D2H copy of the result record.
 ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *const *keys, const uint8_t *letters,
-                          cudaStream_t s, const Launcher &L, bool finalize_now = true, DevOut *dst = nullptr) {
+                          cudaStream_t s, const Launcher &L, bool finalize_now = true, DevOut *dst = nullptr,
+                          bool zero_acc = true) {
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
-  if (!online) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
+  if (!online && zero_acc) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
   CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
   if (plan.N > 0) {
     CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
@@ -616,66 +618,77 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
   return LTL4C_OK;
 }
 
-// Multi-GPU step 1: route this rank's bound events to their
-// owner rank = top bits of an (independent) hash of k0, with one stable
-// partition pass, then exchange them with grouped NCCL send/recv.  Receive
-// buffers are concatenated in source-rank order; rank r holds the trace range
-// preceding rank r+1's, so every slice keeps its trace order.
+// Multi-GPU step 1a: one stable partition pass of the bound events
+// by owner = top `bits` bits of an (independent) hash of k0 -- every tree node
+// below the root lives on one owner -- into (okey, olet); the per-owner counts
+// are left in totals[0 .. 2^bits) (u32, device).
+ltl4c_status owner_partition(ltl4c_state *st, const uint32_t *const *keys, const uint8_t *letters, uint64_t N,
+                             int bits, uint32_t *const *okey, uint8_t *olet, cudaStream_t s, const Launcher &L) {
+  const int K = (int)st->prog->n_levels;
+  const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
+  CU(st->counts.ensure((size_t)kMaxDigits * n_tiles));
+  CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
+  CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
+  CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
+  CU(cudaMemsetAsync(st->d_sacc.p, 0, sizeof(DevAcc), s));
+  if (N == 0) return LTL4C_OK;
+  PartPlan pl{};
+  for (int l = 0; l < K; ++l) {
+    pl.in_key[l] = keys[l];
+    pl.buf_key[0][l] = okey[l];
+    pl.buf_key[1][l] = okey[l];
+  }
+  pl.in_let = letters;
+  pl.buf_let[0] = olet;
+  pl.buf_let[1] = olet;
+  pl.n = N;
+  pl.n_tiles = n_tiles;
+  pl.K = K;
+  pl.bits = bits;
+  pl.passes = 1;
+  pl.salt = kOwnerSalt;
+  pl.hk = 0;  // owner by level-0 key: whole subtrees per owner
+  pl.hcol[0] = okey[0];
+  pl.hcol[1] = okey[0];
+  pl.rank_ballot = st->rank_ballot;
+  pl.let_mask = (1u << st->prog->n_atoms) - 1u;
+  pl.lo[0] = 0;
+  pl.width[0] = bits;
+  pl.digit_hist = st->totals.p;
+  pl.counts = st->counts.p;
+  pl.nvalid = st->d_nvalid.p;
+  pl.acc = st->d_sacc.p;
+  CU(launch_part_count(pl, 0, L));
+  CU(launch_part_scan(pl, 0, L));
+  CU(launch_part_scatter(pl, 0, L));
+  return LTL4C_OK;
+}
+
+// Multi-GPU step 1b: route this rank's bound events to their owner rank and
+// exchange them with grouped NCCL send/recv.  The per-owner counts are
+// all-gathered from device memory (one host synchronisation to size the
+// transfers).  Receive buffers are concatenated in source-rank order; rank r holds
+// the trace range preceding rank r+1's, so every slice keeps its trace order.
 ltl4c_status exchange(ltl4c_state *st, const uint32_t *const *keys, const uint8_t *letters, uint64_t N,
                       cudaStream_t s, const Launcher &L, uint64_t *M) {
   const int K = (int)st->prog->n_levels, G = st->n_ranks;
   Nccl *nc = nccl();
   if (!nc) return fail(LTL4C_E_NCCL, "NCCL library not found");
-  const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
   for (int l = 0; l < K; ++l) CU(st->bufkey[0][l].ensure(N + 16));
   CU(st->buflet[0].ensure(N + 16));
-  CU(st->counts.ensure((size_t)kMaxDigits * n_tiles));
-  CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
-  CU(st->dc_cnt.ensure((size_t)G + (size_t)G * G));
-  CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
-  CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
-  CU(cudaMemsetAsync(st->d_sacc.p, 0, sizeof(DevAcc), s));
-  if (N > 0) {
-    PartPlan pl{};
-    for (int l = 0; l < K; ++l) {
-      pl.in_key[l] = keys[l];
-      pl.buf_key[0][l] = st->bufkey[0][l].p;
-      pl.buf_key[1][l] = st->bufkey[1][l].p;
-    }
-    pl.in_let = letters;
-    pl.buf_let[0] = st->buflet[0].p;
-    pl.buf_let[1] = st->buflet[1].p;
-    pl.n = N;
-    pl.n_tiles = n_tiles;
-    pl.K = K;
-    pl.bits = st->owner_bits;
-    pl.passes = 1;
-    pl.salt = kOwnerSalt;
-    pl.hk = 0;  // owner rank by level-0 key: whole subtrees per rank
-    pl.hcol[0] = pl.buf_key[0][0];
-    pl.hcol[1] = pl.buf_key[1][0];
-    pl.rank_ballot = st->rank_ballot;
-    pl.let_mask = (1u << st->prog->n_atoms) - 1u;
-    pl.lo[0] = 0;
-    pl.width[0] = st->owner_bits;
-    pl.digit_hist = st->totals.p;
-    pl.counts = st->counts.p;
-    pl.nvalid = st->d_nvalid.p;
-    pl.acc = st->d_sacc.p;
-    CU(launch_part_count(pl, 0, L));
-    CU(launch_part_scan(pl, 0, L));
-    CU(launch_part_scatter(pl, 0, L));
+  CU(st->dc_cnt.ensure((size_t)G * G));
+  uint32_t *ok[kMaxLevels] = {st->bufkey[0][0].p, K > 1 ? st->bufkey[0][1].p : nullptr,
+                              K > 2 ? st->bufkey[0][2].p : nullptr};
+  {
+    ltl4c_status r = owner_partition(st, keys, letters, N, st->owner_bits, ok, st->buflet[0].p, s, L);
+    if (r) return r;
   }
-  // per-owner counts -> all-gathered G x G matrix (row = source rank)
-  uint32_t own[256];
-  CU(cudaMemcpyAsync(own, st->totals.p, sizeof(uint32_t) * G, cudaMemcpyDeviceToHost, s));
+  // per-owner counts (u32, device) -> all-gathered G x G matrix (row = source rank)
+  uint32_t *mat_d = reinterpret_cast<uint32_t *>(st->dc_cnt.p);
+  NC(nc->AllGather(st->totals.p, mat_d, (size_t)G, kNcclUint32, st->comm, s));
+  uint32_t *mat = reinterpret_cast<uint32_t *>(st->hc_cnt);
+  CU(cudaMemcpyAsync(mat, mat_d, sizeof(uint32_t) * G * G, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
-  for (int r = 0; r < G; ++r) st->hc_cnt[r] = own[r];
-  CU(cudaMemcpyAsync(st->dc_cnt.p, st->hc_cnt, sizeof(unsigned long long) * G, cudaMemcpyHostToDevice, s));
-  NC(nc->AllGather(st->dc_cnt.p, st->dc_cnt.p + G, (size_t)G, kNcclUint64, st->comm, s));
-  CU(cudaMemcpyAsync(st->hc_cnt + G, st->dc_cnt.p + G, sizeof(unsigned long long) * G * G, cudaMemcpyDeviceToHost, s));
-  CU(cudaStreamSynchronize(s));
-  const unsigned long long *mat = st->hc_cnt + G;
   std::vector<uint64_t> soff(G), scnt(G), roff(G), rcnt(G);
   uint64_t so = 0, ro = 0;
   for (int r = 0; r < G; ++r) {
@@ -739,6 +752,71 @@ void fill_results(const ltl4c_state *st, const DevOut &o, uint64_t events_seen, 
   }
 }
 
+// Test-only virtual shards (LTL4C_VIRTUAL_SHARDS = G, a power of two <= 256): the
+// multi-GPU owner partition with G owners on this GPU, then each owner's events
+// through the local pipeline in turn with the per-level histograms summed in the
+// accumulators, and the root rule once on the summed depth-1 histogram -- the
+// sharded path of SURVEY §8(e) without the NCCL transport.
+ltl4c_status run_virtual(ltl4c_state *st, const uint32_t *const *keys, const uint8_t *letters, uint64_t N,
+                         cudaStream_t s, const Launcher &L) {
+  const int K = (int)st->prog->n_levels, G = st->vshards;
+  const bool online = st->flags & LTL4C_STATE_ONLINE;
+  int bits = 0;
+  while ((1 << bits) < G) ++bits;
+  for (int l = 0; l < K; ++l) CU(st->exkey[l].ensure(N + 16));
+  CU(st->exlet.ensure(N + 16));
+  uint32_t *ok[kMaxLevels] = {st->exkey[0].p, K > 1 ? st->exkey[1].p : nullptr, K > 2 ? st->exkey[2].p : nullptr};
+  {
+    ltl4c_status r = owner_partition(st, keys, letters, N, bits, ok, st->exlet.p, s, L);
+    if (r) return r;
+  }
+  if (!st->hc_cnt && cudaMallocHost((void **)&st->hc_cnt, sizeof(unsigned long long) * (256 + 256 * 256)) != cudaSuccess)
+    return fail(LTL4C_E_OOM, "pinned allocation failed");
+  uint32_t *cnt = reinterpret_cast<uint32_t *>(st->hc_cnt);
+  if (N > 0) CU(cudaMemcpyAsync(cnt, st->totals.p, sizeof(uint32_t) * G, cudaMemcpyDeviceToHost, s));
+  else std::memset(cnt, 0, sizeof(uint32_t) * G);
+  CU(cudaStreamSynchronize(s));
+  if (!online) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
+  uint64_t off = 0;
+  for (int g = 0; g < G; ++g) {
+    const uint64_t ng = cnt[g];
+    const uint32_t *gk[kMaxLevels] = {nullptr, nullptr, nullptr};
+    for (int l = 0; l < K; ++l) gk[l] = st->exkey[l].p + off;
+    const uint8_t *gl = st->exlet.p + off;
+    off += ng;
+    if (online) {
+      ltl4c_status r = ensure_online_tables(st, ng, s, L);
+      if (r) return r;
+      for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
+      CU(st->tcnt.ensure(kMaxLevels));
+      if (++st->batch_id == 0) st->batch_id = 1;
+      st->enq_events += ng;
+    }
+    Plan plan;
+    {
+      ltl4c_status r = plan_batch(st, ng, &plan);
+      if (r) return r;
+    }
+    // the spill-list lengths of this owner's pass start at zero
+    CU(cudaMemsetAsync(&st->d_acc.p->medium_buckets, 0, 4 * sizeof(unsigned long long), s));
+    ltl4c_status r = enqueue_main(st, plan, gk, gl, s, L, false, nullptr, false);
+    if (r) return r;
+    if (!online && ng > 0) {
+      CU(cudaMemcpyAsync(&st->h_out->oversize_buckets, &st->d_acc.p->oversize_buckets, 2 * sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+      if (st->h_out->oversize_buckets) {
+        ltl4c_status r2 = run_heavy(st, bucket_params(st, plan), K, s, L);
+        if (r2) return r2;
+      }
+    }
+  }
+  CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
+  CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return LTL4C_OK;
+}
+
 // async_dst: pipelined online batch -- the result is copied to this pinned slot
 // and the call returns without waiting (ltl4c_result_get reads it)
 ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, ltl4c_result *out,
@@ -752,6 +830,19 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   if (!online) st->events_seen = 0;
   st->events_seen += N;
   const bool comm = st->comm && (st->n_ranks > 1 || st->force_exchange);
+  if (st->vshards > 1 && !comm && !async_dst) {
+    ltl4c_status r = run_virtual(st, keys, letters, N, s, L);
+    if (r) return r;
+    if (st->h_out->table_overflow) return fail(LTL4C_E_OOM, "carried table overflow");
+    if (online) {
+      st->known_leaves = st->h_out->leaves;
+      for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = st->h_out->nodes[l];
+      st->known_cum = st->enq_events;
+    }
+    fill_results(st, *st->h_out, st->events_seen, false, out);
+    st->verifies++;
+    return LTL4C_OK;
+  }
   uint64_t Nloc = N;
   const uint32_t *lkeys[kMaxLevels] = {keys[0], K > 1 ? keys[1] : nullptr, K > 2 ? keys[2] : nullptr};
   const uint8_t *llet = letters;
@@ -962,6 +1053,10 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   if (const char *e = std::getenv("LTL4C_WARP_GRID")) st->warp_grid = (uint32_t)std::max(0, std::atoi(e));
   if (const char *e = std::getenv("LTL4C_RANK_BALLOT")) st->rank_ballot = std::atoi(e);
   st->hot = std::getenv("LTL4C_NO_HOT") == nullptr;
+  if (const char *e = std::getenv("LTL4C_VIRTUAL_SHARDS")) {
+    const int g = std::atoi(e);
+    if (g > 1 && g <= 256 && !(g & (g - 1))) st->vshards = g;
+  }
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;

@@ -468,3 +468,36 @@ def test_records_through_encoder_and_gpu(env):
         got = st.verify(k, l)[0]
         mon.feed_records(chunk)
         _assert_same(got, mon.evaluate(), ("online records", lo))
+
+
+@pytest.mark.parametrize("shards", [2, 4, 8])
+def test_virtual_shards(env, shards):
+    """SURVEY §4 T4 / §8(e) on one GPU: LTL4C_VIRTUAL_SHARDS = G runs the multi-GPU
+    owner partition (hash of k0) with G logical owners, each owner's events through
+    the local pipeline, the per-level histograms summed and the root rule applied
+    once -- offline (K = 1, 2, 3) and online batches, against the oracle."""
+    import os
+    ltl4c, torch, dev = env
+    os.environ["LTL4C_VIRTUAL_SHARDS"] = str(shards)
+    try:
+        for tr in (tracegen.login_trace(seed=51, n=400_000, users=3000, rid_events=3, p_unauth=0.05),
+                   tracegen.zipf_socket_trace(seed=52, n=600_000, support=1 << 14),
+                   tracegen.proxy_trace(seed=53, n=500_000, videos=3000)):
+            _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                         oracle.run_offline(tr.formula, tr.keys, tr.letters), (shards, tr.meta))
+        tr = tracegen.c5_trace(seed=54, n=300_000, users=2000, hosts=64, span_events=60_000)
+        prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+        st = prog.state(0, online=True)
+        props = [oracle.Property(t) for t in tracegen.C5_FORMULAS]
+        for lo, hi in [(0, 1), (1, 70_000), (70_000, 300_000)]:
+            k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+            got = st.verify(k, l, first_index=lo)
+            for f, p in enumerate(props):
+                want = oracle.run_offline(tracegen.C5_FORMULAS[f], [x[:hi] for x in tr.keys],
+                                          _project(tr.letters[:hi], prog.atoms, p.atoms))
+                _assert_same(got[f], want, (shards, hi, f))
+        k, l = _dev(torch, dev, [np.zeros(0, np.uint32)] * 2, np.zeros(0, np.uint8))
+        got = ltl4c.compile(tracegen.LOGIN).state(0).verify(k, l)[0]
+        _assert_same(got, oracle.run_offline(tracegen.LOGIN, [np.zeros(0, np.uint32)] * 2, np.zeros(0, np.uint8)))
+    finally:
+        os.environ.pop("LTL4C_VIRTUAL_SHARDS", None)
