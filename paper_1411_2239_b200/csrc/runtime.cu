@@ -628,6 +628,7 @@ ltl4c_status owner_partition(ltl4c_state *st, const uint32_t *const *keys, const
   const uint32_t n_tiles = (uint32_t)std::max<uint64_t>(1, (N + kTileEv - 1) / kTileEv);
   CU(st->counts.ensure((size_t)kMaxDigits * n_tiles));
   CU(st->totals.ensure(kMaxPasses * kMaxDigits + 16));
+  CU(st->d_sacc.ensure(1));  // (virtual shards run without a communicator)
   CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
   CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
   CU(cudaMemsetAsync(st->d_sacc.p, 0, sizeof(DevAcc), s));
