@@ -6,24 +6,30 @@
 // u^D)) (Def. 5) and delta* over a slice is the ordered composition
 // of the letters' transition maps (associative).  Instead of partitioning the
 // events of the most frequent keys (most of the trace under Zipf skew), they are
-// composed where they lie:
+// composed where they lie, and only the rest of the trace is partitioned:
 //
-//   hot_sample   S evenly spaced events -> sample counts per key (L2 table)
-//   hot_select   keys with >= kHotMinCount samples -> hot table (<= kHotKeys)
-//   part_count_hot  the first partition pass's counting kernel as persistent
-//                CTAs over contiguous tile ranges: cold events are counted by
-//                digit as usual; a hot event's letter map is composed, in trace
-//                order, onto its warp's map of that key (lanes sharing a key in
-//                a round are grouped by __match_any_sync and their maps composed
-//                in lane order); at the end of a tile the warps' maps are
-//                composed onto the CTA's map in warp order; each CTA writes its
-//                chunk's map per hot key
-//   (the first scatter pass drops hot events: they never enter the partition)
-//   hot_finish   per hot key: the CTA chunk maps composed in chunk order (an
-//                ordered shuffle tree), q = map(q0), lambda_f(q) -> the leaf
-//                histogram hist[f][1]
-// Which keys are hot does not change the result (each key is wholly hot or
-// wholly cold); the sample only decides where the work goes.
+//   hot_sample    S evenly spaced events -> sample counts per key (L2 table)
+//   hot_insert    the most sampled keys take a slot of the hot table: 2-way
+//                 buckets indexed by the LOW bits of the partition hash (a key
+//                 whose bucket is full stays cold: hotness only moves work);
+//                 the slot index is the key's dense id
+//   hot_compose   warp per contiguous chunk of the trace, 32 events per round in
+//                 trace order: a hot event's letter is applied to the warp's
+//                 transition map of its key (lanes sharing a key in a round are
+//                 grouped by __match_any_sync and their letters applied by the
+//                 lowest lane in lane order); cold events are compacted, in trace
+//                 order, into the chunk's own range of a scratch buffer; each
+//                 warp finally writes its chunk's map of every slot
+//   hot_gather    the chunks' cold runs concatenated in chunk order: a dense
+//                 cold stream, which the ordinary partition then takes as input
+//   hot_finish    per slot: the chunk maps composed in chunk order, q =
+//                 map(q0), lambda_f(q) -> the leaf histogram hist[f][1]
+//
+// Maps (the image of every start state):
+//   MAPK 0 (nq <= 4 states, <= 16 letters): 2 bits per state in one byte; a
+//          letter is applied through a [256][A] shared-memory table;
+//   MAPK 1 (nq <= 8 states): byte q of a u64 is the image of q; (g o f) is a
+//          byte permutation of g selected by f (PRMT).
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -35,244 +41,345 @@ namespace ltl4c {
 namespace {
 
 constexpr uint32_t kCntSalt = 0x165667b1u;   // sample-count table hash
-
-// Transition maps of monitors with at most NQB (<= 8) states in byte form: byte q
-// is the image of state q (u32 for NQB <= 4, u64 for NQB <= 8).  (g o f)[q] =
-// g[f[q]] is a byte permutation of g selected by f: PRMT with f's bytes packed
-// into selector nibbles.
-template <int NQB> struct HotMap { using T = uint32_t; };
-template <> struct HotMap<8> { using T = unsigned long long; };
+constexpr int kHotBatch = 16;                // rounds of 32 events whose loads are issued together
 
 __device__ __forceinline__ uint32_t sel_of(uint32_t f) {  // bytes b0..b3 (< 8) -> nibbles b0 | b1 << 4 | ...
   const uint32_t x = f | (f >> 4);
   return __byte_perm(x, 0u, 0x4420u);
 }
-__device__ __forceinline__ uint32_t hot_apply(uint32_t g, uint32_t f) { return __byte_perm(g, 0u, sel_of(f)); }
-__device__ __forceinline__ unsigned long long hot_apply(unsigned long long g, unsigned long long f) {
+// (g o f) on byte-form maps: (g o f)[q] = g[f[q]]
+__device__ __forceinline__ uint32_t byte_apply(uint32_t g, uint32_t f) { return __byte_perm(g, 0u, sel_of(f)); }
+__device__ __forceinline__ unsigned long long byte_apply(unsigned long long g, unsigned long long f) {
   const uint32_t glo = (uint32_t)g, ghi = (uint32_t)(g >> 32);
   const uint32_t lo = __byte_perm(glo, ghi, sel_of((uint32_t)f));
   const uint32_t hi = __byte_perm(glo, ghi, sel_of((uint32_t)(f >> 32)));
   return (unsigned long long)hi << 32 | lo;
 }
-template <int NQB>
-__device__ __forceinline__ typename HotMap<NQB>::T hot_ident() {
-  return (typename HotMap<NQB>::T)0x0706050403020100ull;
-}
-template <int NQB>
-__device__ __forceinline__ uint32_t hot_image(typename HotMap<NQB>::T m, uint32_t q) {
-  return (uint32_t)(m >> (8 * q)) & 0xFFu;
-}
 
-__global__ void hot_sample_kernel(HotParams hp) {
-  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+template <int MAPK> struct HotMap;
+template <> struct HotMap<0> {
+  using T = uint8_t;                              // packed: bits 2q..2q+1 = image of q
+  using B = uint32_t;                             // byte form used by hot_finish
+  static constexpr int kSlots = kHotSlotsMax;
+  __device__ static T ident() { return 0xE4; }    // 3 2 1 0
+};
+template <> struct HotMap<1> {
+  using T = unsigned long long;                   // byte form
+  using B = unsigned long long;
+  static constexpr int kSlots = kHotSlotsMax / 4;
+  __device__ static T ident() { return 0x0706050403020100ull; }
+};
+
+// a CTA aggregates its kSampleBlock samples in a shared-memory table first, so a
+// hot key costs one global atomic per CTA (not one per sample)
+constexpr int kSampleBlock = 2048, kSampleTab = 4096;
+__global__ void __launch_bounds__(256) hot_sample_kernel(HotParams hp) {
+  __shared__ uint32_t tk[kSampleTab], tc[kSampleTab];
+  for (int i = threadIdx.x; i < kSampleTab; i += blockDim.x) { tk[i] = kAbsent; tc[i] = 0; }
+  __syncthreads();
   const unsigned long long n = hp.n;
-  if (i >= (uint32_t)kHotSamples || n == 0) return;
-  const unsigned long long j = (unsigned long long)i * n / (unsigned long long)kHotSamples;
-  const uint32_t k = hp.k0[j];
-  if (k == kAbsent) return;
-  uint32_t h = fmix32(k ^ kCntSalt) & (kHotCountCap - 1);
-  for (int probes = 0; probes < kHotCountCap; ++probes) {
-    uint32_t t = hp.cnt_key[h];
-    if (t == kAbsent) {
-      const uint32_t o = atomicCAS(&hp.cnt_key[h], kAbsent, k);
-      t = o == kAbsent ? k : o;
+  for (int x = threadIdx.x; x < kSampleBlock; x += blockDim.x) {
+    const uint32_t i = blockIdx.x * kSampleBlock + x;
+    if (i >= hp.n_samples) break;
+    const unsigned long long j = (unsigned long long)i * n / (unsigned long long)hp.n_samples;
+    const uint32_t k = hp.k0[j];
+    if (k == kAbsent) continue;
+    uint32_t h = fmix32(k ^ kCntSalt) & (kSampleTab - 1);
+    while (true) {  // (at most kSampleBlock < kSampleTab keys)
+      uint32_t t = tk[h];
+      if (t == kAbsent) {
+        const uint32_t o = atomicCAS(&tk[h], kAbsent, k);
+        t = o == kAbsent ? k : o;
+      }
+      if (t == k) { atomicAdd(&tc[h], 1u); break; }
+      h = (h + 1) & (kSampleTab - 1);
     }
-    if (t == k) {
-      atomicAdd(&hp.cnt_val[h], 1u);
-      return;
+  }
+  __syncthreads();
+  for (int x = threadIdx.x; x < kSampleTab; x += blockDim.x) {
+    const uint32_t k = tk[x];
+    if (k == kAbsent) continue;
+    uint32_t h = fmix32(k ^ kCntSalt) & (kHotCountCap - 1);
+    for (int probes = 0; probes < kHotCountCap; ++probes) {
+      uint32_t t = hp.cnt_key[h];
+      if (t == kAbsent) {
+        const uint32_t o = atomicCAS(&hp.cnt_key[h], kAbsent, k);
+        t = o == kAbsent ? k : o;
+      }
+      if (t == k) { atomicAdd(&hp.cnt_val[h], tc[x]); break; }
+      h = (h + 1) & (kHotCountCap - 1);
     }
-    h = (h + 1) & (kHotCountCap - 1);
   }
 }
 
-// the most sampled keys are hot: a histogram of the sample counts (bin 63 = 63 or
-// more) gives the smallest threshold t >= kHotMinCount with at most kHotKeys keys
-// counted >= t
+// histogram of the sample counts (bin 63 = 63 or more)
 __global__ void hot_count_hist_kernel(HotParams hp) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= (uint32_t)kHotCountCap) return;
   const uint32_t c = hp.cnt_val[s];
-  if (c >= (uint32_t)kHotMinCount) atomicAdd(&hp.nhot[1 + min(c, 63u)], 1u);
+  if (c >= (uint32_t)kHotMinCount) atomicAdd(&hp.nhot[8 + min(c, 63u)], 1u);
 }
 
-// keys counted >= t get a dense id and a slot of their table bucket (a key whose
-// bucket is full stays cold: hotness only moves work)
-__global__ void hot_select_kernel(HotParams hp) {
+// keys sampled >= t times, t the smallest threshold >= kHotMinCount leaving at
+// most 3/4 of the slots wanted, take a slot of their bucket; the most sampled
+// first (pass 0: counts >= 4t, pass 1: the rest).  nhot[0] = keys inserted.
+__global__ void hot_insert_kernel(HotParams hp, int pass) {
   __shared__ uint32_t thr;
   if (threadIdx.x == 0) {
+    const uint32_t want = (uint32_t)hp.slots * 3 / 4;
     uint32_t t = 64, tot = 0;
-    while (t > (uint32_t)kHotMinCount && tot + hp.nhot[1 + t - 1] <= (uint32_t)kHotKeys) tot += hp.nhot[1 + --t];
+    while (t > (uint32_t)kHotMinCount && tot + hp.nhot[8 + t - 1] <= want) tot += hp.nhot[8 + --t];
     thr = t;  // keys with count >= t (bin t - 1 and below did not fit)
   }
   __syncthreads();
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= (uint32_t)kHotCountCap || hp.cnt_val[s] < thr || thr >= 64) return;
+  if (s >= (uint32_t)kHotCountCap || thr >= 64) return;
+  const uint32_t c = hp.cnt_val[s];
+  if (pass == 0 ? c < 4 * thr : (c < thr || c >= 4 * thr)) return;
   const uint32_t k = hp.cnt_key[s];
-  const uint32_t id = atomicAdd(hp.nhot, 1u);
-  if (id >= (uint32_t)kHotKeys) return;
-  const uint32_t b = hot_bucket(k);
-  for (int i = 0; i < 4; ++i) {
-    if (atomicCAS(&hp.hot[4 * b + i], kAbsent, k) == kAbsent) {
-      hp.hid[4 * b + i] = (uint16_t)id;
-      hp.key_of[id] = k;
+  const uint32_t b = (fmix32(k ^ kBucketSalt) & (uint32_t)(hp.slots / 2 - 1)) * 2;
+  for (int i = 0; i < 2; ++i)
+    if (atomicCAS(&hp.slot_key[b + i], kAbsent, k) == kAbsent) {
+      atomicAdd(hp.nhot, 1u);
       return;
     }
-  }
 }
 
-constexpr int kHotCtaWarps = 8;
-template <int NQB>
+template <int MAPK>
 struct HotSmem {
-  using M = typename HotMap<NQB>::T;
-  uint4 hot[kHotBuckets];                  // the hot table (4 keys per bucket)
-  uint16_t hid[kHotBuckets * 4];
-  M smap[kMaxLetters];                     // letter maps
-  M wmap[kHotCtaWarps][kHotKeys];          // each warp's map of every hot key over its chunk so far
-  uint32_t hist[kHotCtaWarps][kMaxDigits]; // each warp's digit counts of its current tile
-  M stage[kHotCtaWarps][32];
+  using M = typename HotMap<MAPK>::T;
+  static constexpr int S = HotMap<MAPK>::kSlots;
+  uint32_t key[S];                          // slot -> hot key (ABSENT: empty)
+  M wmap[kHotCtaWarps][S];                  // each warp's map of every slot over its chunk so far
+  uint8_t stage[kHotCtaWarps][32];          // the round's letters
+  // MAPK 0: [256][A] letter table; MAPK 1: [A] letter maps
+  alignas(16) uint8_t tab[MAPK == 0 ? 256 * 16 : 8 * kMaxLetters];
 };
 
-// dense hot id of key k (partition hash h), or -1 (one 16-byte shared-memory probe)
-__device__ __forceinline__ int hot_id(const uint4 *tab, const uint16_t *hid, uint32_t k, uint32_t h) {
-  const uint32_t b = hot_bucket_of_hash(h);
-  const uint4 v = tab[b];
-  const int i = v.x == k ? 0 : v.y == k ? 1 : v.z == k ? 2 : v.w == k ? 3 : -1;
-  return i < 0 ? -1 : (int)hid[4 * b + i];
-}
-
-// The first partition pass's count kernel with the hot keys composed on the fly
-// (K = 1).  Every WARP owns a contiguous range of tiles (a chunk) and walks it in
-// trace order, 32 events per round: cold events are counted by digit into the
-// warp's histogram of the tile (written to counts[d][tile] at the tile's end);
-// lanes holding a hot key are grouped by __match_any_sync, the group's letter
-// maps composed in lane (= trace) order by its lowest lane and that onto the
-// warp's map of the key.  Each round's hot ballot goes to hp.mask (the first
-// scatter pass drops those events); each warp finally writes its chunk's maps.
-template <int NQB>
-__global__ void __launch_bounds__(256, 3) part_count_hot_kernel(PartPlan pl, HotParams hp) {
-  using M = typename HotMap<NQB>::T;
-  constexpr int kBatch = 16;  // rounds whose loads are issued together
+// One warp per contiguous chunk [e0, e1) of the batch (multiple of 512 events).
+template <int MAPK>
+__global__ void __launch_bounds__(32 * kHotCtaWarps, 4) hot_compose_kernel(HotParams hp) {
+  using HM = HotMap<MAPK>;
+  using M = typename HM::T;
+  constexpr int S = HM::kSlots;
   extern __shared__ __align__(16) uint8_t raw[];
-  HotSmem<NQB> &s = *reinterpret_cast<HotSmem<NQB> *>(raw);
+  HotSmem<MAPK> &s = *reinterpret_cast<HotSmem<MAPK> *>(raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const M ident = hot_ident<NQB>();
   const DevProg *prog = hp.prog;
   const int A = 1 << prog->na, nq = prog->nq;
-  for (int i = tid; i < kHotBuckets; i += blockDim.x) s.hot[i] = reinterpret_cast<const uint4 *>(hp.hot)[i];
-  for (int i = tid; i < kHotBuckets * 4; i += blockDim.x) s.hid[i] = hp.hid[i];
-  for (int a = tid; a < A; a += blockDim.x) {
-    M m = ident;
-    for (int q = 0; q < nq; ++q) m = (m & ~((M)0xFF << (8 * q))) | ((M)prog->delta[q][a] << (8 * q));
-    s.smap[a] = m;
-  }
-  for (int i = lane; i < kHotKeys; i += 32) s.wmap[wid][i] = ident;
-  __syncthreads();
-  const bool any_hot = *hp.nhot > 0;
-  const uint32_t *in_k0 = pl.in_key[0];
-  const uint8_t *in_let = pl.in_let;
-  const unsigned long long n = pl.n;
-  const uint32_t dmask = (1u << pl.width[0]) - 1u;
-  const int lo = pl.lo[0];
-  const uint32_t chunk = blockIdx.x * kHotCtaWarps + wid;
-  const uint32_t per = (pl.n_tiles + hp.n_chunks - 1) / hp.n_chunks;
-  const uint32_t t0 = chunk * per;
-  uint32_t *hist = s.hist[wid];
-  M *wmap = s.wmap[wid];
-  M *stage = s.stage[wid];
-  const uint32_t shift = 32 - pl.bits;  // (K = 1 batches have bits >= 1)
-  uint32_t my_cold = 0, my_bound = 0;     // warp-uniform
-  // trip counts are the same in every warp (collectives stay provably convergent):
-  // a warp's tiles past the batch just see no events
-  for (uint32_t i = 0; i < per; ++i) {
-    const uint32_t tile = t0 + i;
-    for (int d = lane; d < kMaxDigits; d += 32) hist[d] = 0;
-    __syncwarp();
-    const unsigned long long tbase = (unsigned long long)tile * kTileEv;
-    const uint32_t tn = tbase < n ? (uint32_t)min((unsigned long long)kTileEv, n - tbase) : 0u;  // events of the tile
-    const uint32_t *tk = in_k0 + tbase;
-    const uint8_t *tl = in_let + tbase;
-    for (uint32_t r0 = 0; r0 < (uint32_t)kTileEv; r0 += 32 * kBatch) {
-      uint32_t kk[kBatch];
-      uint8_t ll[kBatch];
-#pragma unroll
-      for (int r = 0; r < kBatch; ++r) {  // every load of the batch first (memory-level parallelism)
-        const uint32_t j = r0 + r * 32 + lane;
-        const bool in = j < tn;
-        kk[r] = in ? __ldcs(&tk[j]) : kAbsent;
-        ll[r] = in ? (uint8_t)(__ldcs(&tl[j]) & pl.let_mask) : (uint8_t)0;
+  for (int i = tid; i < S; i += blockDim.x) s.key[i] = hp.slot_key[i];
+  if (MAPK == 0) {
+    for (int i = tid; i < 256 * A; i += blockDim.x) {
+      const uint32_t m = (uint32_t)i / A, a = (uint32_t)i % A;
+      uint32_t o = 0;
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t img = (m >> (2 * q)) & 3u;
+        o |= (img < (uint32_t)nq ? (uint32_t)prog->delta[img][a] & 3u : img) << (2 * q);
       }
-      uint32_t hmask = 0;  // lane r: the hot ballot of round r
+      s.tab[i] = (uint8_t)o;
+    }
+  } else {
+    unsigned long long *smap = reinterpret_cast<unsigned long long *>(s.tab);
+    for (int a = tid; a < A; a += blockDim.x) {
+      unsigned long long m = HotMap<1>::ident();
+      for (int q = 0; q < nq; ++q) m = (m & ~(0xFFull << (8 * q))) | ((unsigned long long)prog->delta[q][a] << (8 * q));
+      smap[a] = m;
+    }
+  }
+  for (int i = lane; i < S; i += 32) s.wmap[wid][i] = HM::ident();
+  __syncthreads();
+  const bool dense = hp.nhot[0] > 0;  // no hot key: nothing composed, the partition reads the batch itself
+  const uint32_t chunk = blockIdx.x * kHotCtaWarps + wid;
+  const unsigned long long n = hp.n;
+  const unsigned long long e0 = (unsigned long long)chunk * hp.chunk_ev;
+  const unsigned long long e1 = min(n, e0 + hp.chunk_ev);
+  M *wmap = s.wmap[wid];
+  uint8_t *stage = s.stage[wid];
+  const uint8_t *tab = s.tab;
+  const unsigned long long *smap = reinterpret_cast<const unsigned long long *>(s.tab);
+  const uint32_t let_mask = hp.let_mask;
+  uint32_t ncold = 0, nhot = 0;  // warp-uniform
+  if (dense && chunk < (uint32_t)hp.n_chunks) {
+    for (unsigned long long r0 = e0; r0 < e1; r0 += 32 * kHotBatch) {
+      uint32_t kk[kHotBatch];
+      uint8_t ll[kHotBatch];
 #pragma unroll
-      for (int r = 0; r < kBatch; ++r) {
+      for (int r = 0; r < kHotBatch; ++r) {  // every load of the batch first (memory-level parallelism)
+        const unsigned long long j = r0 + r * 32 + lane;
+        const bool in = j < e1;
+        kk[r] = in ? __ldcs(&hp.k0[j]) : kAbsent;
+        ll[r] = in ? (uint8_t)(__ldcs(&hp.let[j]) & let_mask) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int r = 0; r < kHotBatch; ++r) {
         const uint32_t k = kk[r];
         const bool valid = k != kAbsent;
-        const uint32_t h = fmix32(k ^ pl.salt);
-        const int id = valid && any_hot ? hot_id(s.hot, s.hid, k, h) : -1;
-        const bool cold = valid && id < 0;
-        if (cold) atomicAdd(&hist[(h >> shift >> lo) & dmask], 1u);
-        my_bound += __popc(__ballot_sync(0xffffffffu, valid));
-        my_cold += __popc(__ballot_sync(0xffffffffu, cold));
-        const uint32_t hm = __ballot_sync(0xffffffffu, id >= 0);
-        if (lane == r) hmask = hm;
+        const uint32_t b = (fmix32(k ^ kBucketSalt) & (uint32_t)(S / 2 - 1)) * 2;
+        const uint2 t = *reinterpret_cast<const uint2 *>(&s.key[b]);
+        const int slot = !valid ? -1 : t.x == k ? (int)b : t.y == k ? (int)b + 1 : -1;
+        const bool cold = valid && slot < 0;
+        const uint32_t cm = __ballot_sync(0xffffffffu, cold);
+        if (cold) {
+          const unsigned long long p = e0 + ncold + __popc(cm & lanemask_lt());
+          hp.cold_key[p] = k;
+          hp.cold_let[p] = ll[r];
+        }
+        ncold += __popc(cm);
+        const uint32_t hm = __ballot_sync(0xffffffffu, slot >= 0);
+        nhot += __popc(hm);
         if (hm) {
-          stage[lane] = s.smap[ll[r]];
-          const uint32_t peers = __match_any_sync(0xffffffffu, id);
+          stage[lane] = ll[r];
           __syncwarp();
-          if (id >= 0 && (peers & lanemask_lt()) == 0) {
-            M m = stage[lane];
-            uint32_t pm = peers & (peers - 1);
-            while (pm) {
-              const int i = __ffs(pm) - 1;
-              pm &= pm - 1;
-              m = hot_apply(stage[i], m);
+          if (slot >= 0) {
+            const uint32_t peers = __match_any_sync(hm, (uint32_t)slot);
+            if ((peers & lanemask_lt()) == 0) {  // lowest lane of its group: the letters in lane order
+              M m = wmap[slot];
+              uint32_t pm = peers;
+              do {
+                const int i = __ffs(pm) - 1;
+                pm &= pm - 1;
+                if (MAPK == 0) m = (M)tab[(uint32_t)m * A + stage[i]];
+                else m = (M)byte_apply(smap[stage[i]], (unsigned long long)m);
+              } while (pm);
+              wmap[slot] = m;
             }
-            wmap[id] = hot_apply(m, wmap[id]);
           }
           __syncwarp();
         }
       }
-      if (lane < kBatch && r0 + 32 * lane < tn) hp.mask[((tbase + r0) >> 5) + lane] = hmask;
     }
-    __syncwarp();
-    if (tile < pl.n_tiles)
-      for (uint32_t d = lane; d <= dmask; d += 32) pl.counts[(size_t)d * pl.n_tiles + tile] = hist[d];
-    __syncwarp();
   }
-  if (chunk < (uint32_t)hp.n_chunks)
-    for (int i = lane; i < kHotKeys; i += 32) reinterpret_cast<M *>(hp.partial)[(size_t)chunk * kHotKeys + i] = wmap[i];
-  if (lane == 0) {
-    if (my_cold) atomicAdd(pl.nvalid, (unsigned long long)my_cold);
-    if (my_bound) atomicAdd(&pl.acc->events_bound, (unsigned long long)my_bound);
+  __syncwarp();
+  if (chunk < (uint32_t)hp.n_chunks) {
+    if (dense) {
+      M *out = reinterpret_cast<M *>(hp.partial) + (size_t)chunk * S;
+      if (MAPK == 0) {
+        const uint32_t *w4 = reinterpret_cast<const uint32_t *>(wmap);
+        uint32_t *o4 = reinterpret_cast<uint32_t *>(out);
+        for (int i = lane; i < S / 4; i += 32) o4[i] = w4[i];
+      } else {
+        for (int i = lane; i < S; i += 32) out[i] = wmap[i];
+      }
+    }
+    if (lane == 0) {
+      hp.chunk_cold[chunk] = ncold;
+      if (ncold) atomicAdd(hp.n_cold, (unsigned long long)ncold);
+      if (nhot) atomicAdd(&hp.acc->events_bound, (unsigned long long)nhot);
+    }
   }
 }
 
-// per hot key (a warp each): the chunk maps composed in chunk order, the leaf's
-// verdicts (Def. 5) into the leaf histogram
-template <int NQB>
-__global__ void __launch_bounds__(256) hot_finish_kernel(HotParams hp, int n_chunks) {
-  using M = typename HotMap<NQB>::T;
-  __shared__ uint32_t sacc[kMaxFormulas * 6];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x) sacc[i] = 0;
-  __syncthreads();
-  const DevProg *prog = hp.prog;
-  const M ident = hot_ident<NQB>();
-  const M *partial = reinterpret_cast<const M *>(hp.partial);
-  const int id = blockIdx.x * (blockDim.x >> 5) + wid;
-  if (id < kHotKeys && hp.key_of[id] != kAbsent) {
-    const int per = (n_chunks + 31) / 32;
-    const int c0 = min(n_chunks, lane * per), c1 = min(n_chunks, c0 + per);
-    M m = ident;
-    for (int c = c0; c < c1; ++c) m = hot_apply(partial[(size_t)c * kHotKeys + id], m);
+// exclusive prefix of the chunks' cold counts (one CTA) -> chunk_pre
+__global__ void __launch_bounds__(1024) hot_prefix_kernel(HotParams hp) {
+  __shared__ uint32_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int nc = hp.n_chunks, per = (nc + 1023) / 1024;
+  const int c0 = min(nc, tid * per), c1 = min(nc, c0 + per);
+  uint32_t sum = 0;
+  for (int c = c0; c < c1; ++c) sum += hp.chunk_cold[c];
+  uint32_t inc = sum;
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // ordered tree: lane l's range precedes lane l + d's
-      const M o = __shfl_down_sync(0xffffffffu, m, d);
-      if ((lane & (2 * d - 1)) == 0) m = hot_apply(o, m);
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t t = wsum[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += y;
     }
-    if (lane == 0) {
-      const uint32_t q = hot_image<NQB>(m, prog->q0);
-      for (uint32_t f = 0; f < prog->nf; ++f) atomicAdd(&sacc[f * 6 + prog->lab[f][q]], 1u);
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  uint32_t run = inc - sum + (wid ? wsum[wid - 1] : 0u);
+  for (int c = c0; c < c1; ++c) {
+    hp.chunk_pre[c] = run;
+    run += hp.chunk_cold[c];
+  }
+}
+
+// kGatherParts CTAs per chunk move its cold run to the dense stream (4 elements
+// per thread in flight)
+constexpr int kGatherParts = 4;
+__global__ void __launch_bounds__(256) hot_gather_kernel(HotParams hp) {
+  const uint32_t chunk = blockIdx.x / kGatherParts, part = blockIdx.x % kGatherParts;
+  if (chunk >= (uint32_t)hp.n_chunks || hp.nhot[0] == 0) return;
+  const uint32_t cnt = hp.chunk_cold[chunk];
+  const uint32_t per = (cnt + kGatherParts - 1) / kGatherParts;
+  const uint32_t lo = min(cnt, part * per), hi = min(cnt, lo + per);
+  const unsigned long long src = (unsigned long long)chunk * hp.chunk_ev;
+  const uint32_t *sk = hp.cold_key + src;
+  const uint8_t *sl = hp.cold_let + src;
+  uint32_t *dk = hp.dense_key + hp.chunk_pre[chunk];
+  uint8_t *dl = hp.dense_let + hp.chunk_pre[chunk];
+  for (uint32_t i = lo + threadIdx.x; i < hi; i += 4 * blockDim.x) {
+    uint32_t k[4];
+    uint8_t l[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t x = i + u * blockDim.x;
+      k[u] = x < hi ? __ldcs(&sk[x]) : 0u;
+      l[u] = x < hi ? __ldcs(&sl[x]) : (uint8_t)0;
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t x = i + u * blockDim.x;
+      if (x < hi) { dk[x] = k[u]; dl[x] = l[u]; }
+    }
+  }
+}
+
+// per slot (x: 32 consecutive slots, y: 32 ranges of chunks): the chunk maps in
+// chunk order, then the leaf's verdicts (Def. 5) into the leaf histogram
+template <int MAPK>
+__global__ void __launch_bounds__(1024) hot_finish_kernel(HotParams hp) {
+  using HM = HotMap<MAPK>;
+  using M = typename HM::T;
+  using Bm = typename HM::B;
+  constexpr int S = HM::kSlots;
+  constexpr int kU = 4;
+  __shared__ Bm part[32][33];
+  __shared__ uint32_t unpack[256];
+  __shared__ uint32_t sacc[kMaxFormulas * 6];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x) sacc[i] = 0;
+  if (MAPK == 0)
+    for (int m = threadIdx.x; m < 256; m += blockDim.x) {
+      uint32_t o = 0;
+      for (int q = 0; q < 4; ++q) o |= ((m >> (2 * q)) & 3u) << (8 * q);
+      unpack[m] = o;
+    }
+  __syncthreads();
+  if (hp.nhot[0] == 0) return;
+  const DevProg *prog = hp.prog;
+  const int slot = blockIdx.x * 32 + tx;
+  const int nc = hp.n_chunks, per = (nc + 31) / 32;
+  const int c0 = min(nc, ty * per), c1 = min(nc, c0 + per);
+  const M *partial = reinterpret_cast<const M *>(hp.partial);
+  Bm m = (Bm)HotMap<1>::ident();
+  for (int c = c0; c < c1; c += kU) {
+    M x[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) x[u] = c + u < c1 ? partial[(size_t)(c + u) * S + slot] : HM::ident();
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      Bm f;
+      if (MAPK == 0) f = (Bm)unpack[(uint32_t)x[u]];
+      else f = (Bm)x[u];
+      m = byte_apply(f, m);
+    }
+  }
+  part[ty][tx] = m;
+  __syncthreads();
+  if (ty == 0 && hp.slot_key[slot] != kAbsent) {
+    Bm t = part[0][tx];
+    for (int g = 1; g < 32; ++g) t = byte_apply(part[g][tx], t);
+    const uint32_t q = (uint32_t)(t >> (8 * prog->q0)) & 0xFFu;
+    for (uint32_t f = 0; f < prog->nf; ++f) atomicAdd(&sacc[f * 6 + prog->lab[f][q]], 1u);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x)
@@ -290,47 +397,52 @@ __global__ void __launch_bounds__(256) hot_finish_kernel(HotParams hp, int n_chu
     return e_;                           \
   } while (0)
 
+int hot_slots(int mapk) { return mapk == 0 ? HotMap<0>::kSlots : HotMap<1>::kSlots; }
+int hot_map_bytes(int mapk) { return mapk == 0 ? 1 : 8; }
+
 cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L) {
   if (L.before) L.before(L.ctx, kKHot);
-  hot_sample_kernel<<<kHotSamples / 256, 256, 0, L.stream>>>(hp);
+  hot_sample_kernel<<<(hp.n_samples + kSampleBlock - 1) / kSampleBlock, 256, 0, L.stream>>>(hp);
   hot_count_hist_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp);
-  hot_select_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp);
+  hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 0);
+  hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 1);
   cudaError_t e = cudaGetLastError();
   if (L.after) L.after(L.ctx, kKHot);
   return e;
 }
 
-template <int NQB>
-static cudaError_t count_hot_t(const PartPlan &p, const HotParams &hp, const Launcher &L) {
-  const size_t sm = sizeof(HotSmem<NQB>);
-  cudaFuncSetAttribute(part_count_hot_kernel<NQB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+template <int MAPK>
+static cudaError_t compose_t(const HotParams &hp, const Launcher &L) {
+  const size_t sm = sizeof(HotSmem<MAPK>);
+  cudaFuncSetAttribute(hot_compose_kernel<MAPK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = (hp.n_chunks + kHotCtaWarps - 1) / kHotCtaWarps;
-  LTL4C_LAUNCH(kKPartCount, part_count_hot_kernel<NQB><<<grid, 32 * kHotCtaWarps, sm, L.stream>>>(p, hp));
+  LTL4C_LAUNCH(kKHotCompose, hot_compose_kernel<MAPK><<<grid, 32 * kHotCtaWarps, sm, L.stream>>>(hp));
 }
 
-cudaError_t launch_part_count_hot(const PartPlan &p, const HotParams &hp, int nq, const Launcher &L) {
-  if (nq <= 4) return count_hot_t<4>(p, hp, L);
-  return count_hot_t<8>(p, hp, L);
+cudaError_t launch_hot_compose(const HotParams &hp, const Launcher &L) {
+  cudaError_t e = hp.mapk == 0 ? compose_t<0>(hp, L) : compose_t<1>(hp, L);
+  if (e != cudaSuccess) return e;
+  if (L.before) L.before(L.ctx, kKHot);
+  hot_prefix_kernel<<<1, 1024, 0, L.stream>>>(hp);
+  hot_gather_kernel<<<hp.n_chunks * kGatherParts, 256, 0, L.stream>>>(hp);
+  e = cudaGetLastError();
+  if (L.after) L.after(L.ctx, kKHot);
+  return e;
 }
 
-template <int NQB>
-static cudaError_t finish_t(const HotParams &hp, const Launcher &L) {
-  LTL4C_LAUNCH(kKHot, hot_finish_kernel<NQB><<<kHotKeys / 8, 256, 0, L.stream>>>(hp, hp.n_chunks));
+cudaError_t launch_hot_finish(const HotParams &hp, const Launcher &L) {
+  if (hp.mapk == 0) LTL4C_LAUNCH(kKHot, hot_finish_kernel<0><<<HotMap<0>::kSlots / 32, 1024, 0, L.stream>>>(hp));
+  LTL4C_LAUNCH(kKHot, hot_finish_kernel<1><<<HotMap<1>::kSlots / 32, 1024, 0, L.stream>>>(hp));
 }
 
-cudaError_t launch_hot_finish(const HotParams &hp, int nq, const Launcher &L) {
-  if (nq <= 4) return finish_t<4>(hp, L);
-  return finish_t<8>(hp, L);
-}
-
-int hot_ctas_per_sm(int nq) {
+int hot_ctas_per_sm(int mapk) {
   int n = 1;
-  if (nq <= 4) {
-    cudaFuncSetAttribute(part_count_hot_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HotSmem<4>));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, part_count_hot_kernel<4>, 256, sizeof(HotSmem<4>));
+  if (mapk == 0) {
+    cudaFuncSetAttribute(hot_compose_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HotSmem<0>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, hot_compose_kernel<0>, 32 * kHotCtaWarps, sizeof(HotSmem<0>));
   } else {
-    cudaFuncSetAttribute(part_count_hot_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HotSmem<8>));
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, part_count_hot_kernel<8>, 256, sizeof(HotSmem<8>));
+    cudaFuncSetAttribute(hot_compose_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(HotSmem<1>));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, hot_compose_kernel<1>, 32 * kHotCtaWarps, sizeof(HotSmem<1>));
   }
   return n > 0 ? n : 1;
 }

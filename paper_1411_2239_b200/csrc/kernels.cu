@@ -38,7 +38,7 @@ namespace ltl4c {
 const char *const kKernelNames[kKNumKernels] = {"part_count", "part_scan", "part_scatter", "bucket_bounds",
                                                 "bucket_warp", "bucket_fast",
                                                 "finalize", "rehash", "heavy", "unit_start",
-                                                "bucket_warp_big", "online_leaf", "online_nodes", "hot"};
+                                                "bucket_warp_big", "online_leaf", "online_nodes", "hot", "hot_compose"};
 
 namespace {
 

@@ -40,7 +40,10 @@ struct PartPlan {
   int K, bits, passes;
   int hk;                               // key column hashed for the bucket (0; K-1 in online mode)
   const uint32_t *hcol[2];              // that column in buf_key[0] / buf_key[1]
-  const uint32_t *hot_mask;             // K = 1 offline: hot-event bits (pass 0 drops those events), or null
+  const uint32_t *dense_key;            // K = 1 hot path (hot.cu): pass 0 reads the dense cold stream
+  const uint8_t *dense_let;             //   (dense_key, dense_let) of *dense_n events
+  const unsigned long long *dense_n;    //   instead of the batch
+  const uint32_t *dense_flag;           //   when *dense_flag != 0 (some key is hot); null: never
   uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
@@ -51,29 +54,37 @@ struct PartPlan {
   DevAcc *acc;
 };
 
+__device__ __forceinline__ bool first_dense(const PartPlan &pl) { return pl.dense_flag && *pl.dense_flag; }
+__device__ __forceinline__ unsigned long long first_n(const PartPlan &pl) { return first_dense(pl) ? *pl.dense_n : pl.n; }
+
 // Heavy hitters of single-level properties (hot.cu): the most frequent keys are
-// composed in trace order during the first counting pass and never partitioned.
-constexpr int kHotBuckets = 1024;     // hot table: 1024 buckets of 4 keys (one 16-byte probe)
-constexpr int kHotKeys = 1024;        // at most this many hot keys (dense ids 0 .. kHotKeys-1)
-constexpr int kHotSamples = 65536;    // evenly spaced sample of the batch
-constexpr int kHotCountCap = 1 << 17; // sample-count table slots
-constexpr int kHotMinCount = 3;       // a key with >= 3 of 65536 samples (~5e-5 of the events) is hot
-// hot-table bucket: the LOW bits of the partition hash fmix32(k ^ kBucketSalt) (a
-// partition bucket is its HIGH bits), so the counting kernel hashes a key once
-__device__ __forceinline__ uint32_t hot_bucket_of_hash(uint32_t h) { return h & (kHotBuckets - 1); }
-__device__ __forceinline__ uint32_t hot_bucket(uint32_t k) { return hot_bucket_of_hash(fmix32(k ^ kBucketSalt)); }
+// composed in trace order where they lie; only the other events are partitioned.
+constexpr int kHotSlotsMax = 4096;     // hot-table slots (2-way buckets) for 1-byte maps; 1024 for 8-byte maps
+constexpr int kHotSamplesMax = 1 << 19; // evenly spaced sample of the batch
+constexpr int kHotCountCap = 1 << 20;  // sample-count table slots
+constexpr int kHotMinCount = 4;        // a hot key was sampled at least this often
+constexpr int kHotCtaWarps = 8;
 struct HotParams {
   const uint32_t *k0;                   // the batch's key column (K = 1)
   const uint8_t *let;
   unsigned long long n;
+  uint32_t n_samples;
+  int mapk;                             // 0: 2-bit packed maps (nq <= 4, <= 16 letters); 1: byte maps (nq <= 8)
+  int slots;                            // hot-table slots (hot_slots(mapk))
+  uint32_t let_mask;
   uint32_t *cnt_key, *cnt_val;          // [kHotCountCap] sample counts (key = ABSENT: empty)
-  uint32_t *hot;                        // [kHotBuckets * 4] hot keys (ABSENT: empty)
-  uint16_t *hid;                        // [kHotBuckets * 4] dense id of the key in that slot
-  uint32_t *key_of;                     // [kHotKeys] key of each dense id (ABSENT: unused id)
-  uint32_t *nhot;                       // [0]: dense ids handed out, [1 + c]: keys sampled c times (c < 64)
-  void *partial;                        // [n_chunks][kHotKeys] per-warp-chunk maps (byte form, 4 or 8 B)
-  uint32_t *mask;                       // [n / 32 + 1]: bit j % 32 of word j / 32 = event j is hot
-  int n_chunks;                         // warps of part_count_hot (contiguous tile ranges each)
+  uint32_t *slot_key;                   // [slots] hot key of each slot (ABSENT: empty) = dense id
+  uint32_t *nhot;                       // [0]: hot keys, [8 + c]: keys sampled c times (c < 64)
+  void *partial;                        // [n_chunks][slots] per-warp-chunk maps
+  uint32_t *cold_key;                   // scratch [n]: chunk c's cold events at its own range
+  uint8_t *cold_let;
+  uint32_t *dense_key;                  // [n] the cold events in trace order
+  uint8_t *dense_let;
+  uint32_t *chunk_cold;                 // [n_chunks] cold events per chunk
+  uint32_t *chunk_pre;                  // [n_chunks] their exclusive prefix (dense offset)
+  unsigned long long *n_cold;           // total cold events (zeroed)
+  unsigned long long chunk_ev;          // events per chunk (multiple of 512)
+  int n_chunks;                         // warps of hot_compose
   const DevProg *prog;
   DevAcc *acc;
 };
@@ -182,6 +193,7 @@ enum KernelId {
   kKOnlineLeaf,
   kKOnlineNodes,
   kKHot,
+  kKHotCompose,
   kKNumKernels
 };
 extern const char *const kKernelNames[kKNumKernels];
@@ -205,8 +217,10 @@ cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_leve
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);
 cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L);
-cudaError_t launch_part_count_hot(const PartPlan &p, const HotParams &hp, int nq, const Launcher &L);
-cudaError_t launch_hot_finish(const HotParams &hp, int nq, const Launcher &L);
-int hot_ctas_per_sm(int nq);  // resident CTAs of part_count_hot
+cudaError_t launch_hot_compose(const HotParams &hp, const Launcher &L);  // + gather of the cold stream
+cudaError_t launch_hot_finish(const HotParams &hp, const Launcher &L);
+int hot_ctas_per_sm(int mapk);  // resident hot_compose CTAs
+int hot_slots(int mapk);
+int hot_map_bytes(int mapk);
 
 }  // namespace ltl4c

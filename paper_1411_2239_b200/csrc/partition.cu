@@ -36,10 +36,11 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
   for (int i = tid; i < kMaxDigits; i += kPartThreads) h[i] = 0;
   if (tid == 0) nv = 0;
   __syncthreads();
+  const bool dense = kFirst && first_dense(pl);
   const uint32_t *const *in_key = kFirst ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
-  const unsigned long long n = kFirst ? pl.n : *pl.nvalid;
+  const unsigned long long n = kFirst ? first_n(pl) : *pl.nvalid;
   const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv;
-  if (!kFirst && base >= n) return;  // a tile past the bound events (part_scan stops before it)
+  if (base >= n) return;  // a tile past the events of this pass (part_scan stops before it)
   const uint32_t dmask = (1u << pl.width[pass]) - 1u;
   const int lo = pl.lo[pass];
   uint32_t k0[kRounds];  // the hash key (column 0, or K-1 if kDeep; pass 0 also checks every guard key)
@@ -56,7 +57,7 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
       for (int i = 1; i < K; ++i) ok[r] &= kv[i] != kAbsent;
       k0[r] = kv[0] == kAbsent ? kAbsent : kv[K - 1];  // (kv[0] absent: unbound, never counted)
     } else if (kFirst) {
-      k0[r] = ok[r] ? in_key[0][j] : 0u;
+      k0[r] = ok[r] ? (dense ? pl.dense_key[j] : in_key[0][j]) : 0u;
 #pragma unroll
       for (int i = 1; i < K; ++i) ok[r] &= !(ok[r] && in_key[i][j] == kAbsent);
     } else {
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(kScanThreads) part_scan_kernel(PartPlan pl, in
   uint32_t *row = pl.counts + (size_t)blockIdx.x * pl.n_tiles;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // tiles holding events of this pass (later passes read only the bound events)
-  const uint32_t nt = pass == 0 ? pl.n_tiles : (uint32_t)((*pl.nvalid + kTileEv - 1) / kTileEv);
+  const uint32_t nt = (uint32_t)(((pass == 0 ? first_n(pl) : *pl.nvalid) + kTileEv - 1) / kTileEv);
   uint32_t carry = 0;
   for (uint32_t off = 0; off < nt; off += kScanThreads * kScanPer) {
     const uint32_t per = min((uint32_t)kScanPer, (nt - off + kScanThreads - 1) / kScanThreads);
@@ -176,15 +177,16 @@ __device__ __forceinline__ uint32_t block_scan_512(uint32_t x, uint32_t *wt) {
 // kFirst: pass 0 (events may lack guard keys: the epsilon filter); kFull: a
 // tile without a ragged end (no range checks).  A later pass's input holds only
 // bound events, so a full tile of a later pass needs no validity test at all.
-template <int K, bool kDeep, bool kFirst, bool kFull, bool kHot = false>
+template <int K, bool kDeep, bool kFirst, bool kFull>
 __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, SweepSmem<K> &s, const uint32_t tile) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr bool first = kFirst;
+  const bool dense = first && first_dense(pl);  // K = 1 hot path: the dense cold stream
   const uint32_t *const *in_key = first ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
-  const uint8_t *in_let = first ? pl.in_let : pl.buf_let[(pass - 1) & 1];
+  const uint8_t *in_let = first ? (dense ? pl.dense_let : pl.in_let) : pl.buf_let[(pass - 1) & 1];
   uint32_t *const *out_key = pl.buf_key[pass & 1];
   uint8_t *out_let = pl.buf_let[pass & 1];
-  const unsigned long long n = first ? pl.n : *pl.nvalid;
+  const unsigned long long n = first ? first_n(pl) : *pl.nvalid;
   if ((unsigned long long)tile * kTileEv >= n) return;  // (uniform per CTA) no events in this tile
   const int width = pl.width[pass];
   const uint32_t dmask = (1u << width) - 1u;
@@ -193,14 +195,12 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
   // loads first (memory-level parallelism)
   uint32_t rk[kRounds][K];
   uint8_t rl[kRounds];
-  uint32_t hotw = 0;  // kHot: lane r holds the hot bits of round r (hot.cu)
-  if (kHot && lane < kRounds && (kFull || wbase + 32 * lane < n)) hotw = pl.hot_mask[(wbase >> 5) + lane];
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const unsigned long long j = wbase + r * 32 + lane;
     const bool in = kFull || j < n;
 #pragma unroll
-    for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(&in_key[k][j]) : kAbsent;
+    for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(k == 0 && dense ? &pl.dense_key[j] : &in_key[k][j]) : kAbsent;
     rl[r] = in ? (uint8_t)(__ldcs(&in_let[j]) & (kFirst ? pl.let_mask : 0xFFu)) : (uint8_t)0;
   }
   // digits 2t, 2t+1 belong to thread t < kMaxDigits / 2: global run start =
@@ -228,39 +228,7 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
 #pragma unroll
       for (int k = 0; k < (kFirst ? K : 1); ++k) valid &= rk[r][k] != kAbsent;
     }
-    if (kHot) valid &= !((__shfl_sync(0xffffffffu, hotw, r) >> lane) & 1u);
     vd[r] = valid;
-  }
-  int nr = kRounds;  // rounds holding events (kHot: after compaction)
-  if (kHot) {
-    // most events of the tile are hot and dropped: compact the rest of the warp's
-    // range in trace order (staged in the warp's slice of kout / lout, free until
-    // the local scatter) so that only ceil(kept / 32) rounds are ranked
-    uint32_t *sk = &s.kout[0][wid * (kTileEv / kPWarps)];
-    uint8_t *sl = &s.lout[wid * (kTileEv / kPWarps)];
-    uint32_t cnt = 0;
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
-      if (vd[r]) {
-        const uint32_t at = cnt + __popc(vm & lanemask_lt());
-        sk[at] = rk[r][0];
-        sl[at] = rl[r];
-      }
-      cnt += __popc(vm);
-    }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < kRounds; ++r) {
-      const uint32_t e = r * 32 + lane;
-      vd[r] = e < cnt;
-      if (vd[r]) {
-        rk[r][0] = sk[e];
-        rl[r] = sl[e];
-      }
-    }
-    __syncwarp();
-    nr = (int)((cnt + 31) >> 5);
   }
 #pragma unroll
   for (int r = 0; r < kRounds; ++r)
@@ -268,7 +236,6 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
   if (pl.rank_ballot) {
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-      if (kHot && r >= nr) { pm[r] = 0; continue; }  // (warp-uniform)
       uint32_t m = __ballot_sync(0xffffffffu, vd[r]);
 #pragma unroll
       for (int b = 0; b < kMaxDigitBits; ++b) {
@@ -283,7 +250,6 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
   } else {
 #pragma unroll
     for (int r = 0; r < kRounds; ++r) {
-      if (kHot && r >= nr) { pm[r] = 0; continue; }
       const uint32_t vm = __ballot_sync(0xffffffffu, vd[r]);
       pm[r] = vd[r] ? __match_any_sync(vm, dg[r]) : 0u;
     }
@@ -354,17 +320,9 @@ template <int K, bool kDeep, bool kFirst>
 __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
-  const unsigned long long n = kFirst ? pl.n : *pl.nvalid;
+  const unsigned long long n = kFirst ? first_n(pl) : *pl.nvalid;
   if ((unsigned long long)(blockIdx.x + 1) * kTileEv <= n) scatter_tile<K, kDeep, kFirst, true>(pl, pass, s, blockIdx.x);
   else scatter_tile<K, kDeep, kFirst, false>(pl, pass, s, blockIdx.x);
-}
-
-// pass 0 of a K = 1 batch with hot keys: events whose bit is set in hot_mask drop out
-__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_hot_kernel(PartPlan pl) {
-  extern __shared__ __align__(16) uint8_t raw[];
-  SweepSmem<1> &s = *reinterpret_cast<SweepSmem<1> *>(raw);
-  if ((unsigned long long)(blockIdx.x + 1) * kTileEv <= pl.n) scatter_tile<1, false, true, true, true>(pl, 0, s, blockIdx.x);
-  else scatter_tile<1, false, true, false, true>(pl, 0, s, blockIdx.x);
 }
 
 // off[c] = first position of bucket c in the final order, off[NB] = n.  Each
@@ -446,11 +404,6 @@ static cudaError_t scatter(const PartPlan &p, int pass, const Launcher &L) {
 }
 
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) {
-  if (pass == 0 && p.hot_mask && p.K == 1) {
-    const size_t sm = sizeof(SweepSmem<1>);
-    cudaFuncSetAttribute(part_scatter_hot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    LTL4C_LAUNCH(kKPartScatter, part_scatter_hot_kernel<<<p.n_tiles, kPartThreads, sm, L.stream>>>(p));
-  }
   const bool deep = p.hk != 0;
   switch (p.K) {
     case 1: return scatter<1, false>(p, pass, L);

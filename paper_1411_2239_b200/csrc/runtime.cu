@@ -199,8 +199,11 @@ struct ltl4c_state {
   int vshards = 1;                 // LTL4C_VIRTUAL_SHARDS: test-only owner shards on one GPU (run_virtual)
   int rank_ballot = 1;             // LTL4C_RANK_BALLOT: stable rank by ballots (1) or match.any (0)
   bool hot = true;                 // LTL4C_NO_HOT: no heavy-hitter path for K = 1 (hot.cu)
-  DevBuf<uint32_t> hot_cnt, hot_tab, hot_partial, hot_mask;  // sample counts [2][cap], table [slots + 1], chunk maps, event bits
-  int hot_per_sm = 2;              // resident part_count_hot CTAs per SM
+  DevBuf<uint32_t> hot_cnt, hot_tab, hot_partial;  // sample counts [2][cap], slot keys + nhot, chunk maps
+  DevBuf<uint32_t> hot_chunk;      // cold events per chunk
+  DevBuf<unsigned long long> hot_n;  // cold events in the batch
+  int hot_per_sm = 2;              // resident hot_compose CTAs per SM
+  int hot_mapk = -1;               // map kind of the program (hot.cu), -1: no hot path
   DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
   DevBuf<uint32_t> exkey[kMaxLevels];
   DevBuf<uint8_t> exlet;
@@ -425,11 +428,12 @@ struct Plan {
 
 // K = 1 offline batches take the heavy-hitter path (hot.cu) for monitors of <= 8 states
 bool use_hot(const ltl4c_state *st) {
-  return st->hot && st->prog->n_levels == 1 && !(st->flags & LTL4C_STATE_ONLINE) && st->prog->n_states <= 8;
+  return st->hot && st->hot_mapk >= 0 && st->prog->n_levels == 1 && !(st->flags & LTL4C_STATE_ONLINE);
 }
-uint32_t hot_chunks(const ltl4c_state *st, uint32_t n_tiles) {  // one per warp of part_count_hot
-  const uint32_t g = (uint32_t)(st->hot_per_sm * st->n_sms * 8);
-  return n_tiles < g ? n_tiles : g;
+// hot_compose chunks: one per warp of the resident grid, multiples of 512 events
+uint64_t hot_chunk_ev(const ltl4c_state *st, uint64_t N) {
+  const uint64_t g = (uint64_t)st->hot_per_sm * st->n_sms * kHotCtaWarps;
+  return std::max<uint64_t>(512, ((N + g - 1) / g + 511) / 512 * 512);
 }
 
 // Buffer sizes for a batch of N events (all allocation happens here, outside
@@ -460,10 +464,12 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
   if (use_hot(st)) {
+    const uint64_t nch = (N + hot_chunk_ev(st, N) - 1) / hot_chunk_ev(st, N);
     CU(st->hot_cnt.ensure(2 * (size_t)kHotCountCap));
-    CU(st->hot_tab.ensure(4 * kHotBuckets + 2 * kHotBuckets + kHotKeys + 72));  // keys, ids (u16), key_of, nhot + count bins
-    CU(st->hot_partial.ensure((size_t)hot_chunks(st, pl->n_tiles) * kHotKeys * 2));  // 8-byte maps
-    CU(st->hot_mask.ensure(N / 32 + 2));
+    CU(st->hot_tab.ensure(hot_slots(st->hot_mapk) + 72));  // slot keys, nhot + count bins
+    CU(st->hot_partial.ensure((nch * hot_slots(st->hot_mapk) * hot_map_bytes(st->hot_mapk) + 3) / 4));
+    CU(st->hot_chunk.ensure(2 * nch));
+    CU(st->hot_n.ensure(1));
   }
   return LTL4C_OK;
 }
@@ -546,36 +552,50 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     HotParams hp{};
     const bool hot = use_hot(st);
     if (hot) {
-      // heavy hitters: sampled, then composed during the first counting pass
+      // heavy hitters: sampled, composed where they lie; the rest, gathered into a
+      // dense stream (bufkey[1] / buflet[1], free until pass 1), is partitioned
+      const int S = hot_slots(st->hot_mapk);
       hp.k0 = keys[0];
       hp.let = letters;
       hp.n = plan.N;
+      hp.n_samples = (uint32_t)std::min<uint64_t>(plan.N, kHotSamplesMax);
+      hp.mapk = st->hot_mapk;
+      hp.slots = S;
+      hp.let_mask = pl.let_mask;
       hp.cnt_key = st->hot_cnt.p;
       hp.cnt_val = st->hot_cnt.p + kHotCountCap;
-      hp.hot = st->hot_tab.p;
-      hp.hid = reinterpret_cast<uint16_t *>(st->hot_tab.p + 4 * kHotBuckets);
-      hp.key_of = st->hot_tab.p + 6 * kHotBuckets;
-      hp.nhot = hp.key_of + kHotKeys;
+      hp.slot_key = st->hot_tab.p;
+      hp.nhot = st->hot_tab.p + S;
       hp.partial = st->hot_partial.p;
-      hp.mask = st->hot_mask.p;
-      hp.n_chunks = (int)hot_chunks(st, plan.n_tiles);
+      hp.cold_key = st->bufkey[0][0].p;
+      hp.cold_let = st->buflet[0].p;
+      hp.dense_key = st->bufkey[1][0].p;
+      hp.dense_let = st->buflet[1].p;
+      hp.chunk_cold = st->hot_chunk.p;
+      hp.chunk_pre = st->hot_chunk.p + (st->hot_chunk.n / 2);
+      hp.n_cold = st->hot_n.p;
+      hp.chunk_ev = hot_chunk_ev(st, plan.N);
+      hp.n_chunks = (int)((plan.N + hp.chunk_ev - 1) / hp.chunk_ev);
       hp.prog = st->d_prog.p;
       hp.acc = st->d_acc.p;
       CU(cudaMemsetAsync(hp.cnt_key, 0xFF, sizeof(uint32_t) * kHotCountCap, s));
       CU(cudaMemsetAsync(hp.cnt_val, 0, sizeof(uint32_t) * kHotCountCap, s));
-      CU(cudaMemsetAsync(hp.hot, 0xFF, sizeof(uint32_t) * 4 * kHotBuckets, s));
-      CU(cudaMemsetAsync(hp.key_of, 0xFF, sizeof(uint32_t) * kHotKeys, s));
+      CU(cudaMemsetAsync(hp.slot_key, 0xFF, sizeof(uint32_t) * S, s));
       CU(cudaMemsetAsync(hp.nhot, 0, sizeof(uint32_t) * 72, s));
+      CU(cudaMemsetAsync(hp.n_cold, 0, sizeof(unsigned long long), s));
       CU(launch_hot_select(hp, L));
-      pl.hot_mask = hp.mask;
+      CU(launch_hot_compose(hp, L));
+      pl.dense_key = hp.dense_key;
+      pl.dense_let = hp.dense_let;
+      pl.dense_n = hp.n_cold;
+      pl.dense_flag = hp.nhot;
     }
     for (int pass = 0; pass < plan.P; ++pass) {
-      if (pass == 0 && hot) CU(launch_part_count_hot(pl, hp, (int)prog->n_states, L));
-      else CU(launch_part_count(pl, pass, L));
+      CU(launch_part_count(pl, pass, L));
       CU(launch_part_scan(pl, pass, L));
       CU(launch_part_scatter(pl, pass, L));
     }
-    if (hot) CU(launch_hot_finish(hp, (int)prog->n_states, L));
+    if (hot) CU(launch_hot_finish(hp, L));
     CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
@@ -906,7 +926,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
                           (const void *)st->d_acc.p, (const void *)st->d_out.p, (const void *)st->d_nvalid.p,
                           (const void *)st->d_prog.p, (const void *)st->h_out, (const void *)st->hot_cnt.p,
                           (const void *)st->hot_tab.p, (const void *)st->hot_partial.p,
-                          (const void *)st->hot_mask.p})
+                          (const void *)st->hot_chunk.p, (const void *)st->hot_n.p})
       key.push_back((uintptr_t)b);
     if (st->graph_key != key || !st->graph_exec) {
       drop_graph(st);
@@ -1113,7 +1133,10 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
       e = online_leaf_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states, (int)prog->n_atoms,
                              st->online_cfg);
     if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
-    if (prog->n_levels == 1 && prog->n_states <= 8) st->hot_per_sm = hot_ctas_per_sm((int)prog->n_states);
+    if (prog->n_levels == 1) {
+      st->hot_mapk = prog->n_states <= 4 && prog->n_atoms <= 4 ? 0 : prog->n_states <= 8 ? 1 : -1;
+      if (st->hot_mapk >= 0) st->hot_per_sm = hot_ctas_per_sm(st->hot_mapk);
+    }
   }
   cudaSetDevice(prev);
   *out = st;
@@ -1286,7 +1309,8 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->hot_cnt.release();
   st->hot_tab.release();
   st->hot_partial.release();
-  st->hot_mask.release();
+  st->hot_chunk.release();
+  st->hot_n.release();
   for (auto &t : st->pending) {
     cudaEventDestroy(t.a);
     cudaEventDestroy(t.b);
