@@ -9,9 +9,9 @@
 // composed where they lie, and only the rest of the trace is partitioned:
 //
 //   hot_sample    S evenly spaced events -> sample counts per key (L2 table)
-//   hot_insert    the most sampled keys take a slot of the hot table: 2-way
-//                 buckets indexed by the LOW bits of the partition hash (a key
-//                 whose bucket is full stays cold: hotness only moves work);
+//   hot_insert    the most sampled keys take a slot of the hot table: one of
+//                 two 2-way buckets picked by bits of the partition hash (a key
+//                 whose buckets are full stays cold: hotness only moves work);
 //                 the slot index is the key's dense id
 //   hot_compose   warp per contiguous chunk of the trace, 32 events per round in
 //                 trace order: a hot event's letter is applied to the warp's
@@ -54,6 +54,14 @@ __device__ __forceinline__ unsigned long long byte_apply(unsigned long long g, u
   const uint32_t lo = __byte_perm(glo, ghi, sel_of((uint32_t)f));
   const uint32_t hi = __byte_perm(glo, ghi, sel_of((uint32_t)(f >> 32)));
   return (unsigned long long)hi << 32 | lo;
+}
+
+// a key's two candidate 2-way buckets of the hot table (two choices keep the
+// table nearly collision-free at load 3/4): the LOW bits of the partition hash
+// (a partition bucket is its HIGH bits) and bits 12.. of it
+__device__ __forceinline__ uint32_t hot_bucket1(uint32_t h, int slots) { return (h & (uint32_t)(slots / 2 - 1)) * 2; }
+__device__ __forceinline__ uint32_t hot_bucket2(uint32_t h, int slots) {
+  return ((h >> 12) & (uint32_t)(slots / 2 - 1)) * 2;
 }
 
 template <int MAPK> struct HotMap;
@@ -137,9 +145,10 @@ __global__ void hot_insert_kernel(HotParams hp, int pass) {
   const uint32_t c = hp.cnt_val[s];
   if (pass == 0 ? c < 4 * thr : (c < thr || c >= 4 * thr)) return;
   const uint32_t k = hp.cnt_key[s];
-  const uint32_t b = (fmix32(k ^ kBucketSalt) & (uint32_t)(hp.slots / 2 - 1)) * 2;
-  for (int i = 0; i < 2; ++i)
-    if (atomicCAS(&hp.slot_key[b + i], kAbsent, k) == kAbsent) {
+  const uint32_t h = fmix32(k ^ kBucketSalt);
+  const uint32_t b1 = hot_bucket1(h, hp.slots), b2 = hot_bucket2(h, hp.slots);
+  for (int i = 0; i < 4; ++i)
+    if (atomicCAS(&hp.slot_key[(i < 2 ? b1 : b2) + (i & 1)], kAbsent, k) == kAbsent) {
       atomicAdd(hp.nhot, 1u);
       return;
     }
@@ -214,9 +223,16 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, 4) hot_compose_kernel(HotPa
       for (int r = 0; r < kHotBatch; ++r) {
         const uint32_t k = kk[r];
         const bool valid = k != kAbsent;
-        const uint32_t b = (fmix32(k ^ kBucketSalt) & (uint32_t)(S / 2 - 1)) * 2;
-        const uint2 t = *reinterpret_cast<const uint2 *>(&s.key[b]);
-        const int slot = !valid ? -1 : t.x == k ? (int)b : t.y == k ? (int)b + 1 : -1;
+        const uint32_t h = fmix32(k ^ kBucketSalt);
+        const uint32_t b1 = hot_bucket1(h, S), b2 = hot_bucket2(h, S);
+        const uint2 t1 = *reinterpret_cast<const uint2 *>(&s.key[b1]);
+        const uint2 t2 = *reinterpret_cast<const uint2 *>(&s.key[b2]);
+        const int slot = !valid       ? -1
+                         : t1.x == k ? (int)b1
+                         : t1.y == k ? (int)b1 + 1
+                         : t2.x == k ? (int)b2
+                         : t2.y == k ? (int)b2 + 1
+                                     : -1;
         const bool cold = valid && slot < 0;
         const uint32_t cm = __ballot_sync(0xffffffffu, cold);
         if (cold) {

@@ -38,6 +38,7 @@ struct PartPlan {
   unsigned long long n;                 // events in the batch
   uint32_t n_tiles;                     // ceil(n / kTileEv)
   int K, bits, passes;
+  int n_sms;                            // persistent grids: resident CTAs = n_sms x per-SM occupancy
   int hk;                               // key column hashed for the bucket (0; K-1 in online mode)
   const uint32_t *hcol[2];              // that column in buf_key[0] / buf_key[1]
   const uint32_t *dense_key;            // K = 1 hot path (hot.cu): pass 0 reads the dense cold stream
@@ -216,6 +217,9 @@ cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {wa
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);
+// K = 1 offline units: segmented map scans through warp tables (seg.cu)
+cudaError_t launch_bucket_seg(const BucketParams &p, int nq, int nf, uint32_t grid, const Launcher &L);
+int bucket_seg_ctas_per_sm(int nq);
 cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L);
 cudaError_t launch_hot_compose(const HotParams &hp, const Launcher &L);  // + gather of the cold stream
 cudaError_t launch_hot_finish(const HotParams &hp, const Launcher &L);

@@ -28,6 +28,7 @@ constexpr int kRounds = kTileEv / kPartThreads;  // rounds of 32 events per warp
 
 // Digit counts of one tile (counts[d][tile]).  Pass 0 reads the batch and
 // applies the epsilon filter; later passes read k0 of the previous pass.
+// (persistent: CTA b takes tiles b, b + grid, ... below the events of this pass)
 template <int K, bool kFirst, bool kDeep>
 __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, int pass) {
   __shared__ uint32_t h[kMaxDigits];
@@ -39,44 +40,49 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
   const bool dense = kFirst && first_dense(pl);
   const uint32_t *const *in_key = kFirst ? pl.in_key : (const uint32_t *const *)pl.buf_key[(pass - 1) & 1];
   const unsigned long long n = kFirst ? first_n(pl) : *pl.nvalid;
-  const unsigned long long base = (unsigned long long)blockIdx.x * kTileEv;
-  if (base >= n) return;  // a tile past the events of this pass (part_scan stops before it)
-  const uint32_t dmask = (1u << pl.width[pass]) - 1u;
-  const int lo = pl.lo[pass];
-  uint32_t k0[kRounds];  // the hash key (column 0, or K-1 if kDeep; pass 0 also checks every guard key)
-  bool ok[kRounds];
+  for (uint32_t tile = blockIdx.x; (unsigned long long)tile * kTileEv < n; tile += gridDim.x) {
+    const unsigned long long base = (unsigned long long)tile * kTileEv;
+    const uint32_t dmask = (1u << pl.width[pass]) - 1u;
+    const int lo = pl.lo[pass];
+    uint32_t k0[kRounds];  // the hash key (column 0, or K-1 if kDeep; pass 0 also checks every guard key)
+    bool ok[kRounds];
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r) {  // all loads first (memory-level parallelism)
-    const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
-    ok[r] = j < n;
-    if (kFirst && kDeep) {
-      uint32_t kv[K];
+    for (int r = 0; r < kRounds; ++r) {  // all loads first (memory-level parallelism)
+      const unsigned long long j = base + (unsigned long long)r * kPartThreads + tid;
+      ok[r] = j < n;
+      if (kFirst && kDeep) {
+        uint32_t kv[K];
 #pragma unroll
-      for (int i = 0; i < K; ++i) kv[i] = ok[r] ? in_key[i][j] : 0u;
+        for (int i = 0; i < K; ++i) kv[i] = ok[r] ? in_key[i][j] : 0u;
 #pragma unroll
-      for (int i = 1; i < K; ++i) ok[r] &= kv[i] != kAbsent;
-      k0[r] = kv[0] == kAbsent ? kAbsent : kv[K - 1];  // (kv[0] absent: unbound, never counted)
-    } else if (kFirst) {
-      k0[r] = ok[r] ? (dense ? pl.dense_key[j] : in_key[0][j]) : 0u;
+        for (int i = 1; i < K; ++i) ok[r] &= kv[i] != kAbsent;
+        k0[r] = kv[0] == kAbsent ? kAbsent : kv[K - 1];  // (kv[0] absent: unbound, never counted)
+      } else if (kFirst) {
+        k0[r] = ok[r] ? (dense ? pl.dense_key[j] : in_key[0][j]) : 0u;
 #pragma unroll
-      for (int i = 1; i < K; ++i) ok[r] &= !(ok[r] && in_key[i][j] == kAbsent);
-    } else {
-      k0[r] = ok[r] ? pl.hcol[(pass - 1) & 1][j] : 0u;
+        for (int i = 1; i < K; ++i) ok[r] &= !(ok[r] && in_key[i][j] == kAbsent);
+      } else {
+        k0[r] = ok[r] ? pl.hcol[(pass - 1) & 1][j] : 0u;
+      }
     }
-  }
-  uint32_t myvalid = 0;
+    uint32_t myvalid = 0;
 #pragma unroll
-  for (int r = 0; r < kRounds; ++r) {
-    const bool v = ok[r] && (!kFirst || k0[r] != kAbsent);
-    if (v) atomicAdd(&h[(salted_bucket(k0[r], pl.bits, pl.salt) >> lo) & dmask], 1u);
-    myvalid += v;
+    for (int r = 0; r < kRounds; ++r) {
+      const bool v = ok[r] && (!kFirst || k0[r] != kAbsent);
+      if (v) atomicAdd(&h[(salted_bucket(k0[r], pl.bits, pl.salt) >> lo) & dmask], 1u);
+      myvalid += v;
+    }
+    if (kFirst) {
+      for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
+      if (lane == 0 && myvalid) atomicAdd(&nv, myvalid);
+    }
+    __syncthreads();
+    for (int d = tid; d < (1 << pl.width[pass]); d += kPartThreads) {
+      pl.counts[(size_t)d * pl.n_tiles + tile] = h[d];
+      h[d] = 0;
+    }
+    __syncthreads();
   }
-  if (kFirst) {
-    for (int d = 16; d; d >>= 1) myvalid += __shfl_down_sync(0xffffffffu, myvalid, d);
-    if (lane == 0 && myvalid) atomicAdd(&nv, myvalid);
-  }
-  __syncthreads();
-  for (int d = tid; d < (1 << pl.width[pass]); d += kPartThreads) pl.counts[(size_t)d * pl.n_tiles + blockIdx.x] = h[d];
   if (kFirst && tid == 0 && nv) {
     atomicAdd(pl.nvalid, (unsigned long long)nv);
     atomicAdd(&pl.acc->events_bound, (unsigned long long)nv);
@@ -321,6 +327,7 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
   const unsigned long long n = kFirst ? first_n(pl) : *pl.nvalid;
+  // (one CTA per tile: measured faster than a persistent tile loop, C2 0.476 vs 0.533 ms)
   if ((unsigned long long)(blockIdx.x + 1) * kTileEv <= n) scatter_tile<K, kDeep, kFirst, true>(pl, pass, s, blockIdx.x);
   else scatter_tile<K, kDeep, kFirst, false>(pl, pass, s, blockIdx.x);
 }
@@ -371,9 +378,14 @@ __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long lon
     return e_;                           \
   } while (0)
 
+static unsigned part_grid(const PartPlan &p, int per_sm) {
+  const unsigned g = (unsigned)(p.n_sms > 0 ? p.n_sms * per_sm : 148 * per_sm);
+  return p.n_tiles < g ? (p.n_tiles ? p.n_tiles : 1) : g;
+}
+
 template <int K, bool kDeep>
 static cudaError_t count_first(const PartPlan &p, int pass, const Launcher &L) {
-  LTL4C_LAUNCH(kKPartCount, part_count_kernel<K, true, kDeep><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<K, true, kDeep><<<part_grid(p, 4), kPartThreads, 0, L.stream>>>(p, pass));
 }
 
 cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
@@ -385,7 +397,7 @@ cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
       default: return deep ? count_first<3, true>(p, pass, L) : count_first<3, false>(p, pass, L);
     }
   }
-  LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false, false><<<p.n_tiles, kPartThreads, 0, L.stream>>>(p, pass));
+  LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false, false><<<part_grid(p, 4), kPartThreads, 0, L.stream>>>(p, pass));
 }
 
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {

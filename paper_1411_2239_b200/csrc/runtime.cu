@@ -204,6 +204,8 @@ struct ltl4c_state {
   DevBuf<unsigned long long> hot_n;  // cold events in the batch
   int hot_per_sm = 2;              // resident hot_compose CTAs per SM
   int hot_mapk = -1;               // map kind of the program (hot.cu), -1: no hot path
+  bool seg = true;                 // LTL4C_NO_SEG: K = 1 units through bucket_warp instead of bucket_seg
+  int seg_per_sm = 4;              // resident bucket_seg CTAs per SM
   DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
   DevBuf<uint32_t> exkey[kMaxLevels];
   DevBuf<uint8_t> exlet;
@@ -529,6 +531,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.buf_let[1] = st->buflet[1].p;
     pl.n = plan.N;
     pl.n_tiles = plan.n_tiles;
+    pl.n_sms = st->n_sms;
     pl.K = K;
     pl.bits = plan.B;
     pl.salt = kBucketSalt;
@@ -603,19 +606,32 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       // kernel with kWarpCapBig, above that to the CTA kernel, and above kCap to
       // the heavy path (after the first result copy)
       CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
-      CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[1]), L));
-      BucketParams mp = bp;
-      mp.list = st->medium_list.p;
-      mp.list_len = &st->d_acc.p->medium_buckets;
-      mp.spill_list = st->large_list.p;
-      mp.spill_len = &st->d_acc.p->large_buckets;
-      mp.bucket_counter = bp.bucket_counter + 1;
-      mp.warps_per_cta = st->warp_cfg[2];
-      CU(launch_bucket_warp(mp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[3]), L));
-      BucketParams fp = bp;
-      fp.list = st->large_list.p;
-      fp.list_len = &st->d_acc.p->large_buckets;
-      CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, st->n_sms, L));
+      if (K == 1 && st->seg) {
+        // one level: units streamed through warp tables by segmented map scans (seg.cu);
+        // units with too many distinct keys go to the CTA kernel
+        BucketParams sp = bp;
+        sp.spill_list = st->large_list.p;
+        sp.spill_len = &st->d_acc.p->large_buckets;
+        CU(launch_bucket_seg(sp, (int)prog->n_states, (int)prog->n_formulas, warp_grid(st, st->seg_per_sm), L));
+        BucketParams fp = bp;
+        fp.list = st->large_list.p;
+        fp.list_len = &st->d_acc.p->large_buckets;
+        CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, st->n_sms, L));
+      } else {
+        CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[1]), L));
+        BucketParams mp = bp;
+        mp.list = st->medium_list.p;
+        mp.list_len = &st->d_acc.p->medium_buckets;
+        mp.spill_list = st->large_list.p;
+        mp.spill_len = &st->d_acc.p->large_buckets;
+        mp.bucket_counter = bp.bucket_counter + 1;
+        mp.warps_per_cta = st->warp_cfg[2];
+        CU(launch_bucket_warp(mp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[3]), L));
+        BucketParams fp = bp;
+        fp.list = st->large_list.p;
+        fp.list_len = &st->d_acc.p->large_buckets;
+        CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, st->n_sms, L));
+      }
     } else {
       // carried state: leaves (warp per unit), then touched nodes depth K-1 .. 1
       OnlineParams op{};
@@ -664,6 +680,7 @@ ltl4c_status owner_partition(ltl4c_state *st, const uint32_t *const *keys, const
   pl.buf_let[1] = olet;
   pl.n = N;
   pl.n_tiles = n_tiles;
+  pl.n_sms = st->n_sms;
   pl.K = K;
   pl.bits = bits;
   pl.passes = 1;
@@ -1074,6 +1091,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   if (const char *e = std::getenv("LTL4C_WARP_GRID")) st->warp_grid = (uint32_t)std::max(0, std::atoi(e));
   if (const char *e = std::getenv("LTL4C_RANK_BALLOT")) st->rank_ballot = std::atoi(e);
   st->hot = std::getenv("LTL4C_NO_HOT") == nullptr;
+  st->seg = std::getenv("LTL4C_NO_SEG") == nullptr;
   if (const char *e = std::getenv("LTL4C_VIRTUAL_SHARDS")) {
     const int g = std::atoi(e);
     if (g > 1 && g <= 256 && !(g & (g - 1))) st->vshards = g;
@@ -1136,6 +1154,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
     if (prog->n_levels == 1) {
       st->hot_mapk = prog->n_states <= 4 && prog->n_atoms <= 4 ? 0 : prog->n_states <= 8 ? 1 : -1;
       if (st->hot_mapk >= 0) st->hot_per_sm = hot_ctas_per_sm(st->hot_mapk);
+      st->seg_per_sm = bucket_seg_ctas_per_sm((int)prog->n_states);
     }
   }
   cudaSetDevice(prev);
