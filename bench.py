@@ -44,7 +44,7 @@ import tracegen  # noqa: E402
 
 METRIC = "trace events verified/sec"
 UNIT = "events/s"
-RESULT_BYTES = 928       # sizeof(DevOut) copied device -> host per verify
+RESULT_BYTES = 936       # sizeof(DevOut) copied device -> host per verify
 FLUSH_BYTES = 256 << 20
 
 # name -> (workload text, total events, generator(lo, hi), algorithmic bytes per event)

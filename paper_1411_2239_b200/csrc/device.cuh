@@ -44,6 +44,7 @@ struct DevAcc {
   unsigned long long table_overflow;
   unsigned long long leaves;  // distinct leaves inserted in the carried table
   unsigned long long nodes[kMaxLevels + 1];
+  unsigned long long onepass;  // K = 1 hot batch in one-pass mode (seg.cu: bucket_coarse)
 };
 
 // Result as written by the finalize kernel (mirrors ltl4c_result, per formula).

@@ -821,19 +821,21 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
 
 // ----------------------------------------------- work units for bucket_warp
 // unit u = buckets [unit_start[u], unit_start[u+1]): the buckets whose first event
-// lies in [u * kUnitTarget, (u + 1) * kUnitTarget).  Lane per bucket c: the units
+// lies in [u * target, (u + 1) * target) (target = kUnitTarget; seg_unit for bucket_seg).  Lane per bucket c: the units
 // whose boundary u * kUnitTarget lies in (off[c-1], off[c]] start at c (c = nb,
 // the end: every remaining unit); the warp writes each lane's range together
 // (a skewed bucket can own thousands of unit boundaries).
-__global__ void unit_start_kernel(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units) {
+__global__ void unit_start_kernel(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, uint32_t target,
+                                  const uint32_t *gate, int want) {
+  if (gate && ((*gate != 0) != (want != 0))) return;
   const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
   uint32_t u0 = 1, u1 = 0;  // empty
   if (c <= nb) {
     if (c == 0) { u0 = 0; u1 = 0; }
     else {
-      u0 = off[c - 1] / kUnitTarget + 1;
-      u1 = c == nb ? n_units : min(n_units, off[c] / kUnitTarget);
+      u0 = off[c - 1] / target + 1;
+      u1 = c == nb ? n_units : min(n_units, off[c] / target);
     }
   }
   uint32_t todo = __ballot_sync(0xffffffffu, u0 <= u1);
@@ -1825,6 +1827,7 @@ __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *
     out->table_overflow = acc->table_overflow;
     out->leaves = acc->leaves;
     for (int l = 0; l <= kMaxLevels; ++l) out->nodes[l] = acc->nodes[l];
+    out->onepass = acc->onepass;
   }
 }
 
@@ -1859,8 +1862,10 @@ cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, int n_sms, 
   }
 }
 
-cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L) {
-  LTL4C_LAUNCH(kKUnitStart, unit_start_kernel<<<(nb + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units));
+cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L,
+                              uint32_t target, const uint32_t *gate, int want) {
+  LTL4C_LAUNCH(kKUnitStart,
+               unit_start_kernel<<<(nb + 1 + 255) / 256, 256, 0, L.stream>>>(off, nb, ustart, n_units, target, gate, want));
 }
 
 template <int K, int NF, int CAP>

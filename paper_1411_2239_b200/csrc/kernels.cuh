@@ -45,6 +45,7 @@ struct PartPlan {
   const uint8_t *dense_let;             //   (dense_key, dense_let) of *dense_n events
   const unsigned long long *dense_n;    //   instead of the batch
   const uint32_t *dense_flag;           //   when *dense_flag != 0 (some key is hot); null: never
+  const uint32_t *skip_flag;            // passes >= 1 do nothing when *skip_flag != 0 (one-pass mode), or null
   uint32_t salt;                        // kBucketSalt (buckets) or kOwnerSalt (ranks)
   int lo[kMaxPasses], width[kMaxPasses];
   uint32_t *digit_hist;                 // [kMaxPasses][kMaxDigits] digit totals (bound events)
@@ -57,6 +58,7 @@ struct PartPlan {
 
 __device__ __forceinline__ bool first_dense(const PartPlan &pl) { return pl.dense_flag && *pl.dense_flag; }
 __device__ __forceinline__ unsigned long long first_n(const PartPlan &pl) { return first_dense(pl) ? *pl.dense_n : pl.n; }
+__device__ __forceinline__ bool pass_skipped(const PartPlan &pl, int pass) { return pass > 0 && pl.skip_flag && *pl.skip_flag; }
 
 // Heavy hitters of single-level properties (hot.cu): the most frequent keys are
 // composed in trace order where they lie; only the other events are partitioned.
@@ -151,6 +153,9 @@ struct BucketParams {
   uint32_t *bucket_counter;             // warp path: dynamic unit scheduler
   const uint32_t *unit_start;           // warp path: [n_units + 1] first bucket of each unit
   uint32_t n_units;                     // for the batch's N events (host)
+  uint32_t unit_target;                 // events per unit (unit_start's target)
+  const uint32_t *gate;                 // K = 1 hot batches: the kernel runs iff (*gate != 0) == gate_want
+  int gate_want;
   const unsigned long long *nvalid;     // bound events (device): units past nvalid / kUnitTarget + 1 are empty
   const DevProg *prog;
   DevAcc *acc;
@@ -170,6 +175,7 @@ struct DevOut {
   DevResult res[kMaxFormulas];
   unsigned long long oversize_buckets, oversize_events, table_overflow, leaves;
   unsigned long long nodes[kMaxLevels + 1];
+  unsigned long long onepass;           // the batch took the one-pass mode (oversize buckets are coarse)
 };
 
 struct Launcher {
@@ -202,9 +208,11 @@ extern const char *const kKernelNames[kKNumKernels];
 cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
-cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
+cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L,
+                                 const uint32_t *gate = nullptr, int want = 0, int coarse_bits = 0);
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, int n_sms, const Launcher &L);
-cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L);
+cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L,
+                              uint32_t target = kUnitTarget, const uint32_t *gate = nullptr, int want = 0);
 cudaError_t launch_bucket_warp(const BucketParams &p, int K, int nf, uint32_t grid, const Launcher &L);
 // {warps per CTA, CTAs per SM} of the unit kernel (cfg[0..1]) and of the
 // medium-bucket kernel (cfg[2..3])
@@ -220,6 +228,11 @@ cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out,
 // K = 1 offline units: segmented map scans through warp tables (seg.cu)
 cudaError_t launch_bucket_seg(const BucketParams &p, int nq, int nf, uint32_t grid, const Launcher &L);
 int bucket_seg_ctas_per_sm(int nq);
+// one-pass mode of a K = 1 hot batch (<= 4 states, <= 16 letters): CTA per coarse bucket (seg.cu)
+constexpr int kCoarseBits = 9;
+cudaError_t launch_bucket_coarse(const BucketParams &p, int nf, uint32_t grid, const Launcher &L);
+int bucket_coarse_ctas_per_sm();
+
 cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L);
 cudaError_t launch_hot_compose(const HotParams &hp, const Launcher &L);  // + gather of the cold stream
 cudaError_t launch_hot_finish(const HotParams &hp, const Launcher &L);

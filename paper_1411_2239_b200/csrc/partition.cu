@@ -33,6 +33,7 @@ template <int K, bool kFirst, bool kDeep>
 __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, int pass) {
   __shared__ uint32_t h[kMaxDigits];
   __shared__ uint32_t nv;
+  if (pass_skipped(pl, pass)) return;
   const int tid = threadIdx.x, lane = tid & 31;
   for (int i = tid; i < kMaxDigits; i += kPartThreads) h[i] = 0;
   if (tid == 0) nv = 0;
@@ -96,6 +97,7 @@ constexpr int kScanThreads = 256;
 constexpr int kScanPer = 16;  // rows up to 4096 tiles in one sweep (16.7M events)
 __global__ void __launch_bounds__(kScanThreads) part_scan_kernel(PartPlan pl, int pass) {
   __shared__ uint32_t wt[kScanThreads / 32];
+  if (pass_skipped(pl, pass)) return;
   uint32_t *row = pl.counts + (size_t)blockIdx.x * pl.n_tiles;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   // tiles holding events of this pass (later passes read only the bound events)
@@ -326,6 +328,7 @@ template <int K, bool kDeep, bool kFirst>
 __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
+  if (pass_skipped(pl, pass)) return;
   const unsigned long long n = kFirst ? first_n(pl) : *pl.nvalid;
   // (one CTA per tile: measured faster than a persistent tile loop, C2 0.476 vs 0.533 ms)
   if ((unsigned long long)(blockIdx.x + 1) * kTileEv <= n) scatter_tile<K, kDeep, kFirst, true>(pl, pass, s, blockIdx.x);
@@ -335,15 +338,16 @@ __global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan 
 // off[c] = first position of bucket c in the final order, off[NB] = n.  Each
 // thread covers 16 consecutive positions (four 16-byte loads issued together).
 constexpr int kBoundsPer = 16;
-__global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, int bits,
-                                     uint32_t *off, uint32_t nb) {
+__global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long long *nvalid, uint32_t salt, int shift,
+                                     uint32_t mask, uint32_t *off, uint32_t nb, const uint32_t *gate, int want) {
   // (n < 2^32 - 2^20: 32-bit positions; bucket ids are < 2^27, so b + 1 never wraps)
+  if (gate && ((*gate != 0) != (want != 0))) return;  // (the other mode of a K = 1 hot batch)
   const uint32_t n = (uint32_t)*nvalid;
-  const uint32_t shift = 32 - bits;
+  auto bucket = [&](uint32_t k) { return (fmix32(k ^ salt) >> shift) & mask; };
   for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t <= n / kBoundsPer; t += gridDim.x * blockDim.x) {
     const uint32_t i0 = kBoundsPer * t;
     uint32_t prev = 0;  // bucket of event i0 - 1, plus one (0 before the first event)
-    if (i0 > 0) prev = (bits == 0 ? 0u : fmix32(k0[i0 - 1] ^ kBucketSalt) >> shift) + 1;
+    if (i0 > 0) prev = bucket(k0[i0 - 1]) + 1;
     if (i0 + kBoundsPer <= n) {
       uint32_t kv[kBoundsPer];
 #pragma unroll
@@ -353,13 +357,13 @@ __global__ void bucket_bounds_kernel(const uint32_t *k0, const unsigned long lon
       }
 #pragma unroll
       for (int j = 0; j < kBoundsPer; ++j) {
-        const uint32_t b = bits == 0 ? 0u : fmix32(kv[j] ^ kBucketSalt) >> shift;
+        const uint32_t b = bucket(kv[j]);
         for (uint32_t c = prev; c <= b; ++c) off[c] = i0 + j;  // buckets (previous, b] start here
         prev = max(prev, b + 1);
       }
     } else {  // the ragged end (t = n / 16) also writes the offsets after the last bucket
       for (uint32_t j = 0; i0 + j <= n; ++j) {
-        const uint32_t b = i0 + j < n ? (bits == 0 ? 0u : fmix32(k0[i0 + j] ^ kBucketSalt) >> shift) : nb;
+        const uint32_t b = i0 + j < n ? bucket(k0[i0 + j]) : nb;
         for (uint32_t c = prev; c <= b; ++c) off[c] = i0 + j;
         prev = max(prev, b + 1);
       }
@@ -424,11 +428,22 @@ cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) 
   }
 }
 
-cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
-  const uint32_t *k0 = p.hcol[(p.passes - 1) & 1];
-  const unsigned long long want = (p.n / kBoundsPer + 1 + 255) / 256;
-  const unsigned grid = (unsigned)(want > 148 * 16 ? 148 * 16 : want);
-  LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(k0, p.nvalid, p.bits, off, n_buckets));
+// coarse_bits > 0: the offsets of the first pass's digits (bits [lo[0], lo[0] +
+// width[0]) of the bucket id) in the first pass's output -- the one-pass mode of
+// a K = 1 hot batch (gate = the hot-key count: this launch runs iff (*gate != 0) == want)
+cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L,
+                                 const uint32_t *gate, int want, int coarse_bits) {
+  const uint32_t *k0 = coarse_bits ? p.hcol[0] : p.hcol[(p.passes - 1) & 1];
+  int shift = 0;
+  uint32_t mask = 0;
+  if (p.bits > 0) {
+    shift = 32 - p.bits + (coarse_bits ? p.lo[0] : 0);
+    mask = coarse_bits ? (1u << coarse_bits) - 1u : (p.bits >= 32 ? 0xFFFFFFFFu : (1u << p.bits) - 1u);
+  }
+  const unsigned long long want_t = (p.n / kBoundsPer + 1 + 255) / 256;
+  const unsigned grid = (unsigned)(want_t > 148 * 16 ? 148 * 16 : want_t);
+  LTL4C_LAUNCH(kKBucketBounds, bucket_bounds_kernel<<<grid ? grid : 1, 256, 0, L.stream>>>(
+                                   k0, p.nvalid, p.salt, shift, mask, off, n_buckets, gate, want));
 }
 
 }  // namespace ltl4c

@@ -205,6 +205,11 @@ struct ltl4c_state {
   int hot_per_sm = 2;              // resident hot_compose CTAs per SM
   int hot_mapk = -1;               // map kind of the program (hot.cu), -1: no hot path
   bool seg = true;                 // LTL4C_NO_SEG: K = 1 units through bucket_warp instead of bucket_seg
+  uint32_t seg_unit = 1024;        // LTL4C_SEG_UNIT: events per bucket_seg unit
+  bool coarse = true;              // LTL4C_NO_COARSE: no one-pass mode for K = 1 hot batches
+  int coarse_per_sm = 2;
+  DevBuf<uint32_t> coarse_off;     // one-pass mode: coarse bucket offsets
+  DevBuf<uint32_t> unit_start2;    // bucket_seg units
   int seg_per_sm = 4;              // resident bucket_seg CTAs per SM
   DevBuf<DevAcc> d_gacc, d_sacc;                 // all-reduced result, shard-pass scratch
   DevBuf<uint32_t> exkey[kMaxLevels];
@@ -465,6 +470,8 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->medium_list.ensure(pl->NB));
   CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
+  if (K == 1) CU(st->unit_start2.ensure(N / st->seg_unit + 4));
+  if (K == 1) CU(st->coarse_off.ensure((1u << kCoarseBits) + 1));
   if (use_hot(st)) {
     const uint64_t nch = (N + hot_chunk_ev(st, N) - 1) / hot_chunk_ev(st, N);
     CU(st->hot_cnt.ensure(2 * (size_t)kHotCountCap));
@@ -500,10 +507,29 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.spill_len = &st->d_acc.p->medium_buckets;
   bp.unit_start = st->unit_start.p;
   bp.n_units = (uint32_t)(pl.N / kUnitTarget + 2);
+  bp.unit_target = kUnitTarget;
   bp.nvalid = st->d_nvalid.p;
   bp.prog = st->d_prog.p;
   bp.acc = st->d_acc.p;
   bp.tab = st->tab.d;
+  return bp;
+}
+
+// the one-pass mode's coarse buckets: the first pass's output and its digit offsets
+BucketParams coarse_params(ltl4c_state *st, const Plan &pl, const BucketParams &bp, int width) {
+  BucketParams cp = bp;
+  cp.key[0] = st->bufkey[0][0].p;
+  cp.let = st->buflet[0].p;
+  cp.bucket_off = st->coarse_off.p;
+  cp.n_buckets = 1u << width;
+  cp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 10;
+  return cp;
+}
+
+// the heavy path's buckets: coarse when the batch took the one-pass mode
+BucketParams heavy_params(ltl4c_state *st, const Plan &pl) {
+  BucketParams bp = bucket_params(st, pl);
+  if (st->h_out->onepass) bp = coarse_params(st, pl, bp, kCoarseBits);
   return bp;
 }
 
@@ -593,23 +619,41 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       pl.dense_n = hp.n_cold;
       pl.dense_flag = hp.nhot;
     }
+    // one-pass mode (decided on the device: some key is hot): the cold stream is
+    // partitioned once into coarse buckets, each taken by a CTA (bucket_coarse);
+    // otherwise the second pass and the warp kernels run
+    const bool onepass = hot && st->hot_mapk == 0 && st->coarse && plan.P == 2;
+    if (onepass) pl.skip_flag = hp.nhot;
     for (int pass = 0; pass < plan.P; ++pass) {
       CU(launch_part_count(pl, pass, L));
       CU(launch_part_scan(pl, pass, L));
       CU(launch_part_scatter(pl, pass, L));
     }
     if (hot) CU(launch_hot_finish(hp, L));
-    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L));
+    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, onepass ? hp.nhot : nullptr, 0));
+    if (onepass) CU(launch_bucket_bounds(pl, st->coarse_off.p, 1u << pl.width[0], L, hp.nhot, 1, pl.width[0]));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
       // a warp per unit (<= kWarpCap events); buckets above that go to the same
       // kernel with kWarpCapBig, above that to the CTA kernel, and above kCap to
       // the heavy path (after the first result copy)
-      CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
       if (K == 1 && st->seg) {
-        // one level: units streamed through warp tables by segmented map scans (seg.cu);
-        // units with too many distinct keys go to the CTA kernel
+        // one level: units of ~seg_unit events streamed through warp tables by
+        // segmented map scans (seg.cu); units with too many distinct keys go to the CTA kernel
+        const uint32_t nu = (uint32_t)(plan.N / st->seg_unit + 2);
+        CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start2.p, nu, L, st->seg_unit,
+                             onepass ? hp.nhot : nullptr, 0));
+        if (onepass) {
+          BucketParams cp = coarse_params(st, plan, bp, pl.width[0]);
+          cp.gate = hp.nhot;
+          cp.gate_want = 1;
+          CU(launch_bucket_coarse(cp, (int)prog->n_formulas, warp_grid(st, st->coarse_per_sm), L));
+        }
         BucketParams sp = bp;
+        if (onepass) sp.gate = hp.nhot;
+        sp.unit_start = st->unit_start2.p;
+        sp.n_units = nu;
+        sp.unit_target = st->seg_unit;
         sp.spill_list = st->large_list.p;
         sp.spill_len = &st->d_acc.p->large_buckets;
         CU(launch_bucket_seg(sp, (int)prog->n_states, (int)prog->n_formulas, warp_grid(st, st->seg_per_sm), L));
@@ -618,6 +662,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
         fp.list_len = &st->d_acc.p->large_buckets;
         CU(launch_bucket_fast(fp, K, (int)prog->n_formulas, st->n_sms, L));
       } else {
+        CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start.p, bp.n_units, L));
         CU(launch_bucket_warp(bp, K, (int)prog->n_formulas, warp_grid(st, st->warp_cfg[1]), L));
         BucketParams mp = bp;
         mp.list = st->medium_list.p;
@@ -844,7 +889,7 @@ ltl4c_status run_virtual(ltl4c_state *st, const uint32_t *const *keys, const uin
                          cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       if (st->h_out->oversize_buckets) {
-        ltl4c_status r2 = run_heavy(st, bucket_params(st, plan), K, s, L);
+        ltl4c_status r2 = run_heavy(st, heavy_params(st, plan), K, s, L);
         if (r2) return r2;
       }
     }
@@ -917,7 +962,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
         CU(cudaMemcpyAsync(&st->h_out->oversize_events, &st->d_acc.p->oversize_events, sizeof(unsigned long long),
                            cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
-        ltl4c_status r2 = run_heavy(st, bucket_params(st, plan), K, s, L);
+        ltl4c_status r2 = run_heavy(st, heavy_params(st, plan), K, s, L);
         if (r2) return r2;
       }
     }
@@ -943,7 +988,8 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
                           (const void *)st->d_acc.p, (const void *)st->d_out.p, (const void *)st->d_nvalid.p,
                           (const void *)st->d_prog.p, (const void *)st->h_out, (const void *)st->hot_cnt.p,
                           (const void *)st->hot_tab.p, (const void *)st->hot_partial.p,
-                          (const void *)st->hot_chunk.p, (const void *)st->hot_n.p})
+                          (const void *)st->hot_chunk.p, (const void *)st->hot_n.p, (const void *)st->unit_start2.p,
+                          (const void *)st->coarse_off.p})
       key.push_back((uintptr_t)b);
     if (st->graph_key != key || !st->graph_exec) {
       drop_graph(st);
@@ -980,7 +1026,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   CU(cudaStreamSynchronize(s));
   if (!online && N > 0 && st->h_out->oversize_buckets > 0) {
     // buckets larger than one shared-memory chunk: segmented heavy path
-    ltl4c_status r = run_heavy(st, bucket_params(st, plan), K, s, L);
+    ltl4c_status r = run_heavy(st, heavy_params(st, plan), K, s, L);
     if (r) return r;
     CU(launch_finalize(st->d_prog.p, st->d_acc.p, st->d_out.p, L));
     CU(cudaMemcpyAsync(st->h_out, st->d_out.p, sizeof(DevOut), cudaMemcpyDeviceToHost, s));
@@ -1092,6 +1138,8 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   if (const char *e = std::getenv("LTL4C_RANK_BALLOT")) st->rank_ballot = std::atoi(e);
   st->hot = std::getenv("LTL4C_NO_HOT") == nullptr;
   st->seg = std::getenv("LTL4C_NO_SEG") == nullptr;
+  if (const char *e = std::getenv("LTL4C_SEG_UNIT")) st->seg_unit = std::max(32, std::atoi(e));
+  st->coarse = std::getenv("LTL4C_NO_COARSE") == nullptr;
   if (const char *e = std::getenv("LTL4C_VIRTUAL_SHARDS")) {
     const int g = std::atoi(e);
     if (g > 1 && g <= 256 && !(g & (g - 1))) st->vshards = g;
@@ -1155,6 +1203,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
       st->hot_mapk = prog->n_states <= 4 && prog->n_atoms <= 4 ? 0 : prog->n_states <= 8 ? 1 : -1;
       if (st->hot_mapk >= 0) st->hot_per_sm = hot_ctas_per_sm(st->hot_mapk);
       st->seg_per_sm = bucket_seg_ctas_per_sm((int)prog->n_states);
+      if (st->hot_mapk == 0) st->coarse_per_sm = bucket_coarse_ctas_per_sm();
     }
   }
   cudaSetDevice(prev);
@@ -1329,6 +1378,8 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->hot_tab.release();
   st->hot_partial.release();
   st->hot_chunk.release();
+  st->unit_start2.release();
+  st->coarse_off.release();
   st->hot_n.release();
   for (auto &t : st->pending) {
     cudaEventDestroy(t.a);

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
   using SM = SegMap<NQB>;
   using M = typename SM::T;
   extern __shared__ __align__(16) uint8_t smem_raw[];
+  if (p.gate && ((*p.gate != 0) != (p.gate_want != 0))) return;  // (the other mode of a K = 1 hot batch)
   const DevProg *prog = p.prog;
   const int nq = prog->nq, A = 1 << prog->na;
   M *smap = reinterpret_cast<M *>(smem_raw);                                   // [A] letter maps
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
       lc[f] = 0;
     }
   };
-  const uint32_t n_items = min(p.n_units, (uint32_t)(*p.nvalid / kUnitTarget) + 2u);
+  const uint32_t n_items = min(p.n_units, (uint32_t)(*p.nvalid / p.unit_target) + 2u);
   uint32_t ep = 0;
   auto take = [&]() { uint32_t u = 0; if (lane == 0) u = atomicAdd(p.bucket_counter, 1u); return __shfl_sync(0xffffffffu, u, 0); };
   // stream events [start, end) of buckets [bl, bh) through the table; false: overflow
@@ -178,7 +179,9 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
               const unsigned long long o = atomicCAS(&w.slot[h], s, mine);
               if (o == s) {
                 w.state[h] = (uint8_t)q0;
-                w.list[atomicAdd(&w.ncl, 1u)] = (uint16_t)h;
+                const uint32_t c = atomicAdd(&w.ncl, 1u);  // (lanes of one round may pass the check together)
+                if (c < (uint32_t)(kSegSlots / 2)) w.list[c] = (uint16_t)h;
+                else ovf = true;
                 slot = (int)h;
                 break;
               }
@@ -189,15 +192,36 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
           }
         }
         if (__any_sync(0xffffffffu, ovf)) return false;
-        // segmented inclusive scan of the letter maps over runs of equal slots
-        M m = slot >= 0 ? smap[ll[r]] : SM::ident();
-        const int prev = __shfl_up_sync(0xffffffffu, slot, 1);
-        bool f = lane == 0 || prev != slot;
-        // (a lane whose window (lane - 2d, lane] holds its run's head is done; lane 0
-        // is a head, so the scan stops after log2 of the longest run)
+        // the round regrouped stably by key (a group = the lanes of one key, in lane
+        // order = trace order): __match_any_sync, then group offsets by a scan of
+        // the group sizes over the group leaders (lowest lanes); lane -> position
+        // offset + rank
+        const uint32_t vm = __ballot_sync(0xffffffffu, slot >= 0);
+        const int nv = __popc(vm);  // valid lanes are a prefix of the warp
+        uint32_t peers = 0;
+        if (slot >= 0) peers = __match_any_sync(vm, (uint32_t)slot);
+        const uint32_t rank = __popc(peers & lanemask_lt());
+        const bool lead = slot >= 0 && rank == 0;
+        const uint32_t gsz = lead ? (uint32_t)__popc(peers) : 0u;
+        uint32_t incl = gsz;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-          if (__all_sync(0xffffffffu, f)) break;
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        const int leader = slot >= 0 ? __ffs(peers) - 1 : lane;
+        const uint32_t off = __shfl_sync(0xffffffffu, incl - gsz, leader);
+        const uint32_t heads = __reduce_or_sync(0xffffffffu, lead ? 1u << off : 0u);
+        if (slot >= 0) stage[off + rank] = smap[ll[r]];
+        __syncwarp();
+        // segmented inclusive scan of the regrouped letter maps (a segment = a group;
+        // a lane whose window holds its segment's head is done, so the scan stops
+        // after log2 of the largest group)
+        M m = lane < nv ? stage[lane] : SM::ident();
+        bool f = ((heads >> lane) & 1u) || lane >= nv;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          if (__all_sync(0xffffffffu, f || lane < d)) break;
           const M y = shfl_up(m, d);
           const bool yf = __shfl_up_sync(0xffffffffu, f, d);
           if (lane >= d) {
@@ -205,24 +229,11 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
             f = f || yf;
           }
         }
-        const int next = __shfl_down_sync(0xffffffffu, slot, 1);
-        const bool tail = slot >= 0 && (lane == 31 || next != slot);
-        const uint32_t tm = __ballot_sync(0xffffffffu, tail);
-        if (tail) stage[lane] = m;
         __syncwarp();
-        if (tail) {
-          const uint32_t peers = __match_any_sync(tm, (uint32_t)slot);
-          if ((peers & lanemask_lt()) == 0) {
-            uint32_t q = w.state[slot];
-            uint32_t pm = peers;
-            do {
-              const int i = __ffs(pm) - 1;
-              pm &= pm - 1;
-              q = SM::image(stage[i], q);
-            } while (pm);
-            w.state[slot] = (uint8_t)q;
-          }
-        }
+        stage[lane] = m;
+        __syncwarp();
+        // each group's leader applies the group's composition (at its last position)
+        if (lead) w.state[slot] = (uint8_t)SM::image(stage[off + gsz - 1], w.state[slot]);
         __syncwarp();
       }
     }
@@ -273,6 +284,192 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
     if (sacc[i]) atomicAdd(&p.acc->hist[i / 6][1][i % 6], (unsigned long long)sacc[i]);
 }
 
+
+
+// ---------------------------------------------------------------- bucket_coarse
+// One-pass mode of a K = 1 hot batch (monitors of <= 4 states, <= 16 letters):
+// the cold stream is partitioned ONCE (512 coarse buckets, whole slices each, in
+// trace order, keys interleaved as in the trace).  A CTA takes a coarse bucket
+// and cuts it into 16 contiguous warp ranges; keys are found or inserted in the
+// CTA's table (64-bit CAS on {epoch, key}), and every warp composes, in trace
+// order, its own transition map of each key it meets (2-bit packed maps, a
+// letter applied through a [256][A] table; lanes sharing a key in a round are
+// grouped by __match_any_sync and their letters applied by the lowest lane in
+// lane order).  A leaf's state is q0 taken through the warps' maps in warp
+// order.  A bucket with more than kCoarseClaims keys goes to the heavy path.
+constexpr int kCoarseWarps = 16;
+constexpr int kCoarseSlots = 4096;
+constexpr int kCoarseClaims = 3072;
+struct CoarseSmem {
+  unsigned long long slot[kCoarseSlots];   // epoch << 32 | key
+  uint8_t wmap[kCoarseWarps][kCoarseSlots];   // per-warp maps (identity outside the bucket's keys)
+  uint8_t tab[256 * 16];                   // [map][letter] -> map
+  uint16_t list[kCoarseClaims];            // claimed slots
+  uint8_t stage[kCoarseWarps][32];
+  uint32_t sacc[kMaxFormulas * 6];
+  uint8_t slab[kMaxFormulas * kMaxStates];
+  uint32_t ncl, ovf, item;
+};
+
+template <int NF>
+__global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(BucketParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  if (p.gate && ((*p.gate != 0) != (p.gate_want != 0))) return;  // (the other mode)
+  CoarseSmem &s = *reinterpret_cast<CoarseSmem *>(smem_raw);
+  const DevProg *prog = p.prog;
+  const int nq = prog->nq, A = 1 << prog->na;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (blockIdx.x == 0 && tid == 0) p.acc->onepass = 1;
+  for (int i = tid; i < 256 * A; i += blockDim.x) {
+    const uint32_t m = (uint32_t)i / A, a = (uint32_t)i % A;
+    uint32_t o = 0;
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t img = (m >> (2 * q)) & 3u;
+      o |= (img < (uint32_t)nq ? (uint32_t)prog->delta[img][a] & 3u : img) << (2 * q);
+    }
+    s.tab[i] = (uint8_t)o;
+  }
+  for (int i = tid; i < kCoarseSlots; i += blockDim.x) s.slot[i] = 0;
+  for (int i = tid; i < kCoarseWarps * kCoarseSlots / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t *>(&s.wmap[0][0])[i] = 0xE4E4E4E4u;
+  for (int i = tid; i < kMaxFormulas * 6; i += blockDim.x) s.sacc[i] = 0;
+  for (int i = tid; i < kMaxFormulas * kMaxStates; i += blockDim.x) s.slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
+  const uint32_t q0 = prog->q0;
+  unsigned long long lc[NF];  // per-thread leaf verdict counts, 16-bit fields for v = 0, 2, 3, 5
+#pragma unroll
+  for (int f = 0; f < NF; ++f) lc[f] = 0;
+  uint32_t ep = 0;
+  uint8_t *wm = s.wmap[wid];
+  uint8_t *stage = s.stage[wid];
+  while (true) {
+    __syncthreads();  // every thread is done with the previous bucket's shared state
+    if (tid == 0) {
+      s.item = atomicAdd(p.bucket_counter, 1u);
+      s.ncl = 0;
+      s.ovf = 0;
+    }
+    __syncthreads();
+    const uint32_t c = s.item;
+    if (c >= p.n_buckets) break;
+    const uint32_t s0 = p.bucket_off[c], s1 = p.bucket_off[c + 1];
+    if (s1 == s0) continue;
+    ++ep;
+    const unsigned long long epk = (unsigned long long)ep << 32;
+    const uint32_t per = ((s1 - s0 + kCoarseWarps - 1) / kCoarseWarps + 31) & ~31u;
+    const uint32_t w0 = min(s1, s0 + wid * per), w1 = min(s1, w0 + per);
+    for (uint32_t base = w0; base < w1; base += 32 * kSegRounds) {
+      if (*(volatile uint32_t *)&s.ovf) break;  // (warp-uniform)
+      uint32_t kk[kSegRounds];
+      uint8_t ll[kSegRounds];
+#pragma unroll
+      for (int r = 0; r < kSegRounds; ++r) {
+        const uint32_t e = base + 32 * r + lane;
+        kk[r] = e < w1 ? __ldcs(&p.key[0][e]) : kAbsent;
+        ll[r] = e < w1 ? __ldcs(&p.let[e]) : (uint8_t)0;
+      }
+#pragma unroll
+      for (int r = 0; r < kSegRounds; ++r) {
+        if (base + 32 * r >= w1) break;  // (warp-uniform)
+        const uint32_t k = kk[r];
+        int slot = -1;
+        bool bad = false;
+        if (base + 32 * r + lane < w1) {
+          uint32_t h = fmix32(k ^ kSegSalt) & (kCoarseSlots - 1);
+          const unsigned long long mine = epk | k;
+          while (true) {
+            unsigned long long v = s.slot[h];
+            if ((v >> 32) != ep) {
+              const unsigned long long o = atomicCAS(&s.slot[h], v, mine);
+              if (o == v) {
+                const uint32_t x = atomicAdd(&s.ncl, 1u);
+                if (x < (uint32_t)kCoarseClaims) s.list[x] = (uint16_t)h;
+                else bad = true;
+                slot = (int)h;
+                break;
+              }
+              v = o;
+            }
+            if (v == mine) { slot = (int)h; break; }
+            h = (h + 1) & (kCoarseSlots - 1);
+          }
+        }
+        if (__any_sync(0xffffffffu, bad)) {
+          if (lane == 0) s.ovf = 1;
+          break;
+        }
+        const uint32_t hm = __ballot_sync(0xffffffffu, slot >= 0);
+        stage[lane] = ll[r];
+        __syncwarp();
+        if (slot >= 0) {
+          const uint32_t peers = __match_any_sync(hm, (uint32_t)slot);
+          if ((peers & lanemask_lt()) == 0) {
+            uint32_t m = wm[slot];
+            uint32_t pm = peers;
+            do {
+              const int i = __ffs(pm) - 1;
+              pm &= pm - 1;
+              m = s.tab[m * A + stage[i]];
+            } while (pm);
+            wm[slot] = (uint8_t)m;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    const bool ovf = s.ovf != 0;
+    if (ovf) {
+      // too many keys for the table: the bucket goes to the heavy path (every map is
+      // reset: warps may have met keys that were never listed)
+      for (int i = tid; i < kCoarseWarps * kCoarseSlots / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(&s.wmap[0][0])[i] = 0xE4E4E4E4u;
+      if (tid == 0) {
+        p.oversize_list[atomicAdd(&p.acc->oversize_buckets, 1ull)] = c;
+        atomicAdd(&p.acc->oversize_events, (unsigned long long)(s1 - s0));
+      }
+      continue;
+    }
+    // every leaf of the bucket: q0 through the warps' maps in warp order; the maps
+    // are reset to the identity for the next bucket
+    const uint32_t ncl = s.ncl;
+    for (uint32_t i = tid; i < ncl; i += blockDim.x) {
+      const uint32_t h = s.list[i];
+      uint32_t q = q0;
+#pragma unroll
+      for (int w = 0; w < kCoarseWarps; ++w) {
+        q = (s.wmap[w][h] >> (2 * q)) & 3u;
+        s.wmap[w][h] = 0xE4;
+      }
+#pragma unroll
+      for (int f = 0; f < NF; ++f) lc[f] += 1ull << (16 * ((s.slab[f * kMaxStates + q] + 1) >> 1));
+    }
+    // (a thread counts at most kCoarseClaims / 512 = 6 leaves per bucket: the 16-bit
+    // fields are flushed every 8192 buckets)
+    if ((ep & 8191u) == 0) {
+#pragma unroll
+      for (int f = 0; f < NF; ++f) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t x = __reduce_add_sync(0xffffffffu, (uint32_t)(lc[f] >> (16 * j)) & 0xFFFFu);
+          if (lane == 0 && x) atomicAdd(&s.sacc[f * 6 + (j == 0 ? 0 : j + 1 + (j == 3))], x);
+        }
+        lc[f] = 0;
+      }
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < NF; ++f) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint32_t x = __reduce_add_sync(0xffffffffu, (uint32_t)(lc[f] >> (16 * j)) & 0xFFFFu);
+      if (lane == 0 && x) atomicAdd(&s.sacc[f * 6 + (j == 0 ? 0 : j + 1 + (j == 3))], x);
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < NF * 6; i += blockDim.x)
+    if (s.sacc[i]) atomicAdd(&p.acc->hist[i / 6][1][i % 6], (unsigned long long)s.sacc[i]);
+}
+
 template <int NQB, int NF>
 size_t seg_smem() {
   using M = typename SegMap<NQB>::T;
@@ -318,6 +515,35 @@ int bucket_seg_ctas_per_sm(int nq) {
   if (nq <= 4) q(bucket_seg_kernel<4, 4>, seg_smem<4, 4>());
   else if (nq <= 8) q(bucket_seg_kernel<8, 4>, seg_smem<8, 4>());
   else q(bucket_seg_kernel<16, 4>, seg_smem<16, 4>());
+  return n > 0 ? n : 1;
+}
+
+
+
+template <int NF>
+static cudaError_t coarse_launch(const BucketParams &p, uint32_t grid, const Launcher &L) {
+  const size_t sm = sizeof(CoarseSmem);
+  cudaFuncSetAttribute(bucket_coarse_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (L.before) L.before(L.ctx, kKBucketWarp);
+  bucket_coarse_kernel<NF><<<grid, 32 * kCoarseWarps, sm, L.stream>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (L.after) L.after(L.ctx, kKBucketWarp);
+  return e;
+}
+
+cudaError_t launch_bucket_coarse(const BucketParams &p, int nf, uint32_t grid, const Launcher &L) {
+  switch (nf) {
+    case 1: return coarse_launch<1>(p, grid, L);
+    case 2: return coarse_launch<2>(p, grid, L);
+    case 3: return coarse_launch<3>(p, grid, L);
+    default: return coarse_launch<4>(p, grid, L);
+  }
+}
+
+int bucket_coarse_ctas_per_sm() {
+  int n = 1;
+  cudaFuncSetAttribute(bucket_coarse_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CoarseSmem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, bucket_coarse_kernel<4>, 32 * kCoarseWarps, sizeof(CoarseSmem));
   return n > 0 ? n : 1;
 }
 

@@ -188,3 +188,28 @@ def test_K1_heavy_hitter_path_on_and_off(env):
             finally:
                 os.environ.pop("LTL4C_NO_HOT", None)
             _same(got, want, (tr.formula, off))
+
+
+def test_K1_one_pass_mode_and_coarse_overflow(env):
+    """K = 1 hot batches take the one-pass mode (seg.cu bucket_coarse: the cold
+    stream partitioned once, a CTA per coarse bucket); a coarse bucket with more keys
+    than the CTA table goes to the heavy path on the coarse partition.  Both, and the
+    two-pass mode (LTL4C_NO_COARSE), give the oracle's result."""
+    rng = np.random.default_rng(11)
+    n = 6_000_000
+    hot = rng.random(n) < 0.5
+    keys = np.where(hot, rng.integers(0, 8, n), rng.integers(1000, 1 << 31, n)).astype(np.uint32)
+    letters = rng.choice(np.array([0, 1, 2, 3], np.uint8), size=n, p=[0.4, 0.3, 0.2, 0.1])
+    over = tracegen.Trace(tracegen.FILES, [keys], letters)         # ~3M cold keys: every coarse bucket overflows
+    fits = tracegen.zipf_socket_trace(seed=12, n=n, support=1 << 18)  # ~700 cold keys per coarse bucket
+    for tr in (over, fits):
+        want = oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=NPROC)
+        for env_var in (None, "LTL4C_NO_COARSE"):
+            if env_var:
+                os.environ[env_var] = "1"
+            try:
+                got = _verify(env, tr.formula, tr.keys, tr.letters)[0]
+            finally:
+                if env_var:
+                    os.environ.pop(env_var, None)
+            _same(got, want, (tr.formula, env_var))
