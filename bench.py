@@ -368,12 +368,42 @@ def main():
             extra[x]["workload"] = rx["text"]
             extra[x]["root_verdict"] = rx["verdict"]
             rx = None
+        extra["C1_sweep"] = c1_sweep(args, local_rank)
         line["extra"] = extra
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
+
+
+def c1_sweep(args, local_rank):
+    """The paper's size sweep (N = 2^14 ... 2^23) of the C1 socket property:
+    per size, the mean latency of one ltl4c_verify (graph replay, inputs in HBM, no
+    L2 flush: these inputs are small) and N / latency."""
+    import torch
+    import paper_1411_2239_b200 as ltl4c
+    dev = torch.device("cuda", local_rank)
+    out = []
+    for lg in range(14, 24):
+        tr = tracegen.socket_trace(seed=0, n=1 << lg)
+        keys = [torch.from_numpy(k.view(np.int32)).to(dev) for k in tr.keys]
+        letters = torch.from_numpy(tr.letters).to(dev)
+        st = ltl4c.compile(tr.formula).state(local_rank, capacity=tr.n)
+        stream = torch.cuda.current_stream(dev)
+        for _ in range(args.warmup):
+            st.verify(keys, letters, stream=stream)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            res = st.verify(keys, letters, stream=stream)[0]
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        ms = a.elapsed_time(b) / args.steps
+        out.append({"n": tr.n, "ms": ms, "events_per_s": tr.n / (ms / 1e3), "root_verdict": res.verdict})
+        del st, keys, letters
+    return out
 
 
 def run_c5(args):
