@@ -258,6 +258,7 @@ def roofline(r, steps, peak, peak_kind, config):
     achieved = alg / (per_launch_ms / 1e3) / 1e9
     traffic = None
     try:
+        # (the capture of this config's dominant kernel; null when none was taken)
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             traffic = json.load(f).get(config, {}).get(dom)
     except Exception:
