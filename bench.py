@@ -61,6 +61,9 @@ CONFIGS = {
     "C4": ("C4 (one GPU's share): A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), "
            "125M events, 10^6 videos Zipf(0.8), unique requests of 1-4 events", 125_000_000,
            lambda lo, hi: tracegen.proxy_trace(seed=0, n=125_000_000, lo=lo, hi=hi), 9),
+    "C6": ("C6: A u:user(u) => F small(u), small = avg_chunksize(u) <= maximum (Dropbox fairness, P:1127-1136), "
+           "10M events, 10^5 users", 10_000_000,
+           lambda lo, hi: _cut(tracegen.dropbox_trace(seed=0, n=10_000_000, users=100_000), lo, hi), 5),
     "C4B": ("C4: A v:vid(v) => E_{=0} r:req(r) => (cached(v) && external(r)), 1B-event proxy-cache "
             "trace, 10^6 videos Zipf(0.8), sharded by hash(video) over the GPUs (BASELINE.json configs[3])",
             1_000_000_000,

@@ -96,6 +96,15 @@ def test_C4_proxy(env):
                  oracle.run_offline(tr.formula, tr.keys, tr.letters), "C4")
 
 
+@pytest.mark.parametrize("seed,n,users", [(0, 400_000, 5000), (1, 4_000_000, 100_000)])
+def test_C6_dropbox(env, seed, n, users):
+    """C6 (SURVEY §8(f) NEXT-4 workload): one level, F small(u), uniform users
+    (no hot key at 5000 users of 400k events; at 4M events a two-pass cold stream)."""
+    tr = tracegen.dropbox_trace(seed=seed, n=n, users=users)
+    _assert_same(_gpu_offline(env, tr.formula, tr.keys, tr.letters)[0],
+                 oracle.run_offline(tr.formula, tr.keys, tr.letters), ("C6", n))
+
+
 def _project(letters, prog_atoms, prop_atoms):
     out = np.zeros_like(letters)
     for j, a in enumerate(prop_atoms):

@@ -451,6 +451,24 @@ def test_C4_closed_form():
     assert r["verdict"] == (F if bad.any() else Tc)
 
 
+@pytest.mark.parametrize("seed,p_heavy", [(0, 0.02), (1, 0.0)])
+def test_C6_dropbox_closed_form(seed, p_heavy):
+    """C6, A u : user(u) => F small(u): a user's leaf is T once one of
+    its events has small set (F latches), else Fp (Table 1 / Def. 4: no
+    future is excluded); the root over T and Fp children is Fp if any child is Fp,
+    else Tc (A2: a new user may still come and never be small)."""
+    tr = tracegen.dropbox_trace(seed=seed, n=60_000, users=800, p_heavy=p_heavy)
+    r = oracle.run_offline(tr.formula, tr.keys, tr.letters)
+    u, a = tr.keys[0], tr.letters
+    users = np.unique(u)
+    sat = np.unique(u[(a & 1) == 1])
+    t, fp = sat.shape[0], users.shape[0] - sat.shape[0]
+    assert r["hist"][1][T] == t and r["hist"][1][Fp] == fp and r["hist"][1].sum() == t + fp
+    assert r["verdict"] == (Fp if fp else Tc)
+    if p_heavy == 0.0:
+        assert fp == 0 or r["verdict"] == Fp
+
+
 def test_invariance_relabel_and_interleave():
     """Relabeling key values by a bijection, or interleaving events of different
     slices while keeping each slice's order, leaves every count unchanged."""

@@ -12,7 +12,8 @@ returns a ``Trace`` with
 
 Workload recipes follow SURVEY.md §8(d) / DESIGN.md "Input recipe":
 C1 socket, C2 nested login (Eq. 8), C3 Zipf-skewed
-socket, C4 proxy cache, C5 three-level online batch.
+socket, C4 proxy cache, C5 three-level online batch, C6 the
+Dropbox fairness case study.
 """
 from __future__ import annotations
 
@@ -27,6 +28,7 @@ SOCKET = "forall[>=0.95] s : socket(s) => G (receive(s) -> F respond(s))"
 LOGIN = "forall x : user(x) => exists[<=3] r : rid(r) => (login && unauthorized)"
 PROXY = "forall v : vid(v) => exists[=0] r : req(r) => (cached(v) && external(r))"
 FILES = "forall[>=50%] f : intrace(f) => (opened(f) U close(f))"
+DROPBOX = "forall u : user(u) => F small(u)"
 FIG1 = "forall[>=0.5] f : file(f) => (G a || (b U c))"
 C5_FORMULAS = [
     "forall[>=0.95] h : host(h) => forall u : user(u) => exists[<=2] s : session(s) => F authfail",
@@ -239,6 +241,35 @@ def proxy_trace(seed: int = 0, n: int = 1_000_000, videos: int = 1_000_000, s: f
     cat = (lambda i, dt: np.concatenate([p[i] for p in parts]) if parts else np.zeros(0, dt))
     return Trace(PROXY, [cat(0, np.uint32), cat(1, np.uint32)], cat(2, np.uint8),
                  {"config": "C4", "seed": seed, "videos": videos, "n": n, "lo": lo})
+
+
+def dropbox_trace(seed: int = 0, n: int = 1_000_000, users: int = 10_000, chunk_max: float = 4.0,
+                  p_heavy: float = 0.02) -> Trace:
+    """C6: personal cloud storage fairness: A u : user(u) => F small(u),
+    small(u) = avg_chunksize(u) <= maximum.  Each event is one chunk upload by a user
+    (uniform over `users`); a user's chunk sizes are exponential with a per-user mean
+    (most users well below `chunk_max`; a fraction `p_heavy` repeatedly upload chunks of
+    about the maximum size); bit0 of the letter = the user's running average
+    chunk size over their uploads so far is <= chunk_max (the program variable the
+    predicate reads).  No method arithmetic: the atom is part of the input."""
+    rng = np.random.default_rng(SEED_BASE + 6 + seed)
+    ids = _ids(rng, users)
+    heavy = rng.random(users) < p_heavy
+    mean = np.where(heavy, chunk_max * 1.02, rng.uniform(0.2, 1.5, users) * chunk_max)
+    u = rng.integers(0, users, n)
+    size = rng.exponential(1.0, n) * mean[u]
+    size = np.where(heavy[u], chunk_max * (1.0 + 0.05 * rng.random(n)), size)
+    order = np.argsort(u, kind="stable")            # per-user running averages in trace order
+    su, ss = u[order], size[order]
+    csum = np.cumsum(ss)
+    first = np.r_[True, su[1:] != su[:-1]]
+    start = np.maximum.accumulate(np.where(first, np.arange(n), 0))
+    base = np.where(start > 0, csum[start - 1], 0.0)
+    cnt = np.arange(n) - start + 1
+    avg = (csum - base) / cnt
+    small = np.empty(n, dtype=np.uint8)
+    small[order] = (avg <= chunk_max).astype(np.uint8)
+    return Trace(DROPBOX, [ids[u]], small, {"config": "C6", "seed": seed, "users": users, "n": n})
 
 
 def worked_example() -> Trace:
