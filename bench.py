@@ -373,6 +373,7 @@ def main():
             extra[x]["root_verdict"] = rx["verdict"]
             rx = None
         extra["C1_sweep"] = c1_sweep(args, local_rank)
+        extra["online_batch1"] = online_latency(args, local_rank)
         line["extra"] = extra
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -408,6 +409,29 @@ def c1_sweep(args, local_rank):
         out.append({"n": tr.n, "ms": ms, "events_per_s": tr.n / (ms / 1e3), "root_verdict": res.verdict})
         del st, keys, letters
     return out
+
+
+def online_latency(args, local_rank, n_events=2000):
+    """Per-event verdict stream (SURVEY §8(f) NEXT-4 latency mode): the C2 property
+    online, one event per ltl4c_verify (batch = 1, carried state), each result read
+    back -- the latency of one event's verdict."""
+    import torch
+    import paper_1411_2239_b200 as ltl4c
+    dev = torch.device("cuda", local_rank)
+    tr = tracegen.login_trace(seed=0, n=n_events + 64, users=200)
+    keys = [torch.from_numpy(k.view(np.int32)).to(dev) for k in tr.keys]
+    letters = torch.from_numpy(tr.letters).to(dev)
+    st = ltl4c.compile(tr.formula).state(local_rank, online=True)
+    stream = torch.cuda.current_stream(dev)
+    for j in range(64):
+        st.verify([k[j:j + 1] for k in keys], letters[j:j + 1], stream=stream)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    for j in range(64, 64 + n_events):
+        res = st.verify([k[j:j + 1] for k in keys], letters[j:j + 1], stream=stream)[0]
+    dt = time.perf_counter() - t0
+    return {"events": n_events, "us_per_event": dt / n_events * 1e6, "events_per_s": n_events / dt,
+            "root_verdict": res.verdict, "note": "wall clock per verify call, result on the host each time"}
 
 
 def run_c5(args):

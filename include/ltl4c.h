@@ -195,6 +195,38 @@ ltl4c_status ltl4c_state_reset(ltl4c_state *st);
 
 void ltl4c_state_free(ltl4c_state *st);
 
+/* Checkpoint / restore of an ONLINE state's carried state (
+ * the paper keeps the submonitor tree across invocations): the submonitor
+ * set 𝔻 (every leaf's value vector and monitor state, Def. 5), every
+ * quantifier node with its child histogram and verdict (Def. 6/7), the
+ * per-level counts and the stream position.  The blob is host memory owned by the
+ * caller, opaque, for the same program (checked by a fingerprint of its tables).
+ *   ltl4c_state_checkpoint_size: bytes a checkpoint of `st` takes now;
+ *   ltl4c_state_checkpoint: drains the state's batches in flight, writes the blob
+ *     to buf[0 .. cap) (*written = its size);
+ *   ltl4c_state_restore: replaces the carried state of an online state created
+ *     from the same program (tables reallocated to the checkpoint's capacities);
+ *     later batches continue the stream exactly as the checkpointed state would.
+ * Errors: E_INVALID (null argument, offline state, cap too small, not a
+ * checkpoint, other program), E_CUDA, E_OOM. */
+ltl4c_status ltl4c_state_checkpoint_size(ltl4c_state *st, uint64_t *bytes);
+ltl4c_status ltl4c_state_checkpoint(ltl4c_state *st, void *buf, uint64_t cap, uint64_t *written);
+ltl4c_status ltl4c_state_restore(ltl4c_state *st, const void *buf, uint64_t len);
+
+/* Explain / dump of an ONLINE state's carried tree (the
+ * quantifier tree of §3.3, Fig. 2): the nodes of depth `level`
+ * (1 <= level <= n_levels; depth n_levels = the leaves, i.e. the submonitors of
+ * 𝔻) with their current verdict for formula `formula` -- Def. 6 for inner nodes
+ * (P:648-675), lambda of the monitor state for leaves (Def. 5).
+ * Writes at most `cap` nodes: keys[i][j] (i < level) = the value vector of node j,
+ * verdicts[j] = its B6 code (ltl4c_verdict); *count = the nodes at that depth (all
+ * of them, even beyond cap).  Order unspecified.  Buffers are HOST memory owned by
+ * the caller (keys: `level` arrays of cap u32; either may be null when cap = 0).
+ * Errors: E_INVALID (null state/count, offline state, level or formula out of
+ * range), E_CUDA. */
+ltl4c_status ltl4c_state_nodes(ltl4c_state *st, uint32_t level, uint32_t formula, uint32_t *const *keys,
+                               uint8_t *verdicts, uint64_t cap, uint64_t *count);
+
 /* Kernel-level profiling: when enabled, every library kernel launch is bracketed
  * by CUDA events on the stream it runs on; ltl4c_state_stats sums them (this
  * synchronises the stream).  ltl4c_state_stats_reset zeroes the counters. */

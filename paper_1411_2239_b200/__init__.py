@@ -95,6 +95,11 @@ _lib.ltl4c_verify_host.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, 
 _lib.ltl4c_verify_async.argtypes = [_P, ctypes.POINTER(_Batch), ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_result_get.argtypes = [_P, ctypes.c_uint64, ctypes.POINTER(_Result)]
 _lib.ltl4c_state_reset.argtypes = [_P]
+_lib.ltl4c_state_checkpoint_size.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_state_checkpoint.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_state_restore.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64]
+_lib.ltl4c_state_nodes.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p),
+                                   ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_state_free.argtypes = [_P]
 _lib.ltl4c_state_free.restype = None
 _lib.ltl4c_state_profile.argtypes = [_P, ctypes.c_int]
@@ -351,6 +356,36 @@ class State:
     def reset(self):
         _check(_lib.ltl4c_state_reset(self._h))
         self.next_index = 0
+
+    def checkpoint(self) -> bytes:
+        """The carried state of an online state as an opaque blob (ltl4c_state_checkpoint)."""
+        n = ctypes.c_uint64()
+        _check(_lib.ltl4c_state_checkpoint_size(self._h, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        w = ctypes.c_uint64()
+        _check(_lib.ltl4c_state_checkpoint(self._h, buf, n.value, ctypes.byref(w)))
+        return bytes(buf.raw[:w.value]) + self.next_index.to_bytes(8, "little")
+
+    def nodes(self, level: int, formula: int = 0):
+        """(keys, verdicts) of every node at depth `level` of an online state's tree
+        (level = n_levels: the leaves) -- ltl4c_state_nodes.  keys: list of `level`
+        uint32 arrays; verdicts: uint8 B6 codes."""
+        cnt = ctypes.c_uint64()
+        _check(_lib.ltl4c_state_nodes(self._h, level, formula, None, None, 0, ctypes.byref(cnt)))
+        n = cnt.value
+        keys = [np.zeros(n, np.uint32) for _ in range(level)]
+        ver = np.zeros(n, np.uint8)
+        if n:
+            ptrs = (ctypes.c_void_p * level)(*[k.ctypes.data for k in keys])
+            _check(_lib.ltl4c_state_nodes(self._h, level, formula, ptrs, ver.ctypes.data, n, ctypes.byref(cnt)))
+        return keys, ver
+
+    def restore(self, blob: bytes):
+        """Continue the stream of a checkpointed online state (ltl4c_state_restore)."""
+        body, nxt = blob[:-8], int.from_bytes(blob[-8:], "little")
+        buf = ctypes.create_string_buffer(body, len(body))
+        _check(_lib.ltl4c_state_restore(self._h, buf, len(body)))
+        self.next_index = nxt
 
     def profile(self, enable: bool = True):
         _check(_lib.ltl4c_state_profile(self._h, 1 if enable else 0))

@@ -125,12 +125,13 @@ __global__ void hot_count_hist_kernel(HotParams hp) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= (uint32_t)kHotCountCap) return;
   const uint32_t c = hp.cnt_val[s];
-  if (c >= (uint32_t)kHotMinCount) atomicAdd(&hp.nhot[8 + min(c, 63u)], 1u);
+  if (c >= 1) atomicAdd(&hp.nhot[8 + min(c, 63u)], 1u);  // (bins 1, 2: the sample's singletons / doubletons)
 }
 
 // keys sampled >= t times, t the smallest threshold >= kHotMinCount leaving at
 // most 3/4 of the slots wanted, take a slot of their bucket; the most sampled
-// first (pass 0: counts >= 4t, pass 1: the rest).  nhot[0] = keys inserted.
+// first (pass 0: counts >= 4t, pass 1: the rest).  nhot[0] = keys inserted,
+// nhot[1] = their sampled events.
 __global__ void hot_insert_kernel(HotParams hp, int pass) {
   __shared__ uint32_t thr;
   if (threadIdx.x == 0) {
@@ -150,8 +151,30 @@ __global__ void hot_insert_kernel(HotParams hp, int pass) {
   for (int i = 0; i < 4; ++i)
     if (atomicCAS(&hp.slot_key[(i < 2 ? b1 : b2) + (i & 1)], kAbsent, k) == kAbsent) {
       atomicAdd(hp.nhot, 1u);
+      atomicAdd(hp.nhot + 1, c);
       return;
     }
+}
+
+// The batch's mode, from the sample (one thread):
+//   nhot[2] (dense) = the hot keys carry >= 1/4 of the sampled events: they are
+//     composed where they lie and the rest is compacted into the cold stream;
+//     otherwise nothing is hot and the partition reads the batch itself;
+//   nhot[3] (one pass) = the cold keys are few enough for 512 coarse buckets of
+//     <= ~1500 keys each: Chao1 over the sample's cold keys (D + f1^2 / 2 f2,
+//     f1 / f2 = keys sampled once / twice) <= kOnePassKeys.  A coarse bucket that
+//     still overflows its CTA table goes to the heavy path (same result).
+__global__ void hot_decide_kernel(HotParams hp) {
+  if (threadIdx.x || blockIdx.x) return;
+  const uint32_t *bin = hp.nhot + 8;
+  const bool dense = 4ull * hp.nhot[1] >= (unsigned long long)hp.n_samples && hp.nhot[0] > 0;
+  unsigned long long d = 0;
+  for (int c = 1; c < 64; ++c) d += bin[c];
+  if (dense) d -= min(d, (unsigned long long)hp.nhot[0]);
+  const double f1 = bin[1], f2 = bin[2] > 0 ? bin[2] : 1;
+  const double chao1 = (double)d + f1 * f1 / (2.0 * f2);
+  hp.nhot[2] = dense ? 1u : 0u;
+  hp.nhot[3] = hp.force_onepass || chao1 <= (double)kOnePassKeys ? 1u : 0u;
 }
 
 template <int MAPK>
@@ -197,7 +220,7 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, 4) hot_compose_kernel(HotPa
   }
   for (int i = lane; i < S; i += 32) s.wmap[wid][i] = HM::ident();
   __syncthreads();
-  const bool dense = hp.nhot[0] > 0;  // no hot key: nothing composed, the partition reads the batch itself
+  const bool dense = hp.nhot[2] != 0;  // not dense: nothing composed, the partition reads the batch itself
   const uint32_t chunk = blockIdx.x * kHotCtaWarps + wid;
   const unsigned long long n = hp.n;
   const unsigned long long e0 = (unsigned long long)chunk * hp.chunk_ev;
@@ -323,7 +346,7 @@ __global__ void __launch_bounds__(1024) hot_prefix_kernel(HotParams hp) {
 constexpr int kGatherParts = 4;
 __global__ void __launch_bounds__(256) hot_gather_kernel(HotParams hp) {
   const uint32_t chunk = blockIdx.x / kGatherParts, part = blockIdx.x % kGatherParts;
-  if (chunk >= (uint32_t)hp.n_chunks || hp.nhot[0] == 0) return;
+  if (chunk >= (uint32_t)hp.n_chunks || hp.nhot[2] == 0) return;
   const uint32_t cnt = hp.chunk_cold[chunk];
   const uint32_t per = (cnt + kGatherParts - 1) / kGatherParts;
   const uint32_t lo = min(cnt, part * per), hi = min(cnt, lo + per);
@@ -370,7 +393,7 @@ __global__ void __launch_bounds__(1024) hot_finish_kernel(HotParams hp) {
       unpack[m] = o;
     }
   __syncthreads();
-  if (hp.nhot[0] == 0) return;
+  if (hp.nhot[2] == 0) return;
   const DevProg *prog = hp.prog;
   const int slot = blockIdx.x * 32 + tx;
   const int nc = hp.n_chunks, per = (nc + 31) / 32;
@@ -422,6 +445,7 @@ cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L) {
   hot_count_hist_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp);
   hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 0);
   hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 1);
+  hot_decide_kernel<<<1, 32, 0, L.stream>>>(hp);
   cudaError_t e = cudaGetLastError();
   if (L.after) L.after(L.ctx, kKHot);
   return e;

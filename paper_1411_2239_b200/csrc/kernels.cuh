@@ -67,6 +67,7 @@ constexpr int kHotSamplesMax = 1 << 19; // evenly spaced sample of the batch
 constexpr int kHotCountCap = 1 << 20;  // sample-count table slots
 constexpr int kHotMinCount = 4;        // a hot key was sampled at least this often
 constexpr int kHotCtaWarps = 8;
+constexpr double kOnePassKeys = 768.0 * 1024;  // cold keys (Chao1 estimate) for the one-pass mode
 struct HotParams {
   const uint32_t *k0;                   // the batch's key column (K = 1)
   const uint8_t *let;
@@ -77,7 +78,7 @@ struct HotParams {
   uint32_t let_mask;
   uint32_t *cnt_key, *cnt_val;          // [kHotCountCap] sample counts (key = ABSENT: empty)
   uint32_t *slot_key;                   // [slots] hot key of each slot (ABSENT: empty) = dense id
-  uint32_t *nhot;                       // [0]: hot keys, [8 + c]: keys sampled c times (c < 64)
+  uint32_t *nhot;                       // [0] hot keys, [1] their samples, [2] dense, [3] one pass; [8 + c] keys sampled c times
   void *partial;                        // [n_chunks][slots] per-warp-chunk maps
   uint32_t *cold_key;                   // scratch [n]: chunk c's cold events at its own range
   uint8_t *cold_let;
@@ -88,6 +89,7 @@ struct HotParams {
   unsigned long long *n_cold;           // total cold events (zeroed)
   unsigned long long chunk_ev;          // events per chunk (multiple of 512)
   int n_chunks;                         // warps of hot_compose
+  int force_onepass;                    // LTL4C_FORCE_ONEPASS (tests): one-pass mode whatever the estimate
   const DevProg *prog;
   DevAcc *acc;
 };

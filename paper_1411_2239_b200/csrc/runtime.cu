@@ -208,6 +208,7 @@ struct ltl4c_state {
   uint32_t seg_unit = 1024;        // LTL4C_SEG_UNIT: events per bucket_seg unit
   bool coarse = true;              // LTL4C_NO_COARSE: no one-pass mode for K = 1 hot batches
   int coarse_per_sm = 2;
+  int force_onepass = 0;           // LTL4C_FORCE_ONEPASS (tests): one-pass mode whatever the sample says
   DevBuf<uint32_t> coarse_off;     // one-pass mode: coarse bucket offsets
   DevBuf<uint32_t> unit_start2;    // bucket_seg units
   int seg_per_sm = 4;              // resident bucket_seg CTAs per SM
@@ -605,6 +606,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       hp.n_cold = st->hot_n.p;
       hp.chunk_ev = hot_chunk_ev(st, plan.N);
       hp.n_chunks = (int)((plan.N + hp.chunk_ev - 1) / hp.chunk_ev);
+      hp.force_onepass = st->force_onepass;
       hp.prog = st->d_prog.p;
       hp.acc = st->d_acc.p;
       CU(cudaMemsetAsync(hp.cnt_key, 0xFF, sizeof(uint32_t) * kHotCountCap, s));
@@ -617,21 +619,22 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       pl.dense_key = hp.dense_key;
       pl.dense_let = hp.dense_let;
       pl.dense_n = hp.n_cold;
-      pl.dense_flag = hp.nhot;
+      pl.dense_flag = hp.nhot + 2;
     }
     // one-pass mode (decided on the device: some key is hot): the cold stream is
     // partitioned once into coarse buckets, each taken by a CTA (bucket_coarse);
     // otherwise the second pass and the warp kernels run
     const bool onepass = hot && st->hot_mapk == 0 && st->coarse && plan.P == 2;
-    if (onepass) pl.skip_flag = hp.nhot;
+    const uint32_t *one = onepass ? hp.nhot + 3 : nullptr;  // the one-pass flag (device)
+    if (onepass) pl.skip_flag = one;
     for (int pass = 0; pass < plan.P; ++pass) {
       CU(launch_part_count(pl, pass, L));
       CU(launch_part_scan(pl, pass, L));
       CU(launch_part_scatter(pl, pass, L));
     }
     if (hot) CU(launch_hot_finish(hp, L));
-    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, onepass ? hp.nhot : nullptr, 0));
-    if (onepass) CU(launch_bucket_bounds(pl, st->coarse_off.p, 1u << pl.width[0], L, hp.nhot, 1, pl.width[0]));
+    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, one, 0));
+    if (onepass) CU(launch_bucket_bounds(pl, st->coarse_off.p, 1u << pl.width[0], L, one, 1, pl.width[0]));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
       // a warp per unit (<= kWarpCap events); buckets above that go to the same
@@ -642,15 +645,15 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
         // segmented map scans (seg.cu); units with too many distinct keys go to the CTA kernel
         const uint32_t nu = (uint32_t)(plan.N / st->seg_unit + 2);
         CU(launch_unit_start(st->bucket_off.p, plan.NB, st->unit_start2.p, nu, L, st->seg_unit,
-                             onepass ? hp.nhot : nullptr, 0));
+                             one, 0));
         if (onepass) {
           BucketParams cp = coarse_params(st, plan, bp, pl.width[0]);
-          cp.gate = hp.nhot;
+          cp.gate = one;
           cp.gate_want = 1;
           CU(launch_bucket_coarse(cp, (int)prog->n_formulas, warp_grid(st, st->coarse_per_sm), L));
         }
         BucketParams sp = bp;
-        if (onepass) sp.gate = hp.nhot;
+        sp.gate = one;
         sp.unit_start = st->unit_start2.p;
         sp.n_units = nu;
         sp.unit_target = st->seg_unit;
@@ -1140,6 +1143,7 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   st->seg = std::getenv("LTL4C_NO_SEG") == nullptr;
   if (const char *e = std::getenv("LTL4C_SEG_UNIT")) st->seg_unit = std::max(32, std::atoi(e));
   st->coarse = std::getenv("LTL4C_NO_COARSE") == nullptr;
+  st->force_onepass = std::getenv("LTL4C_FORCE_ONEPASS") != nullptr;
   if (const char *e = std::getenv("LTL4C_VIRTUAL_SHARDS")) {
     const int g = std::atoi(e);
     if (g > 1 && g <= 256 && !(g & (g - 1))) st->vshards = g;
@@ -1340,6 +1344,196 @@ ltl4c_status ltl4c_state_reset(ltl4c_state *st) {
   st->have_index = false;
   st->next_index = 0;
   st->events_seen = 0;
+  cudaSetDevice(prev);
+  return LTL4C_OK;
+}
+
+// ------------------------------------------------------------ checkpoint / restore
+namespace {
+struct CkptHeader {
+  char magic[8];
+  uint64_t prog_hash;
+  uint32_t n_levels, n_formulas, have_index, epoch, batch_id, pad;
+  uint64_t next_index, events_seen, known_leaves, known_nodes[kMaxLevels], known_cum;
+  uint64_t leaf_cap, node_cap;
+};
+constexpr char kCkptMagic[8] = {'L', 'T', 'L', '4', 'C', 'K', '0', '1'};
+
+uint64_t prog_hash(const DevProg &p) {  // FNV-1a over the program tables
+  const unsigned char *b = reinterpret_cast<const unsigned char *>(&p);
+  uint64_t h = 1469598103934665603ull;
+  for (size_t i = 0; i < sizeof p; ++i) h = (h ^ b[i]) * 1099511628211ull;
+  return h;
+}
+
+// (buffer, bytes) of every carried table, in blob order
+std::vector<std::pair<void *, size_t>> carried_buffers(ltl4c_state *st, uint64_t leaf_cap, uint64_t node_cap) {
+  std::vector<std::pair<void *, size_t>> v;
+  Tables &t = st->tab;
+  v.push_back({t.leaf_slot.p, sizeof(uint4) * leaf_cap});
+  v.push_back({t.leaf_state.p, leaf_cap});
+  for (int l = 1; l < (int)st->prog->n_levels; ++l) {
+    v.push_back({t.node_slot[l].p, sizeof(uint4) * node_cap});
+    v.push_back({t.node_verdict[l].p, sizeof(uint32_t) * node_cap});
+    v.push_back({t.node_hist[l].p, sizeof(uint32_t) * node_cap * kMaxFormulas * 6});
+    v.push_back({t.node_aux[l].p, sizeof(uint32_t) * node_cap});
+  }
+  return v;
+}
+
+ltl4c_status drain(ltl4c_state *st) {
+  for (int i = 0; i < ltl4c_state::kRing; ++i)
+    if (st->ring_ticket[i]) CU(cudaEventSynchronize(st->ring_ev[i]));
+  if (st->cur_stream) CU(cudaStreamSynchronize(st->cur_stream));
+  CU(cudaDeviceSynchronize());
+  return LTL4C_OK;
+}
+}  // namespace
+
+ltl4c_status ltl4c_state_checkpoint_size(ltl4c_state *st, uint64_t *bytes) {
+  if (!st || !bytes) return fail(LTL4C_E_INVALID, "null argument");
+  if (!(st->flags & LTL4C_STATE_ONLINE)) return fail(LTL4C_E_INVALID, "checkpoint of an offline state");
+  const uint64_t lc = st->tab.d.leaf_cap, nc = st->prog->n_levels > 1 ? st->tab.d.node_cap[1] : 0;
+  uint64_t n = sizeof(CkptHeader) + sizeof(DevAcc) + (sizeof(uint4) + 1) * lc;
+  for (int l = 1; l < (int)st->prog->n_levels; ++l) n += (sizeof(uint4) + 4 + 4 * kMaxFormulas * 6 + 4) * nc;
+  *bytes = n;
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_checkpoint(ltl4c_state *st, void *buf, uint64_t cap, uint64_t *written) {
+  if (!st || !buf || !written) return fail(LTL4C_E_INVALID, "null argument");
+  uint64_t need = 0;
+  if (ltl4c_status r = ltl4c_state_checkpoint_size(st, &need)) return r;
+  if (cap < need) return fail(LTL4C_E_INVALID, "checkpoint buffer too small");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  if (ltl4c_status r = drain(st)) return r;
+  // the stream position and counters as of the last batch (results in flight included)
+  for (int i = 0; i < ltl4c_state::kRing; ++i) st->ring_ticket[i] = 0;
+  st->outstanding = 0;
+  unsigned long long cnt[1 + kMaxLevels];
+  CU(cudaMemcpy(cnt, &st->d_acc.p->leaves, sizeof cnt, cudaMemcpyDeviceToHost));
+  st->known_leaves = cnt[0];
+  for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = cnt[1 + l];
+  st->known_cum = st->enq_events;
+  CkptHeader h{};
+  std::memcpy(h.magic, kCkptMagic, 8);
+  h.prog_hash = prog_hash(st->hprog);
+  h.n_levels = st->prog->n_levels;
+  h.n_formulas = st->prog->n_formulas;
+  h.have_index = st->have_index;
+  h.epoch = st->tab.d.leaf_cap ? st->tab.d.epoch : st->epoch;
+  h.batch_id = st->batch_id;
+  h.next_index = st->next_index;
+  h.events_seen = st->events_seen;
+  h.known_leaves = st->known_leaves;
+  for (int l = 0; l < kMaxLevels; ++l) h.known_nodes[l] = st->known_nodes[l];
+  h.known_cum = 0;
+  h.leaf_cap = st->tab.d.leaf_cap;
+  h.node_cap = st->prog->n_levels > 1 ? st->tab.d.node_cap[1] : 0;
+  unsigned char *o = static_cast<unsigned char *>(buf);
+  std::memcpy(o, &h, sizeof h);
+  o += sizeof h;
+  CU(cudaMemcpy(o, st->d_acc.p, sizeof(DevAcc), cudaMemcpyDeviceToHost));
+  o += sizeof(DevAcc);
+  if (h.leaf_cap)
+    for (auto &b : carried_buffers(st, h.leaf_cap, h.node_cap)) {
+      CU(cudaMemcpy(o, b.first, b.second, cudaMemcpyDeviceToHost));
+      o += b.second;
+    }
+  *written = (uint64_t)(o - static_cast<unsigned char *>(buf));
+  cudaSetDevice(prev);
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_restore(ltl4c_state *st, const void *buf, uint64_t len) {
+  if (!st || !buf) return fail(LTL4C_E_INVALID, "null argument");
+  if (!(st->flags & LTL4C_STATE_ONLINE)) return fail(LTL4C_E_INVALID, "restore into an offline state");
+  CkptHeader h;
+  if (len < sizeof h) return fail(LTL4C_E_INVALID, "not a checkpoint");
+  std::memcpy(&h, buf, sizeof h);
+  if (std::memcmp(h.magic, kCkptMagic, 8) != 0) return fail(LTL4C_E_INVALID, "not a checkpoint");
+  if (h.prog_hash != prog_hash(st->hprog) || h.n_levels != st->prog->n_levels || h.n_formulas != st->prog->n_formulas)
+    return fail(LTL4C_E_INVALID, "checkpoint of another program");
+  uint64_t need = sizeof h + sizeof(DevAcc);
+  if (h.leaf_cap) {
+    need += (sizeof(uint4) + 1) * h.leaf_cap;
+    for (uint32_t l = 1; l < h.n_levels; ++l) need += (sizeof(uint4) + 4 + 4 * kMaxFormulas * 6 + 4) * h.node_cap;
+  }
+  if (len < need) return fail(LTL4C_E_INVALID, "truncated checkpoint");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  if (ltl4c_status r = drain(st)) return r;
+  for (int i = 0; i < ltl4c_state::kRing; ++i) st->ring_ticket[i] = 0;
+  st->outstanding = 0;
+  st->tab.release();
+  const unsigned char *in = static_cast<const unsigned char *>(buf) + sizeof h;
+  CU(cudaMemcpy(st->d_acc.p, in, sizeof(DevAcc), cudaMemcpyHostToDevice));
+  in += sizeof(DevAcc);
+  if (h.leaf_cap) {
+    if (ltl4c_status r = alloc_tables(st, st->tab, h.leaf_cap, std::max<uint64_t>(h.node_cap, 1), 0, false, true)) return r;
+    CU(cudaDeviceSynchronize());
+    for (auto &b : carried_buffers(st, h.leaf_cap, h.node_cap)) {
+      CU(cudaMemcpy(b.first, in, b.second, cudaMemcpyHostToDevice));
+      in += b.second;
+    }
+    st->tab.d.epoch = h.epoch;
+  }
+  st->epoch = h.epoch;
+  st->batch_id = h.batch_id;
+  st->have_index = h.have_index != 0;
+  st->next_index = h.next_index;
+  st->events_seen = h.events_seen;
+  st->known_leaves = h.known_leaves;
+  for (int l = 0; l < kMaxLevels; ++l) st->known_nodes[l] = h.known_nodes[l];
+  st->enq_events = st->known_cum = 0;
+  st->poisoned = false;
+  std::memset(st->h_out, 0, sizeof(DevOut));
+  cudaSetDevice(prev);
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_nodes(ltl4c_state *st, uint32_t level, uint32_t formula, uint32_t *const *keys,
+                               uint8_t *verdicts, uint64_t cap, uint64_t *count) {
+  if (!st || !count) return fail(LTL4C_E_INVALID, "null argument");
+  if (!(st->flags & LTL4C_STATE_ONLINE)) return fail(LTL4C_E_INVALID, "node dump of an offline state");
+  const uint32_t K = st->prog->n_levels;
+  if (level < 1 || level > K || formula >= st->prog->n_formulas) return fail(LTL4C_E_INVALID, "level or formula out of range");
+  if (cap && (!verdicts || !keys)) return fail(LTL4C_E_INVALID, "null output buffer");
+  *count = 0;
+  const bool leaf = level == K;
+  const uint64_t n = leaf ? st->tab.d.leaf_cap : st->tab.d.node_cap[level];
+  if (n == 0) return LTL4C_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  if (ltl4c_status r = drain(st)) return r;
+  std::vector<uint4> slots(n);
+  std::vector<uint8_t> state;
+  std::vector<uint32_t> packed;
+  CU(cudaMemcpy(slots.data(), leaf ? (const void *)st->tab.d.leaf_slot : (const void *)st->tab.d.node_slot[level],
+                sizeof(uint4) * n, cudaMemcpyDeviceToHost));
+  if (leaf) {
+    state.resize(n);
+    CU(cudaMemcpy(state.data(), st->tab.d.leaf_state, n, cudaMemcpyDeviceToHost));
+  } else {
+    packed.resize(n);
+    CU(cudaMemcpy(packed.data(), st->tab.d.node_verdict[level], sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+  }
+  const uint32_t ready = (st->tab.d.epoch << 1) | 1u;  // table tag of a live slot of this epoch
+  uint64_t c = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (slots[i].x != ready) continue;
+    if (c < cap) {
+      const uint32_t kv[3] = {slots[i].y, slots[i].z, slots[i].w};
+      for (uint32_t l = 0; l < level; ++l) keys[l][c] = kv[l];
+      verdicts[c] = leaf ? st->hprog.lab[formula][state[i] & 0x7Fu] : (uint8_t)((packed[i] >> (8 * formula)) & 0xFFu);
+    }
+    ++c;
+  }
+  *count = c;
   cudaSetDevice(prev);
   return LTL4C_OK;
 }

@@ -191,10 +191,11 @@ def test_K1_heavy_hitter_path_on_and_off(env):
 
 
 def test_K1_one_pass_mode_and_coarse_overflow(env):
-    """K = 1 hot batches take the one-pass mode (seg.cu bucket_coarse: the cold
-    stream partitioned once, a CTA per coarse bucket); a coarse bucket with more keys
-    than the CTA table goes to the heavy path on the coarse partition.  Both, and the
-    two-pass mode (LTL4C_NO_COARSE), give the oracle's result."""
+    """K = 1 batches take the one-pass mode when the sample estimates few cold keys
+    (seg.cu bucket_coarse: the cold stream partitioned once, a CTA per coarse bucket);
+    forced onto ~3M cold keys (LTL4C_FORCE_ONEPASS) every coarse bucket overflows its
+    CTA table and goes to the heavy path on the coarse partition; unforced, that trace
+    takes the two-pass mode.  All, and LTL4C_NO_COARSE, give the oracle's result."""
     rng = np.random.default_rng(11)
     n = 6_000_000
     hot = rng.random(n) < 0.5
@@ -204,7 +205,7 @@ def test_K1_one_pass_mode_and_coarse_overflow(env):
     fits = tracegen.zipf_socket_trace(seed=12, n=n, support=1 << 18)  # ~700 cold keys per coarse bucket
     for tr in (over, fits):
         want = oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=NPROC)
-        for env_var in (None, "LTL4C_NO_COARSE"):
+        for env_var in (None, "LTL4C_NO_COARSE", "LTL4C_FORCE_ONEPASS"):
             if env_var:
                 os.environ[env_var] = "1"
             try:

@@ -129,6 +129,75 @@ def test_C5_formula_batch_online(env):
             _assert_same(got[f], m.evaluate(), (f, hi))
 
 
+def test_checkpoint_restore_continues_the_stream(env):
+    """an online state's carried state checkpointed after
+    some batches and restored into a fresh state (and into a state that had verified
+    something else) continues the stream exactly: every later result equals the oracle
+    on the prefix; a checkpoint of another program is refused."""
+    ltl4c, torch, dev = env
+    tr = tracegen.c5_trace(seed=3, n=240_000, users=1500, hosts=48, span_events=50_000)
+    prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+    props = [oracle.Property(t) for t in tracegen.C5_FORMULAS]
+    mons = [oracle.Monitor(p) for p in props]
+    a = prog.state(0, online=True)
+    cuts = [0, 900, 60_000, 110_000, 180_000, 240_000]
+
+    def feed(st, lo, hi, check):
+        k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+        got = st.verify(k, l, first_index=lo)
+        if check:
+            for f, (p, m) in enumerate(zip(props, mons)):
+                m.feed([x[lo:hi] for x in tr.keys], _project(tr.letters[lo:hi], prog.atoms, p.atoms))
+                _assert_same(got[f], m.evaluate(), ("ckpt", f, hi))
+        return got
+
+    for lo, hi in zip(cuts[:3], cuts[1:4]):
+        feed(a, lo, hi, True)
+    blob = a.checkpoint()
+    b = prog.state(0, online=True)
+    b.restore(blob)
+    c = prog.state(0, online=True)
+    feed(c, 0, 900, False)             # c verified another prefix first: restore replaces it
+    c.restore(blob)
+    for lo, hi in zip(cuts[3:-1], cuts[4:]):
+        gb = feed(b, lo, hi, True)
+        for st in (a, c):
+            g = feed(st, lo, hi, False)
+            for f in range(len(props)):
+                assert g[f].verdict == gb[f].verdict and np.array_equal(g[f].hist, gb[f].hist)
+    other = ltl4c.compile(tracegen.LOGIN).state(0, online=True)
+    with pytest.raises(ltl4c.Ltl4cError):
+        other.restore(blob)
+
+
+def test_node_dump_explains_the_counts(env):
+    """ltl4c_state_nodes lists every node of a depth of the online
+    tree (Fig. 2) with its verdict; each node's verdict equals the oracle's
+    verdict of the same value vector, and the per-verdict counts are the histogram."""
+    ltl4c, torch, dev = env
+    tr = tracegen.c5_trace(seed=5, n=60_000, users=400, hosts=16, span_events=20_000)
+    prog = ltl4c.compile_batch(tracegen.C5_FORMULAS)
+    st = prog.state(0, online=True)
+    props = [oracle.Property(t) for t in tracegen.C5_FORMULAS]
+    mons = [oracle.Monitor(p) for p in props]
+    for lo, hi in [(0, 25_000), (25_000, 60_000)]:
+        k, l = _dev(torch, dev, [x[lo:hi] for x in tr.keys], tr.letters[lo:hi])
+        got = st.verify(k, l, first_index=lo)
+        for p, m in zip(props, mons):
+            m.feed([x[lo:hi] for x in tr.keys], _project(tr.letters[lo:hi], prog.atoms, p.atoms))
+    for f, m in enumerate(mons):
+        want = m.evaluate()
+        for level in (1, 2, 3):
+            keys, ver = st.nodes(level, f)
+            assert np.array_equal(np.bincount(ver, minlength=6), got[f].hist[level]), (f, level)
+            assert np.array_equal(got[f].hist[level], want["hist"][level]), (f, level)
+            pick = np.random.default_rng(level).choice(ver.shape[0], size=min(300, ver.shape[0]), replace=False)
+            for j in pick:
+                assert m.node_verdict([int(k[j]) for k in keys]) == int(ver[j]), (f, level, j)
+    with pytest.raises(ltl4c.Ltl4cError):
+        st.nodes(4, 0)
+
+
 def test_online_batches_equal_offline_prefix(env):
     ltl4c, torch, dev = env
     tr = tracegen.login_trace(seed=9, n=200_000, users=500, rid_events=4, p_unauth=0.05)
