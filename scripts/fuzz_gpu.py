@@ -3,6 +3,7 @@
 repeated leaves, batch splits, formula batches) through the C ABI, every result
 compared bit-exactly with the oracle.  Developer tool (the test suite holds the
 fixed cases); run on a GPU box:  python scripts/fuzz_gpu.py [seconds] [seed]"""
+import os
 import random
 import sys
 import time
@@ -65,12 +66,18 @@ def main():
             prog = ltl4c.compile_batch(texts) if nform > 1 else ltl4c.compile(texts[0])
         except ltl4c.Ltl4cError:
             continue  # product over the budget
-        n = rng.choice([1, 50, 3000, 40_000, 300_000, 1_500_000])
+        n = rng.choice([1, 50, 3000, 40_000, 300_000, 1_500_000, 1_500_000, 6_000_000])
         keys, letters = trace(rng, levels, n, len(prog.atoms))
         want = [oracle.run_offline(t, keys, project(letters, prog.atoms, oracle.Property(t).atoms)) for t in texts]
         online = rng.random() < 0.4
         pipelined = online and rng.random() < 0.5  # ltl4c_verify_async, results read with a lag
+        # K = 1 mode knobs (read at state creation): forced one-pass / two-pass / no hot path
+        knob = rng.choice([None, None, "LTL4C_FORCE_ONEPASS", "LTL4C_NO_COARSE", "LTL4C_NO_HOT"])
+        if knob:
+            os.environ[knob] = "1"
         st = prog.state(0, online=online)
+        if knob:
+            os.environ.pop(knob)
         if online:
             cuts = sorted({0, n, *[rng.randint(0, n) for _ in range(rng.randint(0, 12))]})
         else:
@@ -90,7 +97,7 @@ def main():
         for f, w in enumerate(want):
             ok = got[f].verdict == w["verdict"] and np.array_equal(got[f].hist, w["hist"])
             if not ok:
-                print("MISMATCH", texts[f], n, levels, online, pipelined, cuts, got[f].verdict, w["verdict"],
+                print("MISMATCH", texts[f], n, levels, online, pipelined, knob, cuts, got[f].verdict, w["verdict"],
                       got[f].hist.tolist(), w["hist"].tolist(), flush=True)
                 sys.exit(1)
         cases += 1
