@@ -374,6 +374,7 @@ def main():
             rx = None
         extra["C1_sweep"] = c1_sweep(args, local_rank)
         extra["online_batch1"] = online_latency(args, local_rank)
+        extra["ingest"] = ingest_rate(args, local_rank)
         line["extra"] = extra
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -409,6 +410,40 @@ def c1_sweep(args, local_rank):
         out.append({"n": tr.n, "ms": ms, "events_per_s": tr.n / (ms / 1e3), "root_verdict": res.verdict})
         del st, keys, letters
     return out
+
+
+def ingest_rate(args, local_rank, n=2_000_000):
+    """Trace ingest: C2-shaped JSON-lines records (mixed value
+    spellings, noise keys) encoded on the GPU from device memory (ltl4c_dencode_jsonl)
+    and, for context, by the host encoder on one core."""
+    import torch
+    import paper_1411_2239_b200 as ltl4c
+    dev = torch.device("cuda", local_rank)
+    tr = tracegen.login_trace(seed=0, n=n, users=20_000, rid_events=2)
+    text = tracegen.to_jsonl(tr, ["user", "rid"], ["login", "unauthorized"], [[], []], seed=0, style="mixed")
+    data = text.encode()
+    d_text = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    prog = ltl4c.compile(tr.formula)
+    stream = torch.cuda.current_stream(dev)
+    ms = []
+    for i in range(args.warmup + args.steps):
+        enc = prog.device_encoder(local_rank, max_values=1 << 21)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        k, l = enc.encode(d_text, stream=stream)
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        if i >= args.warmup:
+            ms.append(a.elapsed_time(b))
+        del enc
+    d_ms = sum(ms) / len(ms)
+    t0 = time.perf_counter()
+    prog.encoder().encode(data)
+    h_s = time.perf_counter() - t0
+    return {"records": tr.n, "bytes": len(data), "device_ms": d_ms, "device_records_per_s": tr.n / (d_ms / 1e3),
+            "device_GB_per_s": len(data) / (d_ms / 1e3) / 1e9, "host_records_per_s_1core": tr.n / h_s,
+            "note": "fresh dictionaries per call; the call includes its own line-count sync"}
 
 
 def online_latency(args, local_rank, n_events=2000):

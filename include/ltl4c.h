@@ -267,6 +267,31 @@ ltl4c_status ltl4c_encode_jsonl(ltl4c_encoder *enc, const char *text, uint64_t l
 ltl4c_status ltl4c_encoder_values(const ltl4c_encoder *enc, uint32_t level, uint64_t *count);
 void ltl4c_encoder_free(ltl4c_encoder *enc);
 
+/* --- trace ingest on the device ----------------------- */
+
+/* The host encoder's semantics (above; §4.1 Valuation Extraction, P:915-935,
+ * reading A12) run on the GPU over JSON-lines text in DEVICE memory -- the stage
+ * upstream of the hot path that the paper measures as its strace parsing module
+ * (P:1087-1094).  One record per line; blank lines are skipped.
+ * Dictionary ids are dense per level (0, 1, ... < ltl4c_dencoder_values) and
+ * persist across calls of one encoder, but are assigned in the order concurrent
+ * threads first claim a value (not first appearance): only the partition of values
+ * into ids is the host encoder's, and verdicts and counts depend on nothing else.
+ * Values are identified by a 64-bit hash of their canonical string (DESIGN.md
+ * A28).  `max_values` = capacity of each level's dictionary.
+ * ltl4c_dencode_jsonl: text = DEVICE pointer, len bytes; keys (n_levels DEVICE
+ * arrays) and letters (DEVICE) receive one event per record in line order;
+ * capacity = their length.  The call synchronises `cuda_stream`.  Errors:
+ * E_INVALID (null argument; more records than capacity: *n_events = the number
+ * needed, nothing written), E_SYNTAX (malformed record: the message names the
+ * first bad line, nothing written), E_BUDGET (a dictionary is full), E_CUDA, E_OOM. */
+typedef struct ltl4c_dencoder ltl4c_dencoder;
+ltl4c_status ltl4c_dencoder_create(const ltl4c_program *prog, int device, uint64_t max_values, ltl4c_dencoder **out);
+ltl4c_status ltl4c_dencode_jsonl(ltl4c_dencoder *enc, const char *text, uint64_t len, uint32_t *const *keys,
+                                 uint8_t *letters, uint64_t capacity, uint64_t *n_events, void *cuda_stream);
+ltl4c_status ltl4c_dencoder_values(const ltl4c_dencoder *enc, uint32_t level, uint64_t *count);
+void ltl4c_dencoder_free(ltl4c_dencoder *enc);
+
 /* Thread-local message of the last non-OK status ("" if none). */
 const char *ltl4c_last_error(void);
 

@@ -98,6 +98,12 @@ _lib.ltl4c_state_reset.argtypes = [_P]
 _lib.ltl4c_state_checkpoint_size.argtypes = [_P, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_state_checkpoint.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_state_restore.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64]
+_lib.ltl4c_dencoder_create.argtypes = [_P, ctypes.c_int, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p)]
+_lib.ltl4c_dencode_jsonl.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_void_p),
+                                     ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64), ctypes.c_void_p]
+_lib.ltl4c_dencoder_values.argtypes = [_P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64)]
+_lib.ltl4c_dencoder_free.argtypes = [_P]
+_lib.ltl4c_dencoder_free.restype = None
 _lib.ltl4c_state_nodes.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_state_free.argtypes = [_P]
@@ -191,6 +197,10 @@ class Program:
         """Host trace encoder for this program's guard keys and atoms (ltl4c_encode_jsonl)."""
         return Encoder(self)
 
+    def device_encoder(self, device: int = 0, max_values: int = 1 << 22) -> "DeviceEncoder":
+        """Trace encoder on the GPU (ltl4c_dencode_jsonl)."""
+        return DeviceEncoder(self, device, max_values)
+
 
 class Encoder:
     """JSON-lines records -> (keys, letters) host arrays in the layout verify() takes
@@ -225,6 +235,51 @@ class Encoder:
     def values(self, level: int) -> int:
         c = ctypes.c_uint64()
         _check(_lib.ltl4c_encoder_values(self._h, level, ctypes.byref(c)))
+        return int(c.value)
+
+
+class DeviceEncoder:
+    """JSON-lines records already in device memory -> (keys, letters) device tensors
+    (ltl4c_dencode_jsonl: the host encoder's semantics on the GPU; per-key
+    dictionaries persist across calls; ids are a relabelling of the host encoder's)."""
+
+    def __init__(self, prog: Program, device: int, max_values: int):
+        self.prog, self.device = prog, device
+        self._h = ctypes.c_void_p()
+        _check(_lib.ltl4c_dencoder_create(prog._h, device, max_values, ctypes.byref(self._h)))
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None) and _lib is not None:
+                _lib.ltl4c_dencoder_free(self._h)
+        except Exception:
+            pass
+        self._h = None
+
+    def encode(self, text, stream=None):
+        """`text`: a uint8 CUDA tensor of JSON lines (or bytes / str, copied to the
+        device first).  Returns (keys: list of int32 device tensors, letters: uint8
+        device tensor), one event per record."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if not isinstance(text, torch.Tensor):
+            data = text.encode() if isinstance(text, str) else bytes(text)
+            text = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev) if data else torch.zeros(0, dtype=torch.uint8, device=dev)
+        n_nl = int((text == 10).sum().item()) if text.numel() else 0
+        cap = n_nl + 1
+        keys = [torch.empty(cap, dtype=torch.int32, device=dev) for _ in range(self.prog.n_levels)]
+        letters = torch.empty(cap, dtype=torch.uint8, device=dev)
+        kp = (ctypes.c_void_p * MAX_LEVELS)(*[k.data_ptr() for k in keys])
+        n = ctypes.c_uint64()
+        _check(_lib.ltl4c_dencode_jsonl(self._h, ctypes.c_void_p(text.data_ptr() if text.numel() else 0),
+                                        text.numel(), kp, ctypes.c_void_p(letters.data_ptr()), cap,
+                                        ctypes.byref(n), _stream_handle(stream)))
+        m = int(n.value)
+        return [k[:m] for k in keys], letters[:m]
+
+    def values(self, level: int) -> int:
+        c = ctypes.c_uint64()
+        _check(_lib.ltl4c_dencoder_values(self._h, level, ctypes.byref(c)))
         return int(c.value)
 
 

@@ -548,6 +548,68 @@ def test_records_through_encoder_and_gpu(env):
         _assert_same(got, mon.evaluate(), ("online records", lo))
 
 
+def _same_partition(a, b):
+    """a and b label the same events with a bijection of ids (equal partitions)."""
+    a, b = np.asarray(a, np.int64), np.asarray(b, np.int64)
+    if a.shape != b.shape:
+        return False
+    pairs = np.unique(np.stack([a, b]), axis=1)
+    return np.unique(pairs[0]).shape[0] == pairs.shape[1] == np.unique(pairs[1]).shape[0]
+
+
+def test_device_encoder_matches_host_and_oracle(env):
+    """JSON-lines records in device memory encoded on the GPU
+    (ltl4c_dencode_jsonl) give the host encoder's letters and, per key, the same
+    partition of events by value (ids are a relabelling); verified on the GPU they
+    equal the oracle reading the SAME records with its own reader -- the worked
+    example, mixed spellings (12 / "12" / 12.0 / 1.2e1, noise keys, blank lines,
+    escapes), parametric atoms, three levels, and an online stream in chunks."""
+    import os
+    ltl4c, torch, dev = env
+    golden = open(os.path.join(os.path.dirname(__file__), "golden", "login_example.jsonl")).read()
+    tr = tracegen.login_trace(seed=27, n=200_000, users=2000, rid_events=2, p_unauth=0.05)
+    big = tracegen.to_jsonl(tr, ["user", "rid"], ["login", "unauthorized"], [[], []], seed=4, style="mixed")
+    sock = tracegen.zipf_socket_trace(seed=28, n=150_000, support=1 << 12)
+    sock_txt = tracegen.to_jsonl(sock, ["socket"], ["receive", "respond"], [[0], [0]], seed=5, style="mixed")
+    c5 = tracegen.c5_trace(seed=6, n=80_000, users=600, hosts=20, span_events=20_000)
+    c5_txt = tracegen.to_jsonl(c5, ["host", "user", "session"], ["authfail", "request", "response", "admin", "external"],
+                               [[], [], [], [], []], seed=6, style="mixed")
+    extra = ('\n{"user": "a\\u00e9", "rid": 1e0, "login": true, "unauthorized": true}\n'
+             '   \n{"rid": "1", "user": "a\u00e9", "login": true, "unauthorized": true, "x": {"y": [1, {"z": 2}]}}\n')
+    cases = [(tracegen.LOGIN, golden), (tracegen.LOGIN, big + extra), (tracegen.SOCKET, sock_txt),
+             ("\n".join(tracegen.C5_FORMULAS), c5_txt)]
+    for formula, text in cases:
+        prog = ltl4c.compile_batch(formula.split("\n")) if "\n" in formula else ltl4c.compile(formula)
+        hk, hl = prog.encoder().encode(text)
+        dk, dl = prog.device_encoder().encode(text)
+        assert np.array_equal(dl.cpu().numpy(), hl), formula
+        for a, b in zip(hk, dk):
+            assert _same_partition(a, b.cpu().numpy().view(np.uint32)), formula
+        got = prog.state(0).verify(dk, dl)
+        texts = formula.split("\n")
+        for f, t in enumerate(texts):
+            p = oracle.Property(t)
+            if len(texts) == 1:
+                _assert_same(got[f], oracle.run_records(t, text), ("dev enc", t[:30]))
+            else:
+                want = oracle.run_offline(t, hk, _project(hl, prog.atoms, p.atoms))
+                _assert_same(got[f], want, ("dev enc batch", f))
+    # online: chunks through one device encoder (dictionaries persist)
+    prog = ltl4c.compile(tracegen.LOGIN)
+    enc = prog.device_encoder()
+    st = prog.state(0, online=True)
+    lines = big.splitlines(keepends=True)
+    mon = oracle.RecordMonitor(oracle.Property(tracegen.LOGIN))
+    for lo in range(0, len(lines), 60_000):
+        chunk = "".join(lines[lo:lo + 60_000])
+        k, l = enc.encode(chunk)
+        got = st.verify(k, l)[0]
+        mon.feed_records(chunk)
+        _assert_same(got, mon.evaluate(), ("dev enc online", lo))
+    with pytest.raises(ltl4c.Ltl4cError):
+        enc.encode('{"user": 1, "rid": 2}\n{"user": 1 "rid": 2}\n')
+
+
 @pytest.mark.parametrize("shards", [2, 4, 8])
 def test_virtual_shards(env, shards):
     """SURVEY §4 T4 / §8(e) on one GPU: LTL4C_VIRTUAL_SHARDS = G runs the multi-GPU
