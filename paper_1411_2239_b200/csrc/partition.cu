@@ -202,14 +202,14 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
   const unsigned long long wbase = (unsigned long long)tile * kTileEv + (unsigned long long)wid * (kTileEv / kPWarps);
   // loads first (memory-level parallelism)
   uint32_t rk[kRounds][K];
-  uint8_t rl[kRounds];
+  uint32_t rl[(kRounds + 3) / 4] = {};  // letters, four per register
 #pragma unroll
   for (int r = 0; r < kRounds; ++r) {
     const unsigned long long j = wbase + r * 32 + lane;
     const bool in = kFull || j < n;
 #pragma unroll
     for (int k = 0; k < K; ++k) rk[r][k] = in ? __ldcs(k == 0 && dense ? &pl.dense_key[j] : &in_key[k][j]) : kAbsent;
-    rl[r] = in ? (uint8_t)(__ldcs(&in_let[j]) & (kFirst ? pl.let_mask : 0xFFu)) : (uint8_t)0;
+    rl[r >> 2] |= (in ? (uint32_t)(__ldcs(&in_let[j]) & (kFirst ? pl.let_mask : 0xFFu)) : 0u) << (8 * (r & 3));
   }
   // digits 2t, 2t+1 belong to thread t < kMaxDigits / 2: global run start =
   // pass base (scan of the digit totals) + the tile's offset within the digit
@@ -277,22 +277,24 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
   // digits 2t, 2t+1: exclusive over warps (two u16 halves per word, < 4096 each),
   // tile totals, tile-local run starts
   uint32_t *wc32 = reinterpret_cast<uint32_t *>(&s.wcnt[0][0]);
-  uint32_t wc[kPWarps];
+  // (the per-warp prefix is recomputed in the write-back loop below instead of kept
+  // in 16 registers: the kernel no longer spills at 64 registers)
   uint32_t run = 0;
   if (dth) {
 #pragma unroll
-    for (int w = 0; w < kPWarps; ++w) {
-      wc[w] = run;
-      run += wc32[w * (kMaxDigits / 2) + tid];
-    }
+    for (int w = 0; w < kPWarps; ++w) run += wc32[w * (kMaxDigits / 2) + tid];
   }
   const uint32_t c0 = run & 0xFFFFu, c1 = run >> 16;
   const uint32_t loc0 = block_scan_512(c0 + c1, s.wt), loc1 = loc0 + c0;
   const uint32_t pb0 = block_scan_512(tot0 + tot1, s.wt), pb1 = pb0 + tot0;
   if (dth) {
-    const uint32_t lp = loc0 | loc1 << 16;
+    uint32_t pre = loc0 | loc1 << 16;
 #pragma unroll
-    for (int w = 0; w < kPWarps; ++w) wc32[w * (kMaxDigits / 2) + tid] = wc[w] + lp;
+    for (int w = 0; w < kPWarps; ++w) {
+      const uint32_t v = wc32[w * (kMaxDigits / 2) + tid];
+      wc32[w * (kMaxDigits / 2) + tid] = pre;
+      pre += v;
+    }
     s.gdelta[d0] = pb0 + til0 - loc0;
     s.gdelta[d1] = pb1 + til1 - loc1;
   }
@@ -307,7 +309,7 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
     const uint32_t lp = s.wcnt[wid][d] + (dr[r] >> 16);
 #pragma unroll
     for (int k = 0; k < K; ++k) s.kout[k][lp] = rk[r][k];
-    s.lout[lp] = rl[r];
+    s.lout[lp] = (uint8_t)(rl[r >> 2] >> (8 * (r & 3)));
     s.gout[lp] = lp + s.gdelta[d];
   }
   if (lane == 0) s.wt[wid] = ntile;
