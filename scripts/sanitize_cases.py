@@ -84,6 +84,43 @@ def main():
                 for t in tickets:
                     got = st.result(t)[0]
             check(got, want, f"online K={levels} {mode}")
+    # K = 1 modes (hot.cu / seg.cu): dense + one pass (default), two passes + warp units,
+    # forced one pass over many cold keys (coarse overflow -> heavy), no hot path
+    text = FORMULAS[1]
+    prog = ltl4c.compile(text)
+    m = max(n, 200_000)
+    g = np.random.default_rng(77)
+    hot = g.random(m) < 0.6
+    k1 = np.where(hot, g.integers(0, 6, m), g.integers(100, 1 << 30, m) % 60_000).astype(np.uint32)
+    k1 = ((k1 * 2654435761) & 0xFFFFFFFE).astype(np.uint32)
+    l1 = g.integers(0, 1 << len(prog.atoms), size=m).astype(np.uint8)
+    want = oracle.run_offline(text, [k1], project(l1, prog.atoms, oracle.Property(text).atoms))
+    for knob in (None, "LTL4C_NO_COARSE", "LTL4C_FORCE_ONEPASS", "LTL4C_NO_HOT"):
+        if knob:
+            os.environ[knob] = "1"
+        st = prog.state(0)
+        if knob:
+            os.environ.pop(knob)
+        got = st.verify([torch.from_numpy(k1.view(np.int32)).to(dev)], torch.from_numpy(l1).to(dev))[0]
+        check(got, want, f"K=1 modes knob={knob}")
+    # device encoder (ingest.cu), checkpoint / restore, node dump
+    import tracegen
+    tr = tracegen.login_trace(seed=3, n=20_000, users=300, rid_events=2, p_unauth=0.05)
+    txt = tracegen.to_jsonl(tr, ["user", "rid"], ["login", "unauthorized"], [[], []], seed=1, style="mixed")
+    lp = ltl4c.compile(tracegen.LOGIN)
+    dk, dl = lp.device_encoder(max_values=1 << 16).encode(txt)
+    check(lp.state(0).verify(dk, dl)[0], oracle.run_records(tracegen.LOGIN, txt), "device encoder")
+    st = lp.state(0, online=True)
+    st.verify([x[:9000] for x in dk], dl[:9000])
+    blob = st.checkpoint()
+    st2 = lp.state(0, online=True)
+    st2.restore(blob)
+    got = st2.verify([x[9000:] for x in dk], dl[9000:])[0]
+    check(got, oracle.run_records(tracegen.LOGIN, txt), "checkpoint / restore")
+    for level in (1, 2):
+        kk, vv = st2.nodes(level)
+        assert int(vv.shape[0]) == int(got.hist[level].sum())
+    print("ok       node dump", flush=True)
     torch.cuda.synchronize()
     print("sanitize cases done", flush=True)
 
