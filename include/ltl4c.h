@@ -25,7 +25,8 @@ extern "C" {
 #endif
 
 #define LTL4C_MAX_LEVELS 3      /* quantifier string length n (Eq. 5)        */
-#define LTL4C_MAX_ATOMS 8       /* atoms of psi; a letter is a u8 bitmask           */
+#define LTL4C_MAX_ATOMS 8       /* atoms of one formula's psi                       */
+#define LTL4C_MAX_BATCH_ATOMS 16 /* atoms of a formula batch (letter classes > 8)    */
 #define LTL4C_MAX_STATES 16     /* LTL4 monitor states (after minimisation/product) */
 #define LTL4C_MAX_FORMULAS 4    /* formulas verified together (ltl4c_compile_batch) */
 #define LTL4C_ABSENT 0xFFFFFFFFu /* key value meaning "the event does not bind it"  */
@@ -70,22 +71,32 @@ typedef struct {
 } ltl4c_quantifier;
 
 /* Read-only view of a compiled program (host memory owned by the program).
- * delta[q * (1 << n_atoms) + a] is the LTL4 monitor transition (Def. 5)
- * of the (product) automaton; label[f * n_states + q] is lambda_f(q) in B6 codes
- * {0,2,3,5}; states with label 0/5 are traps. */
+ * Letters: a valuation of the atoms is a bitmask m (bit j = atom j, Def. 1/2);
+ * the batches carry its LETTER CODE: m itself when n_atoms <= 8 (letter_bits =
+ * n_atoms, letter_class = NULL); for a formula batch over 9..16 atoms, the class
+ * letter_class[m] of m, letters of one class acting identically on every state of
+ * the product monitor (letter equivalence classes; at most
+ * 256 classes, else E_BUDGET), codes < 1 << letter_bits.
+ * delta[q * (1 << letter_bits) + code] is the LTL4 monitor transition (Def. 5,
+ * P:326-336) of the (product) automaton; label[f * n_states + q] is lambda_f(q) in
+ * B6 codes {0,2,3,5}; states with label 0/5 are traps. */
 typedef struct {
   uint32_t n_formulas, n_levels, n_atoms, n_states, initial;
   const uint8_t *delta;
   const uint8_t *label;
   const ltl4c_quantifier *quant; /* [n_formulas][n_levels] */
-  const char *const *atom_names; /* [n_atoms], bit j of a letter = atom j             */
+  const char *const *atom_names; /* [n_atoms], bit j of a valuation = atom j          */
+  uint32_t letter_bits;          /* codes are < 1 << letter_bits                      */
+  const uint8_t *letter_class;   /* [1 << n_atoms] code of each valuation, or NULL    */
 } ltl4c_tables;
 
 /* A trace batch u (Def. 2) in encoded form, n_events events.
  * keys[i][j]  : value of guard key i (quantifier level i) in event j, or LTL4C_ABSENT;
  *               an event binding every key has value vector D = (keys[0][j] ...
  *               keys[n-1][j]) (epsilon; Eq. D); others bind no vector.
- * letters[j]  : bit k set iff atom k of the program holds in event j.
+ * letters[j]  : the letter code of event j: bit k set iff atom k of the program holds
+ *               (programs of <= 8 atoms), else the class of that valuation
+ *               (ltl4c_tables.letter_class).
  * first_index : global index of event 0; for an online state it must equal the
  *               previous batch's first_index + n_events (else LTL4C_E_INVALID).
  * Pointers are device pointers for ltl4c_verify and host pointers for
@@ -212,6 +223,12 @@ void ltl4c_state_free(ltl4c_state *st);
 ltl4c_status ltl4c_state_checkpoint_size(ltl4c_state *st, uint64_t *bytes);
 ltl4c_status ltl4c_state_checkpoint(ltl4c_state *st, void *buf, uint64_t cap, uint64_t *written);
 ltl4c_status ltl4c_state_restore(ltl4c_state *st, const void *buf, uint64_t len);
+
+/* Compaction of an ONLINE state's carried tables (NEXT-3): the tables are rehashed
+ * into the smallest power-of-two capacities that hold the live leaves and nodes
+ * at load <= 1/2 (they only ever grow while batches run); results are unchanged.
+ * Drains batches in flight.  Errors: E_INVALID (null or offline state), E_CUDA, E_OOM. */
+ltl4c_status ltl4c_state_compact(ltl4c_state *st);
 
 /* Explain / dump of an ONLINE state's carried tree (the
  * quantifier tree of §3.3, Fig. 2): the nodes of depth `level`

@@ -58,7 +58,8 @@ class _Tables(ctypes.Structure):
                 ("n_atoms", ctypes.c_uint32), ("n_states", ctypes.c_uint32),
                 ("initial", ctypes.c_uint32), ("delta", ctypes.POINTER(ctypes.c_uint8)),
                 ("label", ctypes.POINTER(ctypes.c_uint8)), ("quant", ctypes.POINTER(_Quant)),
-                ("atom_names", ctypes.POINTER(ctypes.c_char_p))]
+                ("atom_names", ctypes.POINTER(ctypes.c_char_p)), ("letter_bits", ctypes.c_uint32),
+                ("letter_class", ctypes.POINTER(ctypes.c_uint8))]
 
 
 class _Batch(ctypes.Structure):
@@ -104,6 +105,7 @@ _lib.ltl4c_dencode_jsonl.argtypes = [_P, ctypes.c_void_p, ctypes.c_uint64, ctype
 _lib.ltl4c_dencoder_values.argtypes = [_P, ctypes.c_uint32, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_dencoder_free.argtypes = [_P]
 _lib.ltl4c_dencoder_free.restype = None
+_lib.ltl4c_state_compact.argtypes = [_P]
 _lib.ltl4c_state_nodes.argtypes = [_P, ctypes.c_uint32, ctypes.c_uint32, ctypes.POINTER(ctypes.c_void_p),
                                    ctypes.c_void_p, ctypes.c_uint64, ctypes.POINTER(ctypes.c_uint64)]
 _lib.ltl4c_state_free.argtypes = [_P]
@@ -168,8 +170,12 @@ class Program:
         self.n_atoms = t.n_atoms
         self.n_states = t.n_states
         self.initial = t.initial
-        A = 1 << t.n_atoms
+        self.letter_bits = t.letter_bits
+        A = 1 << t.letter_bits
         self.delta = np.ctypeslib.as_array(t.delta, shape=(t.n_states * A,)).reshape(t.n_states, A).copy()
+        # letter code of each atom valuation (formula batches over > 8 atoms), or None
+        self.letter_class = (np.ctypeslib.as_array(t.letter_class, shape=(1 << t.n_atoms,)).copy()
+                             if bool(t.letter_class) else None)
         self.label = np.ctypeslib.as_array(t.label, shape=(t.n_formulas * t.n_states,)).reshape(
             t.n_formulas, t.n_states).copy()
         self.atoms = [t.atom_names[j].decode() for j in range(t.n_atoms)]
@@ -192,6 +198,14 @@ class Program:
 
     def state(self, device: int = 0, online: bool = False, capacity: int = 0) -> "State":
         return State(self, device, online, capacity)
+
+    def codes(self, valuations) -> np.ndarray:
+        """Letter codes of atom valuations (bit j = atom j): the valuations themselves up
+        to 8 atoms, their letter classes beyond (ltl4c_tables.letter_class)."""
+        v = np.asarray(valuations)
+        if self.letter_class is None:
+            return v.astype(np.uint8)
+        return self.letter_class[v.astype(np.int64)]
 
     def encoder(self) -> "Encoder":
         """Host trace encoder for this program's guard keys and atoms (ltl4c_encode_jsonl)."""
@@ -420,6 +434,10 @@ class State:
         w = ctypes.c_uint64()
         _check(_lib.ltl4c_state_checkpoint(self._h, buf, n.value, ctypes.byref(w)))
         return bytes(buf.raw[:w.value]) + self.next_index.to_bytes(8, "little")
+
+    def compact(self):
+        """Shrink an online state's carried tables to its live entries (ltl4c_state_compact)."""
+        _check(_lib.ltl4c_state_compact(self._h))
 
     def nodes(self, level: int, formula: int = 0):
         """(keys, verdicts) of every node at depth `level` of an online state's tree

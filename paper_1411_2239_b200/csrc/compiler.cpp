@@ -685,9 +685,9 @@ ltl4c_status compile_many(const char *const *texts, int nf, ltl4c_program **out)
           gbit[i].push_back(g);
         }
       }
-    if (prog->atom_names.size() > LTL4C_MAX_ATOMS) {
+    if (prog->atom_names.size() > LTL4C_MAX_BATCH_ATOMS) {
       delete prog;
-      return fail(LTL4C_E_BUDGET, "more than 8 atoms in the formula batch");
+      return fail(LTL4C_E_BUDGET, "more than 16 atoms in the formula batch");
     }
     prog->n_atoms = (uint32_t)prog->atom_names.size();
     const int A = 1 << prog->n_atoms;
@@ -730,8 +730,40 @@ ltl4c_status compile_many(const char *const *texts, int nf, ltl4c_program **out)
     }
     prog->n_states = (uint32_t)m.Q;
     prog->initial = (uint32_t)m.initial;
-    prog->delta.resize((size_t)m.Q * A);
-    for (size_t i = 0; i < prog->delta.size(); ++i) prog->delta[i] = (uint8_t)m.delta[i];
+    if (prog->n_atoms <= LTL4C_MAX_ATOMS) {
+      prog->letter_bits = prog->n_atoms;
+      prog->delta.resize((size_t)m.Q * A);
+      for (size_t i = 0; i < prog->delta.size(); ++i) prog->delta[i] = (uint8_t)m.delta[i];
+    } else {
+      // letter equivalence classes (NEXT-2): valuations whose columns of the minimised
+      // product's transition table are equal act identically on every state -- they
+      // are one letter to the monitor (lambda depends on the state only)
+      std::map<std::vector<int>, int> cls;
+      std::vector<std::vector<int>> cols;
+      prog->letter_class.resize(A);
+      for (int g = 0; g < A; ++g) {
+        std::vector<int> col(m.Q);
+        for (int q = 0; q < m.Q; ++q) col[q] = m.delta[(size_t)q * A + g];
+        auto it = cls.find(col);
+        if (it == cls.end()) {
+          if (cols.size() >= 256) {
+            delete prog;
+            return fail(LTL4C_E_BUDGET, "more than 256 letter classes in the formula batch");
+          }
+          it = cls.emplace(col, (int)cols.size()).first;
+          cols.push_back(col);
+        }
+        prog->letter_class[g] = (uint8_t)it->second;
+      }
+      int bits = 1;
+      while ((1u << bits) < cols.size()) ++bits;
+      prog->letter_bits = (uint32_t)bits;
+      const int C = 1 << bits;
+      prog->delta.resize((size_t)m.Q * C);
+      for (int q = 0; q < m.Q; ++q)
+        for (int c = 0; c < C; ++c)  // (codes past the classes repeat class 0: never produced)
+          prog->delta[(size_t)q * C + c] = (uint8_t)cols[c < (int)cols.size() ? c : 0][q];
+    }
     prog->label.resize((size_t)nf * m.Q);
     for (int i = 0; i < nf; ++i)
       for (int q = 0; q < m.Q; ++q) prog->label[i * m.Q + q] = sig_min[q][i];
@@ -780,6 +812,8 @@ extern "C" ltl4c_status ltl4c_program_tables(const ltl4c_program *prog, ltl4c_ta
   view->label = prog->label.data();
   view->quant = prog->quant.data();
   view->atom_names = prog->atom_ptrs.data();
+  view->letter_bits = prog->letter_bits;
+  view->letter_class = prog->letter_class.empty() ? nullptr : prog->letter_class.data();
   return LTL4C_OK;
 }
 

@@ -311,7 +311,7 @@ ltl4c_status ltl4c_encode_jsonl(ltl4c_encoder *enc, const char *text, uint64_t l
       }
       keys[l][n] = id;
     }
-    uint8_t let = 0;
+    uint32_t let = 0;  // the atom valuation; its letter code below
     for (size_t j = 0; j < enc->atoms.size(); ++j) {
       const auto &a = enc->atoms[j];
       const Val *v = find(a.pred);
@@ -329,9 +329,9 @@ ltl4c_status ltl4c_encode_jsonl(ltl4c_encoder *enc, const char *text, uint64_t l
           }
         }
       }
-      if (holds) let |= (uint8_t)(1u << j);
+      if (holds) let |= 1u << j;
     }
-    letters[n] = let;
+    letters[n] = enc->prog->letter_class.empty() ? (uint8_t)let : enc->prog->letter_class[let];
     ++n;
     p = nl ? nl + 1 : end;
   }

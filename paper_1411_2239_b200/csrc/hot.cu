@@ -41,7 +41,13 @@ namespace ltl4c {
 namespace {
 
 constexpr uint32_t kCntSalt = 0x165667b1u;   // sample-count table hash
-constexpr int kHotBatch = 16;                // rounds of 32 events whose loads are issued together
+#ifndef LTL4C_HOT_BATCH
+#define LTL4C_HOT_BATCH 16
+#endif
+#ifndef LTL4C_HOT_MINB
+#define LTL4C_HOT_MINB 4
+#endif
+constexpr int kHotBatch = LTL4C_HOT_BATCH;   // rounds of 32 events whose loads are issued together
 
 __device__ __forceinline__ uint32_t sel_of(uint32_t f) {  // bytes b0..b3 (< 8) -> nibbles b0 | b1 << 4 | ...
   const uint32_t x = f | (f >> 4);
@@ -107,15 +113,15 @@ __global__ void __launch_bounds__(256) hot_sample_kernel(HotParams hp) {
   for (int x = threadIdx.x; x < kSampleTab; x += blockDim.x) {
     const uint32_t k = tk[x];
     if (k == kAbsent) continue;
-    uint32_t h = fmix32(k ^ kCntSalt) & (kHotCountCap - 1);
-    for (int probes = 0; probes < kHotCountCap; ++probes) {
+    uint32_t h = fmix32(k ^ kCntSalt) & (hp.cnt_cap - 1);
+    for (uint32_t probes = 0; probes < hp.cnt_cap; ++probes) {
       uint32_t t = hp.cnt_key[h];
       if (t == kAbsent) {
         const uint32_t o = atomicCAS(&hp.cnt_key[h], kAbsent, k);
         t = o == kAbsent ? k : o;
       }
       if (t == k) { atomicAdd(&hp.cnt_val[h], tc[x]); break; }
-      h = (h + 1) & (kHotCountCap - 1);
+      h = (h + 1) & (hp.cnt_cap - 1);
     }
   }
 }
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(256) hot_sample_kernel(HotParams hp) {
 // histogram of the sample counts (bin 63 = 63 or more)
 __global__ void hot_count_hist_kernel(HotParams hp) {
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= (uint32_t)kHotCountCap) return;
+  if (s >= hp.cnt_cap) return;
   const uint32_t c = hp.cnt_val[s];
   if (c >= 1) atomicAdd(&hp.nhot[8 + min(c, 63u)], 1u);  // (bins 1, 2: the sample's singletons / doubletons)
 }
@@ -142,7 +148,7 @@ __global__ void hot_insert_kernel(HotParams hp, int pass) {
   }
   __syncthreads();
   const uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= (uint32_t)kHotCountCap || thr >= 64) return;
+  if (s >= hp.cnt_cap || thr >= 64) return;
   const uint32_t c = hp.cnt_val[s];
   if (pass == 0 ? c < 4 * thr : (c < thr || c >= 4 * thr)) return;
   const uint32_t k = hp.cnt_key[s];
@@ -190,7 +196,7 @@ struct HotSmem {
 
 // One warp per contiguous chunk [e0, e1) of the batch (multiple of 512 events).
 template <int MAPK>
-__global__ void __launch_bounds__(32 * kHotCtaWarps, 4) hot_compose_kernel(HotParams hp) {
+__global__ void __launch_bounds__(32 * kHotCtaWarps, LTL4C_HOT_MINB) hot_compose_kernel(HotParams hp) {
   using HM = HotMap<MAPK>;
   using M = typename HM::T;
   constexpr int S = HM::kSlots;
@@ -442,9 +448,9 @@ int hot_map_bytes(int mapk) { return mapk == 0 ? 1 : 8; }
 cudaError_t launch_hot_select(const HotParams &hp, const Launcher &L) {
   if (L.before) L.before(L.ctx, kKHot);
   hot_sample_kernel<<<(hp.n_samples + kSampleBlock - 1) / kSampleBlock, 256, 0, L.stream>>>(hp);
-  hot_count_hist_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp);
-  hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 0);
-  hot_insert_kernel<<<kHotCountCap / 256, 256, 0, L.stream>>>(hp, 1);
+  hot_count_hist_kernel<<<(hp.cnt_cap + 255) / 256, 256, 0, L.stream>>>(hp);
+  hot_insert_kernel<<<(hp.cnt_cap + 255) / 256, 256, 0, L.stream>>>(hp, 0);
+  hot_insert_kernel<<<(hp.cnt_cap + 255) / 256, 256, 0, L.stream>>>(hp, 1);
   hot_decide_kernel<<<1, 32, 0, L.stream>>>(hp);
   cudaError_t e = cudaGetLastError();
   if (L.after) L.after(L.ctx, kKHot);

@@ -40,7 +40,8 @@
 namespace ltl4c {
 
 constexpr int kSegBytes = 1 << 16;       // bytes per ingest segment (256 threads x 256 B)
-constexpr int kMaxNames = kMaxLevels + 8;
+constexpr int kMaxAtomsB = LTL4C_MAX_BATCH_ATOMS;
+constexpr int kMaxNames = kMaxLevels + kMaxAtomsB;
 
 struct IngestParams {
   const char *text;
@@ -52,8 +53,9 @@ struct IngestParams {
   const unsigned long long *d_n_lines;  // (device)
   int K, A;
   unsigned long long name_hash[kMaxNames];  // K guard keys, then A atom predicates
-  int atom_nargs[8];
-  int atom_lv[8][kMaxLevels];
+  int atom_nargs[kMaxAtomsB];
+  int atom_lv[kMaxAtomsB][kMaxLevels];
+  const uint8_t *letter_class;               // [1 << A] letter code of each valuation, or null (code = valuation)
   unsigned long long *dict_key[kMaxLevels];  // per level: 64-bit value hash (0 = empty)
   uint32_t *dict_id[kMaxLevels];             // dense id (ABSENT until published)
   unsigned long long dict_cap;               // power of two
@@ -411,7 +413,7 @@ __global__ void __launch_bounds__(128) ingest_parse_kernel(IngestParams p) {
     uint32_t ok = 0;
     if (c.p < c.end) {  // (blank lines are no event)
       Val guard[kMaxLevels];
-      Val atom[8];
+      Val atom[kMaxAtomsB];
       bool good = c.peek() == '{';
       if (good) {
         ++c.p;
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(128) ingest_parse_kernel(IngestParams p) {
           }
           if (holds) let |= 1u << j;
         }
-        p.tmp_let[ln] = (uint8_t)let;
+        p.tmp_let[ln] = p.letter_class ? p.letter_class[let] : (uint8_t)let;
       }
     }
     p.valid[ln] = ok;
@@ -537,11 +539,17 @@ cudaError_t ingest_create(DevIngest *e, const ltl4c_program *prog, int device, u
     b.atom_nargs[j] = (int)lv.size();
     for (size_t i = 0; i < lv.size() && i < (size_t)kMaxLevels; ++i) b.atom_lv[j][i] = lv[i];
   }
+  cudaError_t r;
+  if (!prog->letter_class.empty()) {
+    uint8_t *lc = nullptr;
+    if ((r = cudaMalloc((void **)&lc, prog->letter_class.size()))) return r;
+    if ((r = cudaMemcpy(lc, prog->letter_class.data(), prog->letter_class.size(), cudaMemcpyHostToDevice))) return r;
+    b.letter_class = lc;
+  }
   unsigned long long cap = 1024;
   while (cap < 2 * max_values + 1) cap <<= 1;
   e->dict_cap = cap;
   b.dict_cap = cap;
-  cudaError_t r;
   for (int l = 0; l < b.K; ++l) {
     if ((r = cudaMalloc((void **)&b.dict_key[l], sizeof(unsigned long long) * cap))) return r;
     if ((r = cudaMalloc((void **)&b.dict_id[l], sizeof(uint32_t) * cap))) return r;
@@ -560,6 +568,7 @@ void ingest_free(DevIngest *e) {
     cudaFree(e->base.dict_id[l]);
   }
   cudaFree(e->base.dict_count);
+  cudaFree(const_cast<uint8_t *>(e->base.letter_class));
   cudaFree(e->small);
   cudaFree(e->scratch);
 }

@@ -62,9 +62,12 @@ __device__ __forceinline__ bool pass_skipped(const PartPlan &pl, int pass) { ret
 
 // Heavy hitters of single-level properties (hot.cu): the most frequent keys are
 // composed in trace order where they lie; only the other events are partitioned.
-constexpr int kHotSlotsMax = 4096;     // hot-table slots (2-way buckets) for 1-byte maps; 1024 for 8-byte maps
+#ifndef LTL4C_HOT_SLOTS
+#define LTL4C_HOT_SLOTS 4096
+#endif
+constexpr int kHotSlotsMax = LTL4C_HOT_SLOTS;  // hot-table slots (2-way buckets) for 1-byte maps; / 4 for 8-byte maps
 constexpr int kHotSamplesMax = 1 << 19; // evenly spaced sample of the batch
-constexpr int kHotCountCap = 1 << 20;  // sample-count table slots
+constexpr int kHotCountCap = 1 << 20;  // sample-count table slots (at most; 2 x the samples, rounded up)
 constexpr int kHotMinCount = 4;        // a hot key was sampled at least this often
 constexpr int kHotCtaWarps = 8;
 constexpr double kOnePassKeys = 768.0 * 1024;  // cold keys (Chao1 estimate) for the one-pass mode
@@ -76,7 +79,8 @@ struct HotParams {
   int mapk;                             // 0: 2-bit packed maps (nq <= 4, <= 16 letters); 1: byte maps (nq <= 8)
   int slots;                            // hot-table slots (hot_slots(mapk))
   uint32_t let_mask;
-  uint32_t *cnt_key, *cnt_val;          // [kHotCountCap] sample counts (key = ABSENT: empty)
+  uint32_t *cnt_key, *cnt_val;          // [cnt_cap] sample counts (key = ABSENT: empty)
+  uint32_t cnt_cap;                     // power of two >= 2 x n_samples
   uint32_t *slot_key;                   // [slots] hot key of each slot (ABSENT: empty) = dense id
   uint32_t *nhot;                       // [0] hot keys, [1] their samples, [2] dense, [3] one pass; [8 + c] keys sampled c times
   void *partial;                        // [n_chunks][slots] per-warp-chunk maps

@@ -8,7 +8,9 @@
 
 struct ltl4c_program {
   uint32_t n_formulas = 0, n_levels = 0, n_atoms = 0, n_states = 0, initial = 0;
-  std::vector<uint8_t> delta;             // [n_states][1 << n_atoms]
+  uint32_t letter_bits = 0;               // codes < 1 << letter_bits (= n_atoms up to 8 atoms)
+  std::vector<uint8_t> letter_class;      // [1 << n_atoms] code of each valuation (> 8 atoms), else empty
+  std::vector<uint8_t> delta;             // [n_states][1 << letter_bits]
   std::vector<uint8_t> label;             // [n_formulas][n_states], B6 codes {0,2,3,5}
   std::vector<ltl4c_quantifier> quant;    // [n_formulas][n_levels]
   std::vector<std::string> atom_names;    // [n_atoms]

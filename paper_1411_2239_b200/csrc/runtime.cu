@@ -472,7 +472,7 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->large_list.ensure(pl->NB));
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
   if (K == 1) CU(st->unit_start2.ensure(N / st->seg_unit + 4));
-  if (K == 1) CU(st->coarse_off.ensure((1u << kCoarseBits) + 1));
+  if (K == 1) CU(st->coarse_off.ensure(2 * ((1u << kCoarseBits) + 1)));  // offsets | order
   if (use_hot(st)) {
     const uint64_t nch = (N + hot_chunk_ev(st, N) - 1) / hot_chunk_ev(st, N);
     CU(st->hot_cnt.ensure(2 * (size_t)kHotCountCap));
@@ -503,7 +503,7 @@ BucketParams bucket_params(ltl4c_state *st, const Plan &pl) {
   bp.medium_list = st->medium_list.p;
   bp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 8;
   bp.warps_per_cta = st->warp_cfg[0];
-  bp.warp_hdr = bucket_warp_hdr((int)st->prog->n_states, (int)st->prog->n_atoms);
+  bp.warp_hdr = bucket_warp_hdr((int)st->prog->n_states, (int)st->prog->letter_bits);
   bp.spill_list = st->medium_list.p;
   bp.spill_len = &st->d_acc.p->medium_buckets;
   bp.unit_start = st->unit_start.p;
@@ -524,6 +524,7 @@ BucketParams coarse_params(ltl4c_state *st, const Plan &pl, const BucketParams &
   cp.bucket_off = st->coarse_off.p;
   cp.n_buckets = 1u << width;
   cp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 10;
+  cp.list = st->coarse_off.p + (1u << kCoarseBits) + 1;  // the buckets, largest first (coarse_order)
   return cp;
 }
 
@@ -566,7 +567,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.hcol[0] = pl.buf_key[0][pl.hk];
     pl.hcol[1] = pl.buf_key[1][pl.hk];
     pl.rank_ballot = st->rank_ballot;
-    pl.let_mask = (1u << prog->n_atoms) - 1u;
+    pl.let_mask = (1u << prog->letter_bits) - 1u;
     pl.passes = plan.P;
     int lo = 0;
     for (int pass = 0; pass < plan.P; ++pass) {
@@ -589,6 +590,8 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       hp.let = letters;
       hp.n = plan.N;
       hp.n_samples = (uint32_t)std::min<uint64_t>(plan.N, kHotSamplesMax);
+      hp.cnt_cap = 4096;
+      while (hp.cnt_cap < 2 * hp.n_samples && hp.cnt_cap < (uint32_t)kHotCountCap) hp.cnt_cap <<= 1;
       hp.mapk = st->hot_mapk;
       hp.slots = S;
       hp.let_mask = pl.let_mask;
@@ -609,8 +612,8 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       hp.force_onepass = st->force_onepass;
       hp.prog = st->d_prog.p;
       hp.acc = st->d_acc.p;
-      CU(cudaMemsetAsync(hp.cnt_key, 0xFF, sizeof(uint32_t) * kHotCountCap, s));
-      CU(cudaMemsetAsync(hp.cnt_val, 0, sizeof(uint32_t) * kHotCountCap, s));
+      CU(cudaMemsetAsync(hp.cnt_key, 0xFF, sizeof(uint32_t) * hp.cnt_cap, s));
+      CU(cudaMemsetAsync(hp.cnt_val, 0, sizeof(uint32_t) * hp.cnt_cap, s));
       CU(cudaMemsetAsync(hp.slot_key, 0xFF, sizeof(uint32_t) * S, s));
       CU(cudaMemsetAsync(hp.nhot, 0, sizeof(uint32_t) * 72, s));
       CU(cudaMemsetAsync(hp.n_cold, 0, sizeof(unsigned long long), s));
@@ -737,7 +740,7 @@ ltl4c_status owner_partition(ltl4c_state *st, const uint32_t *const *keys, const
   pl.hcol[0] = okey[0];
   pl.hcol[1] = okey[0];
   pl.rank_ballot = st->rank_ballot;
-  pl.let_mask = (1u << st->prog->n_atoms) - 1u;
+  pl.let_mask = (1u << st->prog->letter_bits) - 1u;
   pl.lo[0] = 0;
   pl.width[0] = bits;
   pl.digit_hist = st->totals.p;
@@ -1151,10 +1154,10 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
   DevProg &h = st->hprog;
   h.nf = prog->n_formulas;
   h.nl = prog->n_levels;
-  h.na = prog->n_atoms;
+  h.na = prog->letter_bits;
   h.nq = prog->n_states;
   h.q0 = prog->initial;
-  const int A = 1 << prog->n_atoms;
+  const int A = 1 << prog->letter_bits;
   for (uint32_t q = 0; q < prog->n_states; ++q)
     for (int a = 0; a < A; ++a) h.delta[q][a] = prog->delta[q * A + a];
   for (int a = 0; a < A; ++a) {
@@ -1198,13 +1201,13 @@ ltl4c_status ltl4c_state_create(const ltl4c_program *prog, int device, uint64_t 
     // warp-per-unit kernel: the (warps per CTA, CTAs per SM) pair that keeps the
     // most warps resident for this program's (K, F) shared-memory plan
     cudaError_t e = bucket_warp_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states,
-                                       (int)prog->n_atoms, st->warp_cfg);
+                                       (int)prog->letter_bits, st->warp_cfg);
     if (e == cudaSuccess)
-      e = online_leaf_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states, (int)prog->n_atoms,
+      e = online_leaf_config((int)prog->n_levels, (int)prog->n_formulas, (int)prog->n_states, (int)prog->letter_bits,
                              st->online_cfg);
     if (e != cudaSuccess) return cleanup(fail(LTL4C_E_CUDA, std::string("bucket_warp_config: ") + cudaGetErrorString(e)));
     if (prog->n_levels == 1) {
-      st->hot_mapk = prog->n_states <= 4 && prog->n_atoms <= 4 ? 0 : prog->n_states <= 8 ? 1 : -1;
+      st->hot_mapk = prog->n_states <= 4 && prog->letter_bits <= 4 ? 0 : prog->n_states <= 8 ? 1 : -1;
       if (st->hot_mapk >= 0) st->hot_per_sm = hot_ctas_per_sm(st->hot_mapk);
       st->seg_per_sm = bucket_seg_ctas_per_sm((int)prog->n_states);
       if (st->hot_mapk == 0) st->coarse_per_sm = bucket_coarse_ctas_per_sm();
@@ -1491,6 +1494,46 @@ ltl4c_status ltl4c_state_restore(ltl4c_state *st, const void *buf, uint64_t len)
   st->enq_events = st->known_cum = 0;
   st->poisoned = false;
   std::memset(st->h_out, 0, sizeof(DevOut));
+  cudaSetDevice(prev);
+  return LTL4C_OK;
+}
+
+ltl4c_status ltl4c_state_compact(ltl4c_state *st) {
+  if (!st) return fail(LTL4C_E_INVALID, "null state");
+  if (!(st->flags & LTL4C_STATE_ONLINE)) return fail(LTL4C_E_INVALID, "compact of an offline state");
+  if (st->tab.d.leaf_cap == 0) return LTL4C_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  CU(cudaSetDevice(st->device));
+  if (ltl4c_status r = drain(st)) return r;
+  for (int i = 0; i < ltl4c_state::kRing; ++i) st->ring_ticket[i] = 0;
+  st->outstanding = 0;
+  unsigned long long cnt[1 + kMaxLevels];
+  CU(cudaMemcpy(cnt, &st->d_acc.p->leaves, sizeof cnt, cudaMemcpyDeviceToHost));
+  st->known_leaves = cnt[0];
+  uint64_t nodes = 0;
+  for (int l = 0; l < kMaxLevels; ++l) {
+    st->known_nodes[l] = cnt[1 + l];
+    if (l >= 1 && l < (int)st->prog->n_levels) nodes = std::max<uint64_t>(nodes, cnt[1 + l]);
+  }
+  st->known_cum = st->enq_events = 0;
+  // the smallest power-of-two capacities holding the live entries at load <= 1/2
+  const uint64_t want_leaf = 1ull << std::max(12, ceil_log2(2 * st->known_leaves + 1));
+  const uint64_t want_node = 1ull << std::max(12, ceil_log2(2 * nodes + 1));
+  const bool smaller = want_leaf < st->tab.d.leaf_cap ||
+                       (st->prog->n_levels > 1 && want_node < st->tab.d.node_cap[1]);
+  if (smaller) {
+    Tables nt;
+    Launcher L{0, nullptr, nullptr, nullptr};
+    if (ltl4c_status r = alloc_tables(st, nt, want_leaf, want_node, 0, false, true)) return r;
+    nt.d.epoch = st->tab.d.epoch;
+    CU(launch_rehash(st->tab.d, nt.d, (int)st->prog->n_levels, (int)st->prog->n_formulas,
+                     &st->d_acc.p->table_overflow, L));
+    CU(cudaDeviceSynchronize());
+    st->tab.release();
+    st->tab = nt;
+    nt = Tables{};
+  }
   cudaSetDevice(prev);
   return LTL4C_OK;
 }

@@ -30,7 +30,10 @@ namespace {
 constexpr int kSegWarps = 8;
 constexpr int kSegSlots = 512;          // table slots per warp (claims <= kSegSlots / 2)
 constexpr uint32_t kSegMax = 1u << 14;  // buckets above this many events: heavy path (parallel segments)
-constexpr int kSegRounds = 8;           // rounds of 32 events whose loads are issued together
+#ifndef LTL4C_SEG_ROUNDS
+#define LTL4C_SEG_ROUNDS 8
+#endif
+constexpr int kSegRounds = LTL4C_SEG_ROUNDS;  // rounds of 32 events whose loads are issued together
 constexpr uint32_t kSegSalt = 0x27d4eb2fu;
 
 __device__ __forceinline__ uint32_t sel_of(uint32_t f) {  // bytes b0..b3 (< 8) -> nibbles
@@ -349,8 +352,8 @@ __global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(Buc
       s.ovf = 0;
     }
     __syncthreads();
-    const uint32_t c = s.item;
-    if (c >= p.n_buckets) break;
+    if (s.item >= p.n_buckets) break;
+    const uint32_t c = p.list ? p.list[s.item] : s.item;  // (largest buckets first)
     const uint32_t s0 = p.bucket_off[c], s1 = p.bucket_off[c + 1];
     if (s1 == s0) continue;
     ++ep;
@@ -470,6 +473,29 @@ __global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(Buc
     if (s.sacc[i]) atomicAdd(&p.acc->hist[i / 6][1][i % 6], (unsigned long long)s.sacc[i]);
 }
 
+// the coarse buckets in decreasing size (one CTA, bitonic sort of (size, id)): CTAs
+// take the largest first, so the last wave holds the small ones
+__global__ void __launch_bounds__(1024) coarse_order_kernel(const uint32_t *off, uint32_t nb, uint32_t *order,
+                                                            const uint32_t *gate) {
+  __shared__ unsigned long long v[1024];
+  if (gate && *gate == 0) return;
+  const uint32_t t = threadIdx.x;
+  // key: larger size first, then smaller id (ascending sort of ~size << 32 | id)
+  v[t] = t < nb ? ((unsigned long long)(~(off[t + 1] - off[t])) << 32 | t) : ~0ull;
+  __syncthreads();
+  for (uint32_t k = 2; k <= 1024; k <<= 1)
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      const uint32_t x = t ^ j;
+      if (x > t) {
+        const bool up = (t & k) == 0;
+        const unsigned long long a = v[t], b = v[x];
+        if ((a > b) == up) { v[t] = b; v[x] = a; }
+      }
+      __syncthreads();
+    }
+  if (t < nb) order[t] = (uint32_t)v[t];
+}
+
 template <int NQB, int NF>
 size_t seg_smem() {
   using M = typename SegMap<NQB>::T;
@@ -532,6 +558,11 @@ static cudaError_t coarse_launch(const BucketParams &p, uint32_t grid, const Lau
 }
 
 cudaError_t launch_bucket_coarse(const BucketParams &p, int nf, uint32_t grid, const Launcher &L) {
+  if (p.list) {
+    if (L.before) L.before(L.ctx, kKBucketWarp);
+    coarse_order_kernel<<<1, 1024, 0, L.stream>>>(p.bucket_off, p.n_buckets, const_cast<uint32_t *>(p.list), p.gate);
+    if (L.after) L.after(L.ctx, kKBucketWarp);
+  }
   switch (nf) {
     case 1: return coarse_launch<1>(p, grid, L);
     case 2: return coarse_launch<2>(p, grid, L);

@@ -7,7 +7,7 @@ for spec in $SPECS; do
   v=${spec%%:*}; e=""; [[ "$spec" == *:* ]] && e=${spec#*:}
   lib=""; [ "$v" != "base" ] && lib="LTL4C_LIB_VARIANT=$v"
   echo "== $spec" >> gpurun_out/sweep.log
-  env $lib ${e//,/ } timeout 300 python bench.py --no-cpu-baseline --config ${CFG:-C2} --steps 10 >> gpurun_out/sweep.log 2>&1
+  env $lib ${e//,/ } timeout 300 python bench.py --no-cpu-baseline --no-extra --config ${CFG:-C2} --steps 10 >> gpurun_out/sweep.log 2>&1
 done
 python - <<"PY"
 import json

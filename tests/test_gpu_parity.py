@@ -159,8 +159,10 @@ def test_checkpoint_restore_continues_the_stream(env):
     c = prog.state(0, online=True)
     feed(c, 0, 900, False)             # c verified another prefix first: restore replaces it
     c.restore(blob)
+    a_results = {}
     for lo, hi in zip(cuts[3:-1], cuts[4:]):
         gb = feed(b, lo, hi, True)
+        a_results[hi] = (gb[0].verdict, gb[0].hist.copy())
         for st in (a, c):
             g = feed(st, lo, hi, False)
             for f in range(len(props)):
@@ -168,6 +170,16 @@ def test_checkpoint_restore_continues_the_stream(env):
     other = ltl4c.compile(tracegen.LOGIN).state(0, online=True)
     with pytest.raises(ltl4c.Ltl4cError):
         other.restore(blob)
+    # compaction (NEXT-3): the carried tables shrink to the live entries and the stream
+    # continues exactly
+    d = prog.state(0, online=True)
+    d.restore(blob)
+    before = len(d.checkpoint())
+    d.compact()
+    assert len(d.checkpoint()) < before
+    for lo, hi in zip(cuts[3:-1], cuts[4:]):
+        g = feed(d, lo, hi, False)
+        assert g[0].verdict == a_results[hi][0] and np.array_equal(g[0].hist, a_results[hi][1])
 
 
 def test_node_dump_explains_the_counts(env):
