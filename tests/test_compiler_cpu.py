@@ -107,6 +107,51 @@ def test_formula_batch_product_projects_to_each_formula():
             assert got[f] == p.ltl4(lw)
 
 
+WIDE = ["forall[>=0.5] x : k(x) => exists[<=2] y : j(y) => ((a1 && a2 && !a3) || (a4 && a5))",
+        "exists[>=1] x : k(x) => forall y : j(y) => F (b1 && b2 && b3 && !b4 && b5)",
+        "forall x : k(x) => exists y : j(y) => G (c1 || c2)"]
+
+
+def test_batch_over_more_than_8_atoms_letter_classes():
+    """a formula batch over 12 atoms; the batch carries letter
+    CODES (ltl4c_tables.letter_class), valuations of one class acting identically.
+    Pinned against the oracle's Def. 4 of each formula on the projected valuations
+    (every word up to length 3 over a sample of valuations, and random longer words)."""
+    prog = ltl4c.compile_batch(WIDE)
+    assert prog.n_atoms == 12 and prog.letter_class is not None
+    assert prog.letter_class.shape == (1 << 12,) and int(prog.letter_class.max()) < (1 << prog.letter_bits) <= 256
+    props = [oracle.Property(t) for t in WIDE]
+    gidx = [[prog.atoms.index(a) for a in p.atoms] for p in props]
+    rng = np.random.default_rng(12)
+    vals = [int(x) for x in rng.integers(0, 1 << 12, size=12)] + [0, (1 << 12) - 1, 0b11011]
+
+    def check(w):
+        got = run_word(prog, [int(c) for c in prog.codes(np.array(w))])
+        for f, p in enumerate(props):
+            lw = [sum(((a >> g) & 1) << j for j, g in enumerate(gidx[f])) for a in w]
+            assert got[f] == p.ltl4(lw), (w, f)
+
+    for L in range(1, 4):
+        for w in itertools.product(vals, repeat=L):
+            check(list(w))
+    for _ in range(300):
+        check([int(x) for x in rng.integers(0, 1 << 12, size=rng.integers(1, 8))])
+    # the classes are exactly the valuations with equal transition columns
+    cols = {}
+    for v in range(1 << 12):
+        col = tuple(prog.delta[:, prog.letter_class[v]])
+        cols.setdefault(prog.letter_class[v], col)
+        assert cols[prog.letter_class[v]] == col
+    assert len(set(cols.values())) == len(cols)
+    # budgets: a single formula keeps <= 8 atoms, a batch <= 16
+    with pytest.raises(ltl4c.Ltl4cError):
+        ltl4c.compile("forall x : k(x) => F (" + " && ".join(f"p{i}" for i in range(9)) + ")")
+    with pytest.raises(ltl4c.Ltl4cError, match="16 atoms"):
+        ltl4c.compile_batch(["forall x : k(x) => F (" + " && ".join(f"p{i}" for i in range(8)) + ")",
+                             "forall x : k(x) => G (" + " || ".join(f"q{i}" for i in range(8)) + ")",
+                             "forall x : k(x) => F r0"])
+
+
 def test_batch_requires_same_keys():
     with pytest.raises(ltl4c.Ltl4cError) as e:
         ltl4c.compile_batch([tracegen.SOCKET, tracegen.LOGIN])

@@ -560,6 +560,64 @@ def test_records_through_encoder_and_gpu(env):
         _assert_same(got, mon.evaluate(), ("online records", lo))
 
 
+WIDE = ["forall[>=0.5] x : k(x) => exists[<=2] y : j(y) => ((a1 && a2 && !a3) || (a4 && a5))",
+        "exists[>=1] x : k(x) => forall y : j(y) => F (b1 && b2 && b3 && !b4 && b5)",
+        "forall x : k(x) => exists y : j(y) => G (c1 || c2)"]
+
+
+def test_batch_over_more_than_8_atoms(env):
+    """a formula batch over 12 atoms -- events carry letter
+    codes (classes of atom valuations, ltl4c_tables.letter_class); offline and online
+    results of every formula equal the oracle on that formula's projected valuations;
+    the host encoder emits the codes."""
+    ltl4c, torch, dev = env
+    prog = ltl4c.compile_batch(WIDE)
+    assert prog.n_atoms == 12 and prog.letter_class is not None
+    g = np.random.default_rng(121)
+    n = 400_000
+    keys = [g.integers(0, 3000, n).astype(np.uint32), g.integers(0, 40_000, n).astype(np.uint32)]
+    keys[1][g.random(n) < 0.01] = 0xFFFFFFFF
+    # valuations: each atom set with its own probability (so every formula sees both outcomes)
+    pa = g.uniform(0.2, 0.95, 12)
+    vals = np.zeros(n, np.uint32)
+    for j in range(12):
+        vals |= (g.random(n) < pa[j]).astype(np.uint32) << j
+    codes = prog.codes(vals)
+    props = [oracle.Property(t) for t in WIDE]
+    gidx = [[prog.atoms.index(a) for a in p.atoms] for p in props]
+
+    def proj(v, f):
+        out = np.zeros(v.shape[0], np.uint8)
+        for j, gg in enumerate(gidx[f]):
+            out |= (((v >> gg) & 1) << j).astype(np.uint8)
+        return out
+
+    k, l = _dev(torch, dev, keys, codes)
+    got = prog.state(0).verify(k, l)
+    for f, t in enumerate(WIDE):
+        _assert_same(got[f], oracle.run_offline(t, keys, proj(vals, f)), ("wide offline", f))
+    st = prog.state(0, online=True)
+    for lo, hi in [(0, 1000), (1000, 150_000), (150_000, n)]:
+        k, l = _dev(torch, dev, [x[lo:hi] for x in keys], codes[lo:hi])
+        got = st.verify(k, l, first_index=lo)
+        for f, t in enumerate(WIDE):
+            _assert_same(got[f], oracle.run_offline(t, [x[:hi] for x in keys], proj(vals[:hi], f)), ("wide online", f, hi))
+    # records: the encoders turn the 12 atoms of a record into the code
+    import json as _json
+    recs = []
+    for j in range(2000):
+        r = {"k": int(keys[0][j]), "j": int(keys[1][j])} if keys[1][j] != 0xFFFFFFFF else {"k": int(keys[0][j])}
+        for a in range(12):
+            if (vals[j] >> a) & 1:
+                r[prog.atoms[a]] = True
+        recs.append(_json.dumps(r))
+    text = "\n".join(recs) + "\n"
+    hk, hl = prog.encoder().encode(text)
+    assert np.array_equal(hl, codes[:2000])
+    dk, dl = prog.device_encoder().encode(text)
+    assert np.array_equal(dl.cpu().numpy(), codes[:2000])
+
+
 def _same_partition(a, b):
     """a and b label the same events with a bijection of ids (equal partitions)."""
     a, b = np.asarray(a, np.int64), np.asarray(b, np.int64)
