@@ -48,9 +48,6 @@ constexpr uint32_t kCntSalt = 0x165667b1u;   // sample-count table hash
 #ifndef LTL4C_HOT_MINB
 #define LTL4C_HOT_MINB 4
 #endif
-#ifndef LTL4C_HOT_ALUFOLD
-#define LTL4C_HOT_ALUFOLD 0
-#endif
 constexpr int kHotBatch = LTL4C_HOT_BATCH;   // rounds of 32 events whose loads are issued together
 
 __device__ __forceinline__ uint32_t sel_of(uint32_t f) {  // bytes b0..b3 (< 8) -> nibbles b0 | b1 << 4 | ...
@@ -236,20 +233,6 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, LTL4C_HOT_MINB) hot_compose
   }
   for (int i = lane; i < S; i += 32) s.wmap[wid][i] = HM::ident();
   __syncthreads();
-#if LTL4C_HOT_ALUFOLD
-  // byte-form letter maps of letters 0..3 (MAPK 0: images < 4)
-  uint32_t lmap0 = 0x03020100u, lmap1 = 0x03020100u, lmap2 = 0x03020100u, lmap3 = 0x03020100u;
-  if (MAPK == 0 && A <= 4) {
-    auto bm = [&](int a) {
-      uint32_t o = 0;
-      for (int q = 0; q < 4; ++q) o |= (uint32_t)(q < nq ? prog->delta[q][a] & 3u : q) << (8 * q);
-      return o;
-    };
-    lmap0 = bm(0);
-    if (A > 1) lmap1 = bm(1);
-    if (A > 2) { lmap2 = bm(2); lmap3 = bm(3); }
-  }
-#endif
   const bool dense = hp.nhot[2] != 0;  // not dense: nothing composed, the partition reads the batch itself
   const uint32_t chunk = blockIdx.x * kHotCtaWarps + wid;
   const unsigned long long n = hp.n;
@@ -296,30 +279,6 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, LTL4C_HOT_MINB) hot_compose
         ncold += __popc(cm);
         const uint32_t hm = __ballot_sync(0xffffffffu, slot >= 0);
         nhot += __popc(hm);
-#if LTL4C_HOT_ALUFOLD
-        if (MAPK == 0 && A <= 4 && hm) {
-          // letters of <= 2 bits read from two warp-uniform ballots; the group's letters
-          // composed in registers (byte-form maps, PRMT), then applied to the slot's map
-          const uint32_t L0 = __ballot_sync(0xffffffffu, ll[r] & 1u), L1 = __ballot_sync(0xffffffffu, ll[r] & 2u);
-          if (slot >= 0) {
-            const uint32_t peers = __match_any_sync(hm, (uint32_t)slot);
-            if ((peers & lanemask_lt()) == 0) {
-              uint32_t g = 0x03020100u, pm = peers;
-              do {
-                const int i = __ffs(pm) - 1;
-                pm &= pm - 1;
-                const uint32_t a = ((L0 >> i) & 1u) | (((L1 >> i) & 1u) << 1);
-                const uint32_t lm = a == 0 ? lmap0 : a == 1 ? lmap1 : a == 2 ? lmap2 : lmap3;
-                g = byte_apply(lm, g);
-              } while (pm);
-              const uint32_t m = wmap[slot];
-              uint32_t mb = (m & 3u) | ((m & 0xCu) << 6) | ((m & 0x30u) << 12) | ((m & 0xC0u) << 18);
-              mb = byte_apply(g, mb);
-              wmap[slot] = (M)((mb & 3u) | ((mb >> 6) & 0xCu) | ((mb >> 12) & 0x30u) | ((mb >> 18) & 0xC0u));
-            }
-          }
-        } else
-#endif
         if (hm) {
           stage[lane] = ll[r];
           __syncwarp();
