@@ -67,7 +67,7 @@ __device__ __forceinline__ bool pass_skipped(const PartPlan &pl, int pass) { ret
 #endif
 constexpr int kHotSlotsMax = LTL4C_HOT_SLOTS;  // hot-table slots (2-way buckets) for 1-byte maps; / 4 for 8-byte maps
 #ifndef LTL4C_HOT_SAMPLES
-#define LTL4C_HOT_SAMPLES (1 << 19)
+#define LTL4C_HOT_SAMPLES (1 << 18)
 #endif
 constexpr int kHotSamplesMax = LTL4C_HOT_SAMPLES;  // evenly spaced sample of the batch
 constexpr int kHotCountCap = 1 << 20;  // sample-count table slots (at most; 2 x the samples, rounded up)

@@ -214,3 +214,28 @@ def test_K1_one_pass_mode_and_coarse_overflow(env):
                 if env_var:
                     os.environ.pop(env_var, None)
             _same(got, want, (tr.formula, env_var))
+
+
+def test_C6_full_size_bench_trace(env):
+    """C6 as bench.py --config C6 runs it: 10M events, 10^5 users (seed 0)."""
+    tr = tracegen.dropbox_trace(seed=0, n=10_000_000, users=100_000)
+    got = _verify(env, tr.formula, tr.keys, tr.letters)[0]
+    _same(got, oracle.run_offline(tr.formula, tr.keys, tr.letters, threads=NPROC), "C6 10M")
+
+
+def test_device_ingest_at_bench_size(env):
+    """The records bench.py's extra.ingest encodes (2M C2-shaped records, mixed spellings):
+    device encoder == host encoder up to relabelling, and the verdict equals the oracle's."""
+    ltl4c, torch, dev = env
+    tr = tracegen.login_trace(seed=0, n=2_000_000, users=20_000, rid_events=2)
+    text = tracegen.to_jsonl(tr, ["user", "rid"], ["login", "unauthorized"], [[], []], seed=0, style="mixed")
+    prog = ltl4c.compile(tr.formula)
+    hk, hl = prog.encoder().encode(text)
+    dk, dl = prog.device_encoder(max_values=1 << 21).encode(text)
+    assert np.array_equal(dl.cpu().numpy(), hl)
+    for a, b in zip(hk, dk):
+        b = b.cpu().numpy().view(np.uint32)
+        pairs = np.unique(np.stack([a.astype(np.int64), b.astype(np.int64)]), axis=1)
+        assert np.unique(pairs[0]).shape[0] == pairs.shape[1] == np.unique(pairs[1]).shape[0]
+    got = prog.state(0).verify(dk, dl)[0]
+    _same(got, oracle.run_offline(tr.formula, hk, hl, threads=NPROC), "ingest 2M")
