@@ -86,18 +86,24 @@ template <> struct HotMap<1> {
 };
 
 // a CTA aggregates its kSampleBlock samples in a shared-memory table first, so a
-// hot key costs one global atomic per CTA (not one per sample)
-constexpr int kSampleBlock = 2048, kSampleTab = 4096;
-__global__ void __launch_bounds__(256) hot_sample_kernel(HotParams hp) {
+// hot key costs one global atomic per CTA (not one per sample); a thread's
+// samples are loaded together
+constexpr int kSampleThreads = 256, kSamplePer = 2;
+constexpr int kSampleBlock = kSampleThreads * kSamplePer, kSampleTab = 2 * kSampleBlock;
+__global__ void __launch_bounds__(kSampleThreads) hot_sample_kernel(HotParams hp) {
   __shared__ uint32_t tk[kSampleTab], tc[kSampleTab];
   for (int i = threadIdx.x; i < kSampleTab; i += blockDim.x) { tk[i] = kAbsent; tc[i] = 0; }
-  __syncthreads();
   const unsigned long long n = hp.n;
-  for (int x = threadIdx.x; x < kSampleBlock; x += blockDim.x) {
-    const uint32_t i = blockIdx.x * kSampleBlock + x;
-    if (i >= hp.n_samples) break;
-    const unsigned long long j = (unsigned long long)i * n / (unsigned long long)hp.n_samples;
-    const uint32_t k = hp.k0[j];
+  uint32_t kv[kSamplePer];
+#pragma unroll
+  for (int q = 0; q < kSamplePer; ++q) {
+    const uint32_t i = blockIdx.x * kSampleBlock + q * kSampleThreads + threadIdx.x;
+    kv[q] = i < hp.n_samples ? hp.k0[(unsigned long long)i * n / (unsigned long long)hp.n_samples] : kAbsent;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < kSamplePer; ++q) {
+    const uint32_t k = kv[q];
     if (k == kAbsent) continue;
     uint32_t h = fmix32(k ^ kCntSalt) & (kSampleTab - 1);
     while (true) {  // (at most kSampleBlock < kSampleTab keys)
@@ -146,11 +152,13 @@ __global__ void __launch_bounds__(256) hot_count_hist_kernel(HotParams hp) {
 // first (pass 0: counts >= 4t, pass 1: the rest).  nhot[0] = keys inserted,
 // nhot[1] = their sampled events.
 __global__ void hot_insert_kernel(HotParams hp, int pass) {
-  __shared__ uint32_t thr;
+  __shared__ uint32_t thr, bins[64];
+  if (threadIdx.x < 64) bins[threadIdx.x] = hp.nhot[8 + threadIdx.x];  // (one load each, not 64 in a chain)
+  __syncthreads();
   if (threadIdx.x == 0) {
     const uint32_t want = (uint32_t)hp.slots * 3 / 4;
     uint32_t t = 64, tot = 0;
-    while (t > (uint32_t)kHotMinCount && tot + hp.nhot[8 + t - 1] <= want) tot += hp.nhot[8 + --t];
+    while (t > (uint32_t)kHotMinCount && tot + bins[t - 1] <= want) tot += bins[--t];
     thr = t;  // keys with count >= t (bin t - 1 and below did not fit)
   }
   __syncthreads();
