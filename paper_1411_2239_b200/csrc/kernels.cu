@@ -1803,6 +1803,19 @@ __global__ void __launch_bounds__(256) heavy_nodes_kernel(HeavyParams h, int l) 
   }
 }
 
+// ----------------------------------------------- per-verify reset
+// the accumulators (offline), the bound-event counter and the partition totals
+// zeroed in one launch (three memset nodes of the graph otherwise)
+__global__ void __launch_bounds__(1024) reset_kernel(DevAcc *acc, unsigned long long *nvalid, uint32_t *totals, int ntot) {
+  if (acc) {
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(acc);
+    for (int i = threadIdx.x; i < (int)(sizeof(DevAcc) / 8); i += blockDim.x) a[i] = 0;
+  }
+  if (threadIdx.x == 0) *nvalid = 0;
+  if (totals)
+    for (int i = threadIdx.x; i < ntot; i += blockDim.x) totals[i] = 0;
+}
+
 // ----------------------------------------------- finalize
 __global__ void finalize_kernel(const DevProg *prog, const DevAcc *acc, DevOut *out) {
   const int f = threadIdx.x;
@@ -2012,6 +2025,10 @@ cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int nq, int n_sms,
     case 2: return heavy_nq<2>(h, nf, nq, n_sms, L);
     default: return heavy_nq<3>(h, nf, nq, n_sms, L);
   }
+}
+
+cudaError_t launch_reset(DevAcc *acc, unsigned long long *nvalid, uint32_t *totals, int ntot, const Launcher &L) {
+  LTL4C_LAUNCH(kKFinalize, reset_kernel<<<1, 1024, 0, L.stream>>>(acc, nvalid, totals, ntot));
 }
 
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L) {

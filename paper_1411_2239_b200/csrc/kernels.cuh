@@ -234,6 +234,8 @@ cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {wa
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);
+// zero acc (if set), *nvalid and totals[0 .. ntot) (if set) in one launch
+cudaError_t launch_reset(DevAcc *acc, unsigned long long *nvalid, uint32_t *totals, int ntot, const Launcher &L);
 // K = 1 offline units: segmented map scans through warp tables (seg.cu)
 cudaError_t launch_bucket_seg(const BucketParams &p, int nq, int nf, uint32_t grid, const Launcher &L);
 int bucket_seg_ctas_per_sm(int nq);

@@ -434,9 +434,13 @@ struct Plan {
   uint32_t NB = 0, n_tiles = 0;
 };
 
-// K = 1 offline batches take the heavy-hitter path (hot.cu) for monitors of <= 8 states
-bool use_hot(const ltl4c_state *st) {
-  return st->hot && st->hot_mapk >= 0 && st->prog->n_levels == 1 && !(st->flags & LTL4C_STATE_ONLINE);
+// K = 1 offline batches of >= kHotMinBatch events take the heavy-hitter path
+// (hot.cu) for monitors of <= 8 states (below that the batch is launch-bound and
+// the sampling kernels are pure overhead)
+constexpr uint64_t kHotMinBatch = 1u << 17;  // (C1 sweep: 2^16 faster without, 2^17 with)
+bool use_hot(const ltl4c_state *st, uint64_t N) {
+  return st->hot && st->hot_mapk >= 0 && st->prog->n_levels == 1 && !(st->flags & LTL4C_STATE_ONLINE) &&
+         N >= kHotMinBatch;
 }
 // hot_compose chunks: one per warp of the resident grid, multiples of 512 events
 uint64_t hot_chunk_ev(const ltl4c_state *st, uint64_t N) {
@@ -473,7 +477,7 @@ ltl4c_status plan_batch(ltl4c_state *st, uint64_t N, Plan *pl) {
   CU(st->unit_start.ensure(N / kUnitTarget + 4));
   if (K == 1) CU(st->unit_start2.ensure(N / st->seg_unit + 4));
   if (K == 1) CU(st->coarse_off.ensure(2 * ((1u << kCoarseBits) + 1)));  // offsets | order
-  if (use_hot(st)) {
+  if (use_hot(st, N)) {
     const uint64_t nch = (N + hot_chunk_ev(st, N) - 1) / hot_chunk_ev(st, N);
     CU(st->hot_cnt.ensure(2 * (size_t)kHotCountCap));
     CU(st->hot_tab.ensure(hot_slots(st->hot_mapk) + 72));  // slot keys, nhot + count bins
@@ -544,10 +548,9 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
   const ltl4c_program *prog = st->prog;
   const int K = (int)prog->n_levels;
   const bool online = st->flags & LTL4C_STATE_ONLINE;
-  if (!online && zero_acc) CU(cudaMemsetAsync(st->d_acc.p, 0, sizeof(DevAcc), s));
-  CU(cudaMemsetAsync(st->d_nvalid.p, 0, sizeof(unsigned long long), s));
+  CU(launch_reset(!online && zero_acc ? st->d_acc.p : nullptr, st->d_nvalid.p, plan.N > 0 ? st->totals.p : nullptr,
+                  kMaxPasses * kMaxDigits + 16, L));
   if (plan.N > 0) {
-    CU(cudaMemsetAsync(st->totals.p, 0, sizeof(uint32_t) * (kMaxPasses * kMaxDigits + 16), s));
     PartPlan pl{};
     for (int l = 0; l < K; ++l) {
       pl.in_key[l] = keys[l];
@@ -581,7 +584,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     pl.nvalid = st->d_nvalid.p;
     pl.acc = st->d_acc.p;
     HotParams hp{};
-    const bool hot = use_hot(st);
+    const bool hot = use_hot(st, plan.N);
     if (hot) {
       // heavy hitters: sampled, composed where they lie; the rest, gathered into a
       // dense stream (bufkey[1] / buflet[1], free until pass 1), is partitioned
