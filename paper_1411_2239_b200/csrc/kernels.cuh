@@ -165,6 +165,7 @@ struct BucketParams {
   uint32_t unit_target;                 // events per unit (unit_start's target)
   const uint32_t *gate;                 // K = 1 hot batches: the kernel runs iff (*gate != 0) == gate_want
   int gate_want;
+  const uint32_t *coarse_hist;          // one-pass mode: the first pass's digit totals (coarse bucket sizes)
   const unsigned long long *nvalid;     // bound events (device): units past nvalid / kUnitTarget + 1 are empty
   const DevProg *prog;
   DevAcc *acc;
@@ -218,7 +219,7 @@ cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L,
-                                 const uint32_t *gate = nullptr, int want = 0, int coarse_bits = 0);
+                                 const uint32_t *gate = nullptr, int want = 0);
 cudaError_t launch_bucket_fast(const BucketParams &p, int K, int nf, int n_sms, const Launcher &L);
 cudaError_t launch_unit_start(const uint32_t *off, uint32_t nb, uint32_t *ustart, uint32_t n_units, const Launcher &L,
                               uint32_t target = kUnitTarget, const uint32_t *gate = nullptr, int want = 0);

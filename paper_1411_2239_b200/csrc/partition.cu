@@ -439,17 +439,16 @@ cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L) 
   }
 }
 
-// coarse_bits > 0: the offsets of the first pass's digits (bits [lo[0], lo[0] +
-// width[0]) of the bucket id) in the first pass's output -- the one-pass mode of
-// a K = 1 hot batch (gate = the hot-key count: this launch runs iff (*gate != 0) == want)
+// gate: the launch runs iff (*gate != 0) == want (a K = 1 hot batch: the one-pass
+// mode's coarse offsets are the first pass's digit totals, coarse_order_kernel)
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L,
-                                 const uint32_t *gate, int want, int coarse_bits) {
-  const uint32_t *k0 = coarse_bits ? p.hcol[0] : p.hcol[(p.passes - 1) & 1];
+                                 const uint32_t *gate, int want) {
+  const uint32_t *k0 = p.hcol[(p.passes - 1) & 1];
   int shift = 0;
   uint32_t mask = 0;
   if (p.bits > 0) {
-    shift = 32 - p.bits + (coarse_bits ? p.lo[0] : 0);
-    mask = coarse_bits ? (1u << coarse_bits) - 1u : (p.bits >= 32 ? 0xFFFFFFFFu : (1u << p.bits) - 1u);
+    shift = 32 - p.bits;
+    mask = p.bits >= 32 ? 0xFFFFFFFFu : (1u << p.bits) - 1u;
   }
   const unsigned long long want_t = (p.n / kBoundsPer + 1 + 255) / 256;
   const unsigned grid = (unsigned)(want_t > 148 * 16 ? 148 * 16 : want_t);

@@ -529,6 +529,7 @@ BucketParams coarse_params(ltl4c_state *st, const Plan &pl, const BucketParams &
   cp.n_buckets = 1u << width;
   cp.bucket_counter = st->totals.p + kMaxPasses * kMaxDigits + 10;
   cp.list = st->coarse_off.p + (1u << kCoarseBits) + 1;  // the buckets, largest first (coarse_order)
+  cp.coarse_hist = st->totals.p;                          // (pass 0's digit totals: coarse_order writes the offsets)
   return cp;
 }
 
@@ -640,7 +641,6 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     }
     if (hot) CU(launch_hot_finish(hp, L));
     CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, one, 0));
-    if (onepass) CU(launch_bucket_bounds(pl, st->coarse_off.p, 1u << pl.width[0], L, one, 1, pl.width[0]));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
       // a warp per unit (<= kWarpCap events); buckets above that go to the same

@@ -473,15 +473,41 @@ __global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(Buc
     if (s.sacc[i]) atomicAdd(&p.acc->hist[i / 6][1][i % 6], (unsigned long long)s.sacc[i]);
 }
 
-// the coarse buckets in decreasing size (one CTA, bitonic sort of (size, id)): CTAs
-// take the largest first, so the last wave holds the small ones
-__global__ void __launch_bounds__(1024) coarse_order_kernel(const uint32_t *off, uint32_t nb, uint32_t *order,
-                                                            const uint32_t *gate) {
+// the coarse buckets' offsets and their order by decreasing size (one CTA).  A
+// coarse bucket is a digit of the first partition pass, so its size is that
+// digit's total (hist, from part_scan) and the offsets are their exclusive scan
+// (no pass over the events); then a bitonic sort of (size, id): CTAs take the
+// largest first, so the last wave holds the small ones
+__global__ void __launch_bounds__(1024) coarse_order_kernel(const uint32_t *hist, uint32_t *off, uint32_t nb,
+                                                            uint32_t *order, const uint32_t *gate) {
   __shared__ unsigned long long v[1024];
+  __shared__ uint32_t wt[32];
   if (gate && *gate == 0) return;
-  const uint32_t t = threadIdx.x;
+  const uint32_t t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const uint32_t c = t < nb ? hist[t] : 0u;
+  uint32_t inc = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) wt[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = wt[lane];
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, d);
+      if (lane >= d) w += y;
+    }
+    wt[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t ex = inc - c + (wid ? wt[wid - 1] : 0u);
+  if (t < nb) off[t] = ex;
+  if (t == nb - 1) off[nb] = ex + c;
   // key: larger size first, then smaller id (ascending sort of ~size << 32 | id)
-  v[t] = t < nb ? ((unsigned long long)(~(off[t + 1] - off[t])) << 32 | t) : ~0ull;
+  v[t] = t < nb ? ((unsigned long long)(~c) << 32 | t) : ~0ull;
   __syncthreads();
   for (uint32_t k = 2; k <= 1024; k <<= 1)
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
@@ -560,7 +586,8 @@ static cudaError_t coarse_launch(const BucketParams &p, uint32_t grid, const Lau
 cudaError_t launch_bucket_coarse(const BucketParams &p, int nf, uint32_t grid, const Launcher &L) {
   if (p.list) {
     if (L.before) L.before(L.ctx, kKBucketWarp);
-    coarse_order_kernel<<<1, 1024, 0, L.stream>>>(p.bucket_off, p.n_buckets, const_cast<uint32_t *>(p.list), p.gate);
+    coarse_order_kernel<<<1, 1024, 0, L.stream>>>(p.coarse_hist, const_cast<uint32_t *>(p.bucket_off), p.n_buckets,
+                                                  const_cast<uint32_t *>(p.list), p.gate);
     if (L.after) L.after(L.ctx, kKBucketWarp);
   }
   switch (nf) {
