@@ -430,15 +430,48 @@ struct alignas(16) WarpTab {
   uint16_t nlist[NL][NS];
   uint16_t npar[NL][NS];                // parent slot (depth l - 1), l >= 2
   uint32_t ncnt[4];                     // claimed node slots per level
+  alignas(8) unsigned long long mbar;   // staging barrier (stage_bulk)
 };
 
-__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+// TMA bulk staging of a work unit into warp-private shared memory: lane 0 arms
+// the warp's mbarrier with the byte count and issues one cp.async.bulk (global ->
+// shared, UBLKCP) per key column and one for the letters; every lane then waits on
+// the barrier's phase (complete_tx).  Sources are the 16-byte aligned addresses at
+// or below the unit's first event: event i lands at key[k][i + (start & 3)] and
+// let[i + (start & 15)]; the buffers hold the rounded-up sizes.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *mb) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n"
+               "fence.mbarrier_init.release.cluster;" ::"r"(smem_u32(mb)) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+__device__ __forceinline__ void mbar_wait(unsigned long long *mb, uint32_t parity) {
+  asm volatile("{\n .reg .pred p;\n"
+               "LTL4C_WAIT_%=:\n"
+               " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+               " @!p bra LTL4C_WAIT_%=;\n}" ::"r"(smem_u32(mb)), "r"(parity) : "memory");
 }
+template <int K>
+__device__ __forceinline__ void stage_bulk(uint32_t *key0, int row, uint8_t *let, const uint32_t *const *gkey,
+                                           const uint8_t *glet, uint32_t start, uint32_t cnt,
+                                           unsigned long long *mbar, uint32_t &parity) {
+  __syncwarp();  // every lane is done with the previous unit's staged data
+  if ((threadIdx.x & 31) == 0) {
+    const uint32_t koff = start & 3u, loff = start & 15u;
+    const uint32_t kb = ((koff + cnt) * 4u + 15u) & ~15u, lb = (loff + cnt + 15u) & ~15u;
+    const uint32_t mb = smem_u32(mbar);
+    asm volatile("fence.proxy.async.shared::cta;\n"
+                 "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(K * kb + lb) : "memory");
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(key0 + k * row)), "l"(gkey[k] + (start - koff)), "r"(kb), "r"(mb) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_u32(let)), "l"(glet + (start - loff)), "r"(lb), "r"(mb) : "memory");
+  }
+  mbar_wait(mbar, parity);
+  parity ^= 1u;
+}
+
 // TMA bulk prefetch of [p, p + bytes) into L2 (16-byte granules)
 __device__ __forceinline__ void bulk_prefetch_l2(const void *p, uint32_t bytes) {
   const uintptr_t a = (uintptr_t)p & ~uintptr_t(15);
@@ -510,6 +543,8 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
   for (int i = lane; i < Tab::NL * Tab::NS; i += 32) (&w.ntag[0][0])[i] = 0;
   for (int i = lane; i < NF * 6; i += 32) w.pleaf[i] = 0;
+  if (lane == 0) mbar_init(&w.mbar);
+  uint32_t mpar = 0;  // phase parity of w.mbar
   __syncthreads();
   const uint32_t q0 = prog->q0;
   const uint32_t node_limit = Tab::NSL / 2;
@@ -598,19 +633,9 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
           ep = 1;
         }
         if (lane < 4) w.ncnt[lane] = 0;
-        // stage the unit (cp.async, 16-byte chunks from 16-byte aligned addresses)
+        // stage the unit (TMA bulk copies, one per column)
         const uint32_t koff = start & 3u, loff = start & 15u;
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-          const uint32_t *g = p.key[k] + (start - koff);
-          for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
-        }
-        {
-          const uint8_t *g = p.let + (start - loff);
-          for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
-        }
-        cp_async_wait_all();
-        __syncwarp();
+        stage_bulk<K>(&w.key[0][0], CAP + 4, w.let, p.key, p.let, start, cnt, &w.mbar, mpar);
         const uint32_t *kb[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
@@ -932,6 +957,7 @@ struct alignas(16) OnlineTab {
   uint16_t llist[CAP];
   uint32_t tstage[CAP];                 // nodes touched first by this chunk (appended together)
   uint32_t tn;
+  alignas(8) unsigned long long mbar;   // staging barrier (stage_bulk)
 };
 
 // node of depth l (keys k[0..l-1]) in the carried tables; a new node starts with
@@ -975,6 +1001,8 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
     slab[i] = prog->lab[i / kMaxStates][i % kMaxStates];
   for (int i = threadIdx.x; i < kMaxFormulas * (kMaxLevels + 1) * 6; i += blockDim.x) sacc[i] = 0;
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+  if (lane == 0) mbar_init(&w.mbar);
+  uint32_t mpar = 0;  // phase parity of w.mbar
   __syncthreads();
   const uint32_t q0 = prog->q0;
   uint32_t newleaves = 0;  // leaves this lane inserted in the carried table
@@ -1015,17 +1043,7 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
         ep = 1;
       }
       const uint32_t koff = start & 3u, loff = start & 15u;
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const uint32_t *g = p.key[k] + (start - koff);
-        for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
-      }
-      {
-        const uint8_t *g = p.let + (start - loff);
-        for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
-      }
-      cp_async_wait_all();
-      __syncwarp();
+      stage_bulk<K>(&w.key[0][0], Tab::CAP + 4, w.let, p.key, p.let, start, cnt, &w.mbar, mpar);
       const uint32_t *kb[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];
@@ -1338,6 +1356,7 @@ struct alignas(16) SegTab {
   uint32_t ltag[LS];
   unsigned long long lmap[LS];
   uint16_t llist[kSegW];
+  alignas(8) unsigned long long mbar;   // staging barrier (stage_bulk)
 };
 
 template <int K, int NQB>
@@ -1351,6 +1370,8 @@ __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
   Tab &w = reinterpret_cast<Tab *>(smem_raw + 8 * kMaxLetters)[wid];
   for (int i = threadIdx.x; i < A; i += blockDim.x) smap[i] = prog->map[i];
   for (int i = lane; i < Tab::LS; i += 32) w.ltag[i] = 0;
+  if (lane == 0) mbar_init(&w.mbar);
+  uint32_t mpar = 0;  // phase parity of w.mbar
   __syncthreads();
   const DevTables &T = h.tab;
   unsigned long long ident = 0;
@@ -1379,17 +1400,7 @@ __global__ void __launch_bounds__(256) heavy_segw_kernel(HeavyParams h) {
       ep = 1;
     }
     const uint32_t koff = start & 3u, loff = start & 15u;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const uint32_t *g = h.key[k] + (start - koff);
-      for (uint32_t c = lane; 4 * c < koff + cnt; c += 32) cp_async16(&w.key[k][4 * c], g + 4 * c);
-    }
-    {
-      const uint8_t *g = h.let + (start - loff);
-      for (uint32_t c = lane; 16 * c < loff + cnt; c += 32) cp_async16(&w.let[16 * c], g + 16 * c);
-    }
-    cp_async_wait_all();
-    __syncwarp();
+    stage_bulk<K>(&w.key[0][0], kSegW + 4, w.let, h.key, h.let, start, cnt, &w.mbar, mpar);
     const uint32_t *kb[K];
 #pragma unroll
     for (int k = 0; k < K; ++k) kb[k] = &w.key[k][koff];

@@ -6,8 +6,11 @@
 
 namespace ltl4c {
 
-constexpr int kTileEv = 4096;        // events per partition tile
-constexpr int kPartThreads = 512;    // 16 warps x 8 rounds x 32 lanes
+#ifndef LTL4C_PART_THREADS
+#define LTL4C_PART_THREADS 512
+#endif
+constexpr int kPartThreads = LTL4C_PART_THREADS;  // partition CTA: 16 warps (or 32)
+constexpr int kTileEv = 8 * kPartThreads;         // events per partition tile: 8 rounds x 32 lanes per warp
 constexpr int kMaxDigitBits = 9;     // <= 512 digits per stable partition pass
 constexpr int kMaxDigits = 1 << kMaxDigitBits;
 constexpr int kMaxPasses = 3;        // bucket bits <= 27

@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kScanThreads) part_scan_kernel(PartPlan pl, in
   if (threadIdx.x == 0) pl.digit_hist[pass * kMaxDigits + blockIdx.x] = carry;
 }
 
-static_assert(kPartThreads == kMaxDigits, "one partition thread per digit");
+static_assert(kPartThreads >= kMaxDigits / 2 && kPartThreads <= 1024, "two digits per thread of the first half");
 
 template <int K>
 struct SweepSmem {
@@ -327,7 +327,7 @@ __device__ __forceinline__ void scatter_tile(const PartPlan &pl, int pass, Sweep
 }
 
 template <int K, bool kDeep, bool kFirst>
-__global__ void __launch_bounds__(kPartThreads, 2) part_scatter_kernel(PartPlan pl, int pass) {
+__global__ void __launch_bounds__(kPartThreads, 1024 / kPartThreads) part_scatter_kernel(PartPlan pl, int pass) {
   extern __shared__ __align__(16) uint8_t raw[];
   SweepSmem<K> &s = *reinterpret_cast<SweepSmem<K> *>(raw);
   if (pass_skipped(pl, pass)) return;
