@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(Buc
     const uint32_t per = ((s1 - s0 + kCoarseWarps - 1) / kCoarseWarps + 31) & ~31u;
     const uint32_t w0 = min(s1, s0 + wid * per), w1 = min(s1, w0 + per);
     for (uint32_t base = w0; base < w1; base += 32 * kSegRounds) {
-      if (*(volatile uint32_t *)&s.ovf) break;  // (warp-uniform)
+      if (__any_sync(0xffffffffu, *(volatile uint32_t *)&s.ovf != 0)) break;
       uint32_t kk[kSegRounds];
       uint8_t ll[kSegRounds];
 #pragma unroll
@@ -379,27 +379,29 @@ __global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(Buc
         if (base + 32 * r + lane < w1) {
           uint32_t h = fmix32(k ^ kSegSalt) & (kCoarseSlots - 1);
           const unsigned long long mine = epk | k;
-          while (true) {
+          bad = true;  // (unless found or claimed within one sweep of the table)
+          for (int it = 0; it < kCoarseSlots; ++it) {
             unsigned long long v = s.slot[h];
             if ((v >> 32) != ep) {
               const unsigned long long o = atomicCAS(&s.slot[h], v, mine);
               if (o == v) {
                 const uint32_t x = atomicAdd(&s.ncl, 1u);
-                if (x < (uint32_t)kCoarseClaims) s.list[x] = (uint16_t)h;
-                else bad = true;
+                bad = x >= (uint32_t)kCoarseClaims;
+                if (!bad) s.list[x] = (uint16_t)h;
                 slot = (int)h;
                 break;
               }
               v = o;
             }
-            if (v == mine) { slot = (int)h; break; }
+            if (v == mine) { slot = (int)h; bad = false; break; }
             h = (h + 1) & (kCoarseSlots - 1);
           }
         }
-        if (__any_sync(0xffffffffu, bad)) {
-          if (lane == 0) s.ovf = 1;
-          break;
-        }
+        // too many keys: the bucket goes to the heavy path.  Every warp reads the flag
+        // each round, so no warp keeps claiming slots after the table is over its bound
+        // (and a probe gives up after one sweep of the table)
+        if (bad) s.ovf = 1;
+        if (__any_sync(0xffffffffu, *(volatile uint32_t *)&s.ovf != 0)) break;
         const uint32_t hm = __ballot_sync(0xffffffffu, slot >= 0);
         stage[lane] = ll[r];
         __syncwarp();
