@@ -978,12 +978,13 @@ __device__ __forceinline__ unsigned long long online_node(const OnlineParams &p,
   return s;
 }
 
-__device__ __forceinline__ void online_touch(const OnlineParams &p, int l, unsigned long long s) {
-  if (atomicExch(&p.b.tab.node_aux[l][s], p.bid) != p.bid) p.tlist[l][atomicAdd(&p.tcnt[l], 1u)] = (uint32_t)s;
+__device__ __forceinline__ void online_touch(const OnlineParams &p, uint32_t bid, int l, unsigned long long s) {
+  if (atomicExch(&p.b.tab.node_aux[l][s], bid) != bid) p.tlist[l][atomicAdd(&p.tcnt[l], 1u)] = (uint32_t)s;
 }
 
 template <int K, int NF>
 __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
+  const uint32_t bid = op.bid_dev ? *op.bid_dev : op.bid;  // (the params stay in the constant bank)
   using Tab = OnlineTab<K>;
   constexpr int CAP = Tab::CAP;
   const BucketParams &p = op.b;
@@ -1180,7 +1181,7 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
             pslot = (long long)online_node(op, K - 1, k, &pok);
 #pragma unroll
             for (int x = 0; x < K - 1; ++x) pk[x] = k[x];
-            if (pok && atomicExch(&T.node_aux[K - 1][pslot], op.bid) != op.bid)
+            if (pok && atomicExch(&T.node_aux[K - 1][pslot], bid) != bid)
               w.tstage[atomicAdd(&w.tn, 1u)] = (uint32_t)pslot;  // first touch this batch
           }
           if (pok) {
@@ -1230,6 +1231,7 @@ __global__ void __launch_bounds__(256) online_leaf_kernel(OnlineParams op) {
 // one child of the parent (depth l-1), or of the root's histogram for l = 1
 template <int NF>
 __global__ void __launch_bounds__(256) online_nodes_kernel(OnlineParams op, int l) {
+  const uint32_t bid = op.bid_dev ? *op.bid_dev : op.bid;  // (the params stay in the constant bank)
   __shared__ int sacc[kMaxFormulas * 6];
   const BucketParams &p = op.b;
   const DevTables &T = p.tab;
@@ -1267,7 +1269,7 @@ __global__ void __launch_bounds__(256) online_nodes_kernel(OnlineParams op, int 
       bool ok;
       const unsigned long long ps = online_node(op, l - 1, k, &ok);
       if (!ok) continue;
-      online_touch(op, l - 1, ps);
+      online_touch(op, bid, l - 1, ps);
       uint32_t *ph = T.node_hist[l - 1] + ps * kMaxFormulas * 6;
 #pragma unroll
       for (int f = 0; f < NF; ++f) {
@@ -2036,6 +2038,12 @@ cudaError_t launch_heavy(const HeavyParams &h, int K, int nf, int nq, int n_sms,
     case 2: return heavy_nq<2>(h, nf, nq, n_sms, L);
     default: return heavy_nq<3>(h, nf, nq, n_sms, L);
   }
+}
+
+__global__ void set_u32_kernel(uint32_t *p, uint32_t v) { *p = v; }
+
+cudaError_t launch_set_u32(uint32_t *p, uint32_t v, const Launcher &L) {
+  LTL4C_LAUNCH(kKFinalize, set_u32_kernel<<<1, 1, 0, L.stream>>>(p, v));
 }
 
 cudaError_t launch_reset(DevAcc *acc, unsigned long long *nvalid, uint32_t *totals, int ntot, const Launcher &L) {

@@ -179,6 +179,7 @@ struct BucketParams {
 struct OnlineParams {
   BucketParams b;
   uint32_t bid;                         // batch id (!= 0), the touch mark of this batch
+  const uint32_t *bid_dev;              // if set: the batch id is read here (graph replays: set per batch)
   uint32_t *tlist[kMaxLevels];          // touched node slots per depth (capacity node_cap)
   uint32_t *tcnt;                       // [kMaxLevels] entries in tlist (zeroed per batch)
 };
@@ -238,6 +239,7 @@ cudaError_t online_leaf_config(int K, int nf, int nq, int na, int *cfg);  // {wa
 cudaError_t launch_rehash(const DevTables &from, const DevTables &to, int n_levels, int nf,
                           unsigned long long *overflow, const Launcher &L);
 cudaError_t launch_finalize(const DevProg *prog, const DevAcc *acc, DevOut *out, const Launcher &L);
+cudaError_t launch_set_u32(uint32_t *p, uint32_t v, const Launcher &L);  // *p = v (stream-ordered)
 // zero acc (if set), *nvalid and totals[0 .. ntot) (if set) in one launch
 cudaError_t launch_reset(DevAcc *acc, unsigned long long *nvalid, uint32_t *totals, int ntot, const Launcher &L);
 // K = 1 offline units: segmented map scans through warp tables (seg.cu)

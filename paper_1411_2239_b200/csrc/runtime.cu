@@ -184,8 +184,11 @@ struct ltl4c_state {
   uint64_t known_leaves = 0, known_nodes[kMaxLevels] = {}, known_cum = 0;
   uint32_t batch_id = 0;           // online: touch mark of the current batch
   DevBuf<uint32_t> tlist[kMaxLevels], tcnt;
+  DevBuf<uint32_t> d_bid;          // online: the batch id as the kernels read it (set per batch, graphs replay)
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
+  uint8_t *h_pack = nullptr;       // small host batches: pinned staging block (one H2D copy per verify)
+  DevBuf<uint8_t> d_pack;          //   its device copy (fixed size: the same layout every call)
   Tables tab;
   // multi-GPU (ltl4c_state_comm)
   void *comm = nullptr;
@@ -234,6 +237,7 @@ struct ltl4c_state {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   std::vector<uintptr_t> graph_key;
+  std::vector<uintptr_t> graph_pending;  // online: the last layout run directly (captured if seen again)
   uint64_t graph_kernels = 0;
   uint64_t k_launches_saved[kKNumKernels] = {};
 };
@@ -692,6 +696,7 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
       op.b = bp;
       op.b.warps_per_cta = st->online_cfg[0];
       op.bid = st->batch_id;
+      op.bid_dev = st->d_bid.p;  // (set by the caller before this sequence runs)
       for (int l = 1; l < K; ++l) op.tlist[l] = st->tlist[l].p;
       op.tcnt = st->tcnt.p;
       CU(cudaMemsetAsync(st->tcnt.p, 0, sizeof(uint32_t) * kMaxLevels, s));
@@ -883,6 +888,8 @@ ltl4c_status run_virtual(ltl4c_state *st, const uint32_t *const *keys, const uin
       CU(st->tcnt.ensure(kMaxLevels));
       if (++st->batch_id == 0) st->batch_id = 1;
       st->enq_events += ng;
+      CU(st->d_bid.ensure(1));
+      CU(launch_set_u32(st->d_bid.p, st->batch_id, L));
     }
     Plan plan;
     {
@@ -952,6 +959,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     for (int l = 1; l < K; ++l) CU(st->tlist[l].ensure(st->tab.d.node_cap[l]));
     CU(st->tcnt.ensure(kMaxLevels));
     if (++st->batch_id == 0) st->batch_id = 1;  // wrap: marks of batch 0 never exist
+    CU(st->d_bid.ensure(1));
     st->enq_events += Nloc;
   }
   Plan plan;
@@ -960,6 +968,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     if (r) return r;
   }
   if (comm) {
+    if (online) CU(launch_set_u32(st->d_bid.p, st->batch_id, L));
     ltl4c_status r = enqueue_main(st, plan, lkeys, llet, s, L, false);
     if (r) return r;
     if (!online && Nloc > 0) {
@@ -978,12 +987,25 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     ltl4c_status r3 = reduce_and_finalize(st, s, L);
     if (r3) return r3;
   } else {
-  // Offline batches replay a captured CUDA graph of the launch sequence (one
-  // graph per input pointers / size); profiling runs the sequence directly so
-  // every kernel can be bracketed by events.
-  const bool use_graph = !online && !st->profiling && st->graphs && N > 0;
+  // Batches replay a captured CUDA graph of the launch sequence (one graph per
+  // input pointers / size; online: per carried-table layout too, the batch id is
+  // read from device memory); profiling runs the sequence directly so every kernel
+  // can be bracketed by events; pipelined online batches copy their result to a
+  // per-ticket slot and run the sequence directly.
+  const bool use_graph = (!online || !async_dst) && !st->profiling && st->graphs && N > 0;  // (online: see below)
+  if (online) CU(launch_set_u32(st->d_bid.p, st->batch_id, L));
   if (use_graph) {
-    std::vector<uintptr_t> key = {(uintptr_t)N, (uintptr_t)letters};
+    std::vector<uintptr_t> key = {(uintptr_t)N, (uintptr_t)letters, (uintptr_t)online};
+    if (online) {
+      const DevTables &T = st->tab.d;
+      for (uintptr_t v : {(uintptr_t)T.epoch, (uintptr_t)T.leaf_cap, (uintptr_t)T.leaf_slot, (uintptr_t)T.leaf_state,
+                          (uintptr_t)T.leaf_aux, (uintptr_t)st->tcnt.p, (uintptr_t)st->d_bid.p})
+        key.push_back(v);
+      for (int l = 0; l < kMaxLevels; ++l)
+        for (uintptr_t v : {(uintptr_t)T.node_cap[l], (uintptr_t)T.node_slot[l], (uintptr_t)T.node_hist[l],
+                            (uintptr_t)T.node_verdict[l], (uintptr_t)T.node_aux[l], (uintptr_t)st->tlist[l].p})
+          key.push_back(v);
+    }
     for (int l = 0; l < K; ++l) key.push_back((uintptr_t)keys[l]);
     // the captured launches bake in every buffer pointer: a buffer reallocated by an
     // ungraphed verify in between (profiling, another size) must not be replayed
@@ -1000,6 +1022,14 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
                           (const void *)st->hot_chunk.p, (const void *)st->hot_n.p, (const void *)st->unit_start2.p,
                           (const void *)st->coarse_off.p})
       key.push_back((uintptr_t)b);
+    // online: a stream of batches at new device addresses every call (slices) would be
+    // captured every time; a layout is captured the second time in a row it is seen
+    const bool known = !online || (st->graph_key == key && st->graph_exec) || st->graph_pending == key;
+    if (!known) {
+      st->graph_pending = key;
+      ltl4c_status r = enqueue_main(st, plan, keys, letters, s, L, true, async_dst);
+      if (r) return r;
+    } else {
     if (st->graph_key != key || !st->graph_exec) {
       drop_graph(st);
       if (!st->cap_stream) CU(cudaStreamCreateWithFlags(&st->cap_stream, cudaStreamNonBlocking));
@@ -1023,6 +1053,7 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
     }
     CU(cudaGraphLaunch(st->graph_exec, s));
     st->launches += st->graph_kernels;
+    }
   } else {
     ltl4c_status r = enqueue_main(st, plan, keys, letters, s, L, true, async_dst);
     if (r) return r;
@@ -1055,6 +1086,8 @@ ltl4c_status run_verify(ltl4c_state *st, const ltl4c_batch *b, cudaStream_t s, l
   return LTL4C_OK;
 }
 
+constexpr uint64_t kPackEvents = 1u << 16;  // host batches up to this size take the packed copy
+constexpr size_t kPackBytes = kMaxLevels * 4 * kPackEvents + kPackEvents + 64;
 ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, ltl4c_result *out,
                            bool host, DevOut *async_dst = nullptr) {
   if (!st || !b || (!out && !async_dst)) return fail(LTL4C_E_INVALID, "null argument");
@@ -1078,7 +1111,24 @@ ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, 
   const uint8_t *letters = b->letters;
   for (int l = 0; l < K; ++l) keys[l] = b->keys[l];
   ltl4c_status r = LTL4C_OK;
-  if (host && b->n_events > 0) {
+  const uint64_t n = b->n_events;
+  if (host && n > 0 && n <= kPackEvents) {
+    // a small batch from host memory (e.g. one event of a verdict stream): packed into
+    // one pinned block and copied with one H2D copy into a buffer of fixed address, so
+    // successive calls have the same layout (online: the sequence replays as a graph).
+    // (the previous call's copy has completed: ltl4c_verify_host waits for its result)
+    const size_t kb = (4 * n + 15) & ~size_t(15), total = K * kb + n;
+    if (!st->h_pack && cudaMallocHost((void **)&st->h_pack, kPackBytes) != cudaSuccess) r = fail(LTL4C_E_OOM, "pinned alloc");
+    else if (st->d_pack.ensure(kPackBytes) != cudaSuccess) r = fail(LTL4C_E_OOM, "staging alloc");
+    else {
+      for (int l = 0; l < K; ++l) std::memcpy(st->h_pack + l * kb, b->keys[l], 4 * n);
+      std::memcpy(st->h_pack + K * kb, b->letters, n);
+      if (cudaMemcpyAsync(st->d_pack.p, st->h_pack, total, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        r = fail(LTL4C_E_CUDA, "H2D copy of the batch failed");
+      for (int l = 0; l < K; ++l) keys[l] = reinterpret_cast<const uint32_t *>(st->d_pack.p + l * kb);
+      letters = st->d_pack.p + K * kb;
+    }
+  } else if (host && n > 0) {
     for (int l = 0; l < K && !r; ++l) {
       if (st->hkeys[l].ensure(b->n_events) != cudaSuccess) r = fail(LTL4C_E_OOM, "staging alloc");
       else if (cudaMemcpyAsync(st->hkeys[l].p, b->keys[l], 4 * b->n_events, cudaMemcpyHostToDevice, s) != cudaSuccess)
@@ -1616,6 +1666,7 @@ void ltl4c_state_free(ltl4c_state *st) {
   st->h_cnt.release();
   st->hot_cnt.release();
   st->hot_tab.release();
+  st->d_bid.release();
   st->hot_partial.release();
   st->hot_chunk.release();
   st->unit_start2.release();
@@ -1639,6 +1690,8 @@ void ltl4c_state_free(ltl4c_state *st) {
     if (st->ring_ev[i]) cudaEventDestroy(st->ring_ev[i]);
   if (st->ring_out) cudaFreeHost(st->ring_out);
   if (st->h_out) cudaFreeHost(st->h_out);
+  if (st->h_pack) cudaFreeHost(st->h_pack);
+  st->d_pack.release();
   cudaSetDevice(prev);
   delete st;
 }

@@ -239,3 +239,28 @@ def test_device_ingest_at_bench_size(env):
         assert np.unique(pairs[0]).shape[0] == pairs.shape[1] == np.unique(pairs[1]).shape[0]
     got = prog.state(0).verify(dk, dl)[0]
     _same(got, oracle.run_offline(tr.formula, hk, hl, threads=NPROC), "ingest 2M")
+
+
+def test_online_graph_replay_batches_from_host(env):
+    """Online batches through ltl4c_verify_host (the state's staging buffers: the same
+    layout every call, so the launch sequence is captured as a CUDA graph and replayed,
+    the batch id read from device memory): batch = 1 events, then 50k-event batches
+    whose leaves outgrow the carried tables (a rehash: a new layout, captured again);
+    the carried result equals the oracle on every checked prefix."""
+    ltl4c = env[0]
+    tr = tracegen.login_trace(seed=21, n=1_400_000, users=30_000, p_unauth=0.05)
+    st = ltl4c.compile(tr.formula).state(0, online=True)
+    keys = [np.ascontiguousarray(k) for k in tr.keys]
+    lets = np.ascontiguousarray(tr.letters)
+    pos = 0
+    for _ in range(300):                       # batch = 1
+        got = st.verify_host([k[pos:pos + 1] for k in keys], lets[pos:pos + 1])[0]
+        pos += 1
+    _same(got, oracle.run_offline(tr.formula, [k[:pos] for k in keys], lets[:pos]), pos)
+    b = 50_000
+    checks = {2, 11, 20, 26}
+    for i in range(27):                        # ~1.35M leaves: past the first table size
+        got = st.verify_host([k[pos:pos + b] for k in keys], lets[pos:pos + b])[0]
+        pos += b
+        if i in checks:
+            _same(got, oracle.run_offline(tr.formula, [k[:pos] for k in keys], lets[:pos], threads=NPROC), pos)
