@@ -291,6 +291,17 @@ class DeviceEncoder:
         m = int(n.value)
         return [k[:m] for k in keys], letters[:m]
 
+    def encode_into(self, text, keys, letters, stream=None) -> int:
+        """As encode(), into caller-allocated device buffers (int32 key tensors, a uint8
+        letter tensor; capacity = letters.numel()): no host-side pass over the text and
+        no allocation.  Returns the number of events written."""
+        kp = (ctypes.c_void_p * MAX_LEVELS)(*[k.data_ptr() for k in keys])
+        n = ctypes.c_uint64()
+        _check(_lib.ltl4c_dencode_jsonl(self._h, ctypes.c_void_p(text.data_ptr() if text.numel() else 0),
+                                        text.numel(), kp, ctypes.c_void_p(letters.data_ptr()), letters.numel(),
+                                        ctypes.byref(n), _stream_handle(stream)))
+        return int(n.value)
+
     def values(self, level: int) -> int:
         c = ctypes.c_uint64()
         _check(_lib.ltl4c_dencoder_values(self._h, level, ctypes.byref(c)))

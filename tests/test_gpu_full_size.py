@@ -239,6 +239,13 @@ def test_device_ingest_at_bench_size(env):
         assert np.unique(pairs[0]).shape[0] == pairs.shape[1] == np.unique(pairs[1]).shape[0]
     got = prog.state(0).verify(dk, dl)[0]
     _same(got, oracle.run_offline(tr.formula, hk, hl, threads=NPROC), "ingest 2M")
+    # encode_into (what bench.py times): caller buffers, a fresh encoder -> the same events
+    d_text = torch.frombuffer(bytearray(text.encode()), dtype=torch.uint8).to(dev)
+    ko = [torch.empty(tr.n + 1, dtype=torch.int32, device=dev) for _ in range(2)]
+    lo = torch.empty(tr.n + 1, dtype=torch.uint8, device=dev)
+    m = prog.device_encoder(max_values=1 << 21).encode_into(d_text, ko, lo)
+    assert m == tr.n
+    assert torch.equal(lo[:m], dl) and all(torch.equal(a[:m], b) for a, b in zip(ko, dk))
 
 
 def test_online_graph_replay_batches_from_host(env):
