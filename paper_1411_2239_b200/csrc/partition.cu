@@ -93,8 +93,11 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
 // exclusive scan of counts[d][0..n_tiles) in place (one CTA per digit), totals[d]:
 // thread t owns a contiguous run of the row (all its loads issued at once), one
 // block scan of the run sums
-constexpr int kScanThreads = 256;
-constexpr int kScanPer = 16;  // rows up to 4096 tiles in one sweep (16.7M events)
+#ifndef LTL4C_SCAN_THREADS
+#define LTL4C_SCAN_THREADS 256
+#endif
+constexpr int kScanThreads = LTL4C_SCAN_THREADS;
+constexpr int kScanPer = 16;  // rows up to 16 x kScanThreads tiles in one sweep (256: 4096 tiles, 16.7M events)
 __global__ void __launch_bounds__(kScanThreads) part_scan_kernel(PartPlan pl, int pass) {
   __shared__ uint32_t wt[kScanThreads / 32];
   if (pass_skipped(pl, pass)) return;
