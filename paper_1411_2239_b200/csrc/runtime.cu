@@ -188,6 +188,7 @@ struct ltl4c_state {
   DevBuf<uint32_t> hkeys[kMaxLevels];  // staging for ltl4c_verify_host
   DevBuf<uint8_t> hlet;
   uint8_t *h_pack = nullptr;       // small host batches: pinned staging block (one H2D copy per verify)
+  cudaEvent_t pack_done = nullptr; //   recorded after its copy (the block is not refilled before)
   DevBuf<uint8_t> d_pack;          //   its device copy (fixed size: the same layout every call)
   Tables tab;
   // multi-GPU (ltl4c_state_comm)
@@ -1116,14 +1117,17 @@ ltl4c_status verify_common(ltl4c_state *st, const ltl4c_batch *b, void *stream, 
     // a small batch from host memory (e.g. one event of a verdict stream): packed into
     // one pinned block and copied with one H2D copy into a buffer of fixed address, so
     // successive calls have the same layout (online: the sequence replays as a graph).
-    // (the previous call's copy has completed: ltl4c_verify_host waits for its result)
     const size_t kb = (4 * n + 15) & ~size_t(15), total = K * kb + n;
     if (!st->h_pack && cudaMallocHost((void **)&st->h_pack, kPackBytes) != cudaSuccess) r = fail(LTL4C_E_OOM, "pinned alloc");
     else if (st->d_pack.ensure(kPackBytes) != cudaSuccess) r = fail(LTL4C_E_OOM, "staging alloc");
+    else if (!st->pack_done && cudaEventCreateWithFlags(&st->pack_done, cudaEventDisableTiming) != cudaSuccess)
+      r = fail(LTL4C_E_CUDA, "event create failed");
     else {
+      cudaEventSynchronize(st->pack_done);  // (the previous copy out of the block has completed)
       for (int l = 0; l < K; ++l) std::memcpy(st->h_pack + l * kb, b->keys[l], 4 * n);
       std::memcpy(st->h_pack + K * kb, b->letters, n);
-      if (cudaMemcpyAsync(st->d_pack.p, st->h_pack, total, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      if (cudaMemcpyAsync(st->d_pack.p, st->h_pack, total, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+          cudaEventRecord(st->pack_done, s) != cudaSuccess)
         r = fail(LTL4C_E_CUDA, "H2D copy of the batch failed");
       for (int l = 0; l < K; ++l) keys[l] = reinterpret_cast<const uint32_t *>(st->d_pack.p + l * kb);
       letters = st->d_pack.p + K * kb;
@@ -1691,6 +1695,7 @@ void ltl4c_state_free(ltl4c_state *st) {
   if (st->ring_out) cudaFreeHost(st->ring_out);
   if (st->h_out) cudaFreeHost(st->h_out);
   if (st->h_pack) cudaFreeHost(st->h_pack);
+  if (st->pack_done) cudaEventDestroy(st->pack_done);
   st->d_pack.release();
   cudaSetDevice(prev);
   delete st;
