@@ -52,7 +52,7 @@ def main():
     for name in ("tests.log", "smoke.log", "sanitize_memcheck.log", "sanitize_racecheck.log",
                  "sanitize_synccheck.log", "sanitize_initcheck.log"):
         src = f"{G}/{TAG}_{name}"
-        if os.path.exists(src):
+        if os.path.exists(src) and "closed on this pool" not in open(src, errors="replace").read():
             shutil.copy(src, f"{P}/{TAG}_{name}")
     summary = {}
     for cfg in ("C3", "C2"):

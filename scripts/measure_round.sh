@@ -1,7 +1,8 @@
 #!/bin/bash
 # GPU box: the round's evidence -- parity tests, smoke, bench line (+ reference arm),
 # per-config bench lines, ncu launch list of the bench command, ncu --set full of the
-# top kernels (C3 headline and C2), compute-sanitizer over cases reaching every kernel.
+# top kernels (C3 headline and C2).  compute-sanitizer (scripts/sanitize.sh) runs
+# separately: this pool has closed it.
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-r02}
@@ -21,6 +22,4 @@ timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"ho
   -o gpurun_out/${TAG}_full_C3 -f python scripts/one_verify.py C3 > gpurun_out/${TAG}_ncu_C3.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"bucket_warp|part_scatter" -s 4 -c 4 \
   -o gpurun_out/${TAG}_full_C2 -f python scripts/one_verify.py C2 > gpurun_out/${TAG}_ncu_C2.log 2>&1
-N=40000 bash scripts/sanitize.sh > gpurun_out/${TAG}_sanitize.log 2>&1
-for t in memcheck racecheck synccheck initcheck; do cp gpurun_out/sanitize_$t.log gpurun_out/${TAG}_sanitize_$t.log 2>/dev/null; done
 echo done
