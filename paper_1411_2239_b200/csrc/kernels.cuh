@@ -221,6 +221,11 @@ extern const char *const kKernelNames[kKNumKernels];
 
 cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L);
+// a batch of <= kTinyBatch events as ONE bucket: its bound events compacted in trace
+// order into the final partition buffers, the bucket offsets (all events in bucket 0)
+// and the bound count -- instead of the count / scan / scatter passes and mu
+constexpr int kTinyBatch = 256;
+cudaError_t launch_tiny_stage(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L);
 cudaError_t launch_part_scatter(const PartPlan &p, int pass, const Launcher &L);
 cudaError_t launch_bucket_bounds(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L,
                                  const uint32_t *gate = nullptr, int want = 0);

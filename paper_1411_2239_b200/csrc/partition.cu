@@ -90,6 +90,47 @@ __global__ void __launch_bounds__(kPartThreads) part_count_kernel(PartPlan pl, i
   }
 }
 
+// A tiny batch (<= kTinyBatch events, one CTA): the epsilon filter (Eq. D: an
+// event binds a value vector only if every guard key is present), the bound events
+// compacted in trace order into the final partition buffers as ONE bucket (bucket 0;
+// every later bucket starts at the end), the bound count.  The bucket kernels then
+// see a single unit holding the whole batch in trace order.
+template <int K>
+__global__ void __launch_bounds__(kTinyBatch) tiny_stage_kernel(PartPlan pl, uint32_t *off, uint32_t nb) {
+  __shared__ uint32_t wt[kTinyBatch / 32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t n = (uint32_t)pl.n;
+  uint32_t kv[K];
+  uint8_t let = 0;
+  bool v = (uint32_t)tid < n;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    kv[i] = v ? pl.in_key[i][tid] : kAbsent;
+    v &= kv[i] != kAbsent;
+  }
+  if (v) let = (uint8_t)(pl.in_let[tid] & pl.let_mask);
+  const uint32_t bal = __ballot_sync(0xffffffffu, v);
+  if (lane == 0) wt[wid] = __popc(bal);
+  __syncthreads();
+  uint32_t before = 0, total = 0;
+  for (int w = 0; w < kTinyBatch / 32; ++w) {
+    before += w < wid ? wt[w] : 0u;
+    total += wt[w];
+  }
+  const int fin = (pl.passes - 1) & 1;
+  if (v) {
+    const uint32_t pos = before + __popc(bal & lanemask_lt());
+#pragma unroll
+    for (int i = 0; i < K; ++i) pl.buf_key[fin][i][pos] = kv[i];
+    pl.buf_let[fin][pos] = let;
+  }
+  for (uint32_t c = tid; c <= nb; c += blockDim.x) off[c] = c == 0 ? 0u : total;
+  if (tid == 0) {
+    *pl.nvalid = total;
+    if (total) atomicAdd(&pl.acc->events_bound, (unsigned long long)total);
+  }
+}
+
 // exclusive scan of counts[d][0..n_tiles) in place (one CTA per digit), totals[d]:
 // thread t owns a contiguous run of the row (all its loads issued at once), one
 // block scan of the run sums
@@ -414,6 +455,14 @@ cudaError_t launch_part_count(const PartPlan &p, int pass, const Launcher &L) {
     }
   }
   LTL4C_LAUNCH(kKPartCount, part_count_kernel<1, false, false><<<part_grid(p, 4), kPartThreads, 0, L.stream>>>(p, pass));
+}
+
+cudaError_t launch_tiny_stage(const PartPlan &p, uint32_t *off, uint32_t n_buckets, const Launcher &L) {
+  switch (p.K) {
+    case 1: LTL4C_LAUNCH(kKPartCount, tiny_stage_kernel<1><<<1, kTinyBatch, 0, L.stream>>>(p, off, n_buckets));
+    case 2: LTL4C_LAUNCH(kKPartCount, tiny_stage_kernel<2><<<1, kTinyBatch, 0, L.stream>>>(p, off, n_buckets));
+    default: LTL4C_LAUNCH(kKPartCount, tiny_stage_kernel<3><<<1, kTinyBatch, 0, L.stream>>>(p, off, n_buckets));
+  }
 }
 
 cudaError_t launch_part_scan(const PartPlan &p, int pass, const Launcher &L) {

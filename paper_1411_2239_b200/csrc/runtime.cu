@@ -639,13 +639,18 @@ ltl4c_status enqueue_main(ltl4c_state *st, const Plan &plan, const uint32_t *con
     const bool onepass = hot && st->hot_mapk == 0 && st->coarse && plan.P == 2;
     const uint32_t *one = onepass ? hp.nhot + 3 : nullptr;  // the one-pass flag (device)
     if (onepass) pl.skip_flag = one;
-    for (int pass = 0; pass < plan.P; ++pass) {
-      CU(launch_part_count(pl, pass, L));
-      CU(launch_part_scan(pl, pass, L));
-      CU(launch_part_scatter(pl, pass, L));
+    if (!hot && plan.N <= (uint64_t)kTinyBatch) {
+      // a tiny batch (a verdict stream of single events): one bucket, staged by one CTA
+      CU(launch_tiny_stage(pl, st->bucket_off.p, plan.NB, L));
+    } else {
+      for (int pass = 0; pass < plan.P; ++pass) {
+        CU(launch_part_count(pl, pass, L));
+        CU(launch_part_scan(pl, pass, L));
+        CU(launch_part_scatter(pl, pass, L));
+      }
+      if (hot) CU(launch_hot_finish(hp, L));
+      CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, one, 0));
     }
-    if (hot) CU(launch_hot_finish(hp, L));
-    CU(launch_bucket_bounds(pl, st->bucket_off.p, plan.NB, L, one, 0));
     BucketParams bp = bucket_params(st, plan);
     if (!online) {
       // a warp per unit (<= kWarpCap events); buckets above that go to the same
