@@ -216,6 +216,9 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, LTL4C_HOT_MINB) hot_compose
   using M = typename HM::T;
   constexpr int S = HM::kSlots;
   extern __shared__ __align__(16) uint8_t raw[];
+  // not dense (no key carries enough of the sample): nothing is composed here and the
+  // partition reads the batch itself -- leave before staging any table
+  if (hp.nhot[2] == 0) return;
   HotSmem<MAPK> &s = *reinterpret_cast<HotSmem<MAPK> *>(raw);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const DevProg *prog = hp.prog;
@@ -332,6 +335,7 @@ __global__ void __launch_bounds__(32 * kHotCtaWarps, LTL4C_HOT_MINB) hot_compose
 // exclusive prefix of the chunks' cold counts (one CTA) -> chunk_pre
 __global__ void __launch_bounds__(1024) hot_prefix_kernel(HotParams hp) {
   __shared__ uint32_t wsum[32];
+  if (hp.nhot[2] == 0) return;  // (not dense: no cold runs)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int nc = hp.n_chunks, per = (nc + 1023) / 1024;
   const int c0 = min(nc, tid * per), c1 = min(nc, c0 + per);
@@ -405,6 +409,7 @@ __global__ void __launch_bounds__(1024) hot_finish_kernel(HotParams hp) {
   __shared__ Bm part[32][33];
   __shared__ uint32_t unpack[256];
   __shared__ uint32_t sacc[kMaxFormulas * 6];
+  if (hp.nhot[2] == 0) return;  // (not dense: no hot key was composed)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < kMaxFormulas * 6; i += blockDim.x) sacc[i] = 0;
   if (MAPK == 0)
@@ -414,7 +419,6 @@ __global__ void __launch_bounds__(1024) hot_finish_kernel(HotParams hp) {
       unpack[m] = o;
     }
   __syncthreads();
-  if (hp.nhot[2] == 0) return;
   const DevProg *prog = hp.prog;
   const int slot = blockIdx.x * 32 + tx;
   const int nc = hp.n_chunks, per = (nc + 31) / 32;
