@@ -88,7 +88,10 @@ template <> struct HotMap<1> {
 // a CTA aggregates its kSampleBlock samples in a shared-memory table first, so a
 // hot key costs one global atomic per CTA (not one per sample); a thread's
 // samples are loaded together
-constexpr int kSampleThreads = 256, kSamplePer = 2;
+#ifndef LTL4C_SAMPLE_PER
+#define LTL4C_SAMPLE_PER 2
+#endif
+constexpr int kSampleThreads = 256, kSamplePer = LTL4C_SAMPLE_PER;
 constexpr int kSampleBlock = kSampleThreads * kSamplePer, kSampleTab = 2 * kSampleBlock;
 __global__ void __launch_bounds__(kSampleThreads) hot_sample_kernel(HotParams hp) {
   __shared__ uint32_t tk[kSampleTab], tc[kSampleTab];
