@@ -300,7 +300,10 @@ __global__ void __launch_bounds__(32 * kSegWarps, 4) bucket_seg_kernel(BucketPar
 // grouped by __match_any_sync and their letters applied by the lowest lane in
 // lane order).  A leaf's state is q0 taken through the warps' maps in warp
 // order.  A bucket with more than kCoarseClaims keys goes to the heavy path.
-constexpr int kCoarseWarps = 16;
+#ifndef LTL4C_COARSE_WARPS
+#define LTL4C_COARSE_WARPS 16
+#endif
+constexpr int kCoarseWarps = LTL4C_COARSE_WARPS;
 constexpr int kCoarseSlots = 4096;
 constexpr int kCoarseClaims = 3072;
 struct CoarseSmem {
@@ -315,7 +318,7 @@ struct CoarseSmem {
 };
 
 template <int NF>
-__global__ void __launch_bounds__(32 * kCoarseWarps, 2) bucket_coarse_kernel(BucketParams p) {
+__global__ void __launch_bounds__(32 * kCoarseWarps, 32 / kCoarseWarps) bucket_coarse_kernel(BucketParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   if (p.gate && ((*p.gate != 0) != (p.gate_want != 0))) return;  // (the other mode)
   CoarseSmem &s = *reinterpret_cast<CoarseSmem *>(smem_raw);
