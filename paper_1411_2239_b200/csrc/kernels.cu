@@ -204,11 +204,14 @@ __device__ void order_segments(const Smem &s, int n, int C) {
 template <int NQB>
 __device__ __forceinline__ unsigned long long map_apply_t(unsigned long long g, unsigned long long f) {
   if constexpr (NQB <= 8) {
+    // byte permutes (PRMT): g's 8 nibbles spread to 8 bytes, f's nibbles (images < 8)
+    // are the selectors, the selected bytes packed back to nibbles
     const uint32_t g32 = (uint32_t)g, f32 = (uint32_t)f;
-    uint32_t r = 0;
-#pragma unroll
-    for (int q = 0; q < NQB; ++q) r |= ((g32 >> (4 * ((f32 >> (4 * q)) & 15u))) & 15u) << (4 * q);
-    return r;
+    const uint32_t ge = g32 & 0x0F0F0F0Fu, go = (g32 >> 4) & 0x0F0F0F0Fu;  // nibbles 0,2,4,6 / 1,3,5,7
+    const uint32_t glo = __byte_perm(ge, go, 0x5140), ghi = __byte_perm(ge, go, 0x7362);  // g[0..3], g[4..7]
+    const uint32_t rlo = __byte_perm(glo, ghi, f32 & 0xFFFFu), rhi = __byte_perm(glo, ghi, f32 >> 16);
+    const uint32_t r = __byte_perm(rlo, rhi, 0x6420) | __byte_perm(rlo, rhi, 0x7531) << 4;
+    return NQB == 8 ? r : r & ((1u << (4 * NQB)) - 1u);
   } else {
     unsigned long long r = 0;
 #pragma unroll
