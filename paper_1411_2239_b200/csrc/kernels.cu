@@ -400,6 +400,9 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_fast_kernel(BucketParam
 #ifndef LTL4C_ILP
 #define LTL4C_ILP 4
 #endif
+#ifndef LTL4C_UNIT_BATCH
+#define LTL4C_UNIT_BATCH 1  // units taken per atomic by a warp of bucket_warp
+#endif
 #ifndef LTL4C_STATIC_UNITS
 #define LTL4C_STATIC_UNITS 0
 #endif
@@ -585,7 +588,18 @@ __global__ void __launch_bounds__(256, LTL4C_WARP_MINB) bucket_warp_kernel(Bucke
   const uint32_t sstep = gridDim.x * (blockDim.x >> 5);
   auto take = [&]() { const uint32_t u = snext; snext += sstep; return u; };
 #else
-  auto take = [&]() { uint32_t u = 0; if (lane == 0) u = atomicAdd(p.bucket_counter, 1u); return u; };
+  // dynamic: LTL4C_UNIT_BATCH consecutive units per atomic on the shared counter (lane 0
+  // keeps the rest of its batch)
+  uint32_t bnext = 0, bleft = 0;
+  auto take = [&]() {
+    uint32_t u = 0;
+    if (lane == 0) {
+      if (bleft == 0) { bnext = atomicAdd(p.bucket_counter, (uint32_t)LTL4C_UNIT_BATCH); bleft = LTL4C_UNIT_BATCH; }
+      u = bnext++;
+      --bleft;
+    }
+    return u;
+  };
 #endif
   uint32_t nraw = take();
   uint32_t cu = __shfl_sync(0xffffffffu, nraw, 0);
