@@ -274,3 +274,39 @@ def test_online_graph_replay_batches_from_host(env):
         pos += b
         if i in checks:
             _same(got, oracle.run_offline(tr.formula, [k[:pos] for k in keys], lets[:pos], threads=NPROC), pos)
+
+
+def test_online_graph_replays_across_reset_compact_restore(env):
+    """Online streams through verify_host (graph replays) across the operations that change
+    the carried state under a captured graph: reset (a new epoch), compact (new tables),
+    checkpoint -> restore into the same state and into a fresh one; every result equals
+    the oracle on the stream fed since the last reset."""
+    ltl4c = env[0]
+    tr = tracegen.login_trace(seed=23, n=60_000, users=500, p_unauth=0.05)
+    keys = [np.ascontiguousarray(k) for k in tr.keys]
+    lets = np.ascontiguousarray(tr.letters)
+    prog = ltl4c.compile(tr.formula)
+    b = 2_000
+
+    def feed(st, lo, hi):
+        got = None
+        for p0 in range(lo, hi, b):
+            got = st.verify_host([k[p0:p0 + b] for k in keys], lets[p0:p0 + b])[0]
+        return got
+
+    def want(lo, hi):
+        return oracle.run_offline(tr.formula, [k[lo:hi] for k in keys], lets[lo:hi])
+
+    st = prog.state(0, online=True)
+    _same(feed(st, 0, 20_000), want(0, 20_000), "first 20k")
+    st.reset()
+    _same(feed(st, 0, 10_000), want(0, 10_000), "after reset")
+    st.compact()
+    _same(feed(st, 10_000, 20_000), want(0, 20_000), "after compact")
+    blob = st.checkpoint()
+    _same(feed(st, 20_000, 40_000), want(0, 40_000), "continued")
+    st.restore(blob)
+    _same(feed(st, 20_000, 30_000), want(0, 30_000), "restored in place")
+    st2 = prog.state(0, online=True)
+    st2.restore(blob)
+    _same(feed(st2, 20_000, 60_000), want(0, 60_000), "restored into a fresh state")
