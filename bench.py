@@ -236,6 +236,35 @@ def run_config(name, args, rank, world, local_rank, with_e2e=True, profile=True)
             e2e_ms.append((time.perf_counter() - t0) * 1e3)
         assert r2.verdict == res.verdict
         e2e_total = float(sum(e2e_ms))
+        out["e2e_serial_total_ms"] = e2e_total
+        if world == 1:
+            # the deployment shape of a stream of independent batches: two states on two
+            # streams, stepped from two host threads, so one batch's H2D copy overlaps the
+            # other's verify (every step still copies its inputs and reads its result back)
+            import threading
+            st_h2 = prog.state(local_rank, capacity=n)
+            streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+            states = [st_h, st_h2]
+            for x in range(2):
+                for _ in range(max(1, args.warmup)):
+                    states[x].verify_host(hkeys, hlet, stream=streams[x])
+            torch.cuda.synchronize(dev)
+            got = [None, None]
+
+            def worker(x):
+                for _ in range(x, args.steps, 2):
+                    got[x] = states[x].verify_host(hkeys, hlet, stream=streams[x])[0]
+
+            t0 = time.perf_counter()
+            ths = [threading.Thread(target=worker, args=(x,)) for x in range(2)]
+            for t in ths:
+                t.start()
+            for t in ths:
+                t.join()
+            e2e_total = (time.perf_counter() - t0) * 1e3
+            assert all(g is None or g.verdict == res.verdict for g in got)
+            out["e2e_streams"] = 2
+            del st_h2
         if dist is not None:
             t = torch.tensor([e2e_total], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -318,6 +347,12 @@ def line_for(r, args, world, peak, peak_kind, name):
     if "e2e_total_ms" in r:
         line["e2e"] = {"value": n_total * args.steps / (r["e2e_total_ms"] / 1e3), "unit": UNIT,
                        "h2d_bytes_per_step": r["h2d"] * world, "d2h_bytes_per_step": RESULT_BYTES * world}
+        if "e2e_serial_total_ms" in r:
+            line["e2e"]["serial_value"] = n_total * args.steps / (r["e2e_serial_total_ms"] / 1e3)
+        if r.get("e2e_streams"):
+            line["e2e"]["note"] = ("ltl4c_verify_host on pinned host buffers, two states on two streams stepped "
+                                   "from two host threads (a batch's copy overlaps the other's verify); "
+                                   "serial_value: one call after the other")
     return line
 
 
